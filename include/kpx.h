@@ -1,0 +1,187 @@
+/*
+ * kpx.h -- C ABI of the B200-native Kino-PAX planner (libkpx.so).
+ *
+ * Plain pointers and sizes only; no torch / C++ types cross this boundary.
+ * Every entry point returns 0 on success and a nonzero KPX_E_* code on failure
+ * (never throws); kpx_last_error() gives the message for the calling thread.
+ *
+ * Which reference interface each entry point replaces
+ * (paths relative to /root/reference/pkg/src/kinopax):
+ *
+ *   kpx_propagate_batch      _kernel.propagate_batch           _kernel.pyx:299-379
+ *                            (called by CompiledBackend,       backend.py:77-89)
+ *   kpx_plan_create          KinoPax.__init__                  planner.py:137-172
+ *                            (TreeArena planner.py:54-62, Decomposition arrays decomposition.py:66-74)
+ *   kpx_plan_reset           init_root + make_available        planner.py:169-172
+ *   kpx_plan_run             KinoPax.solve loop                planner.py:271-303
+ *                            (propagate_pass :176, update_estimates_pass :206, update_node_sets_pass :212)
+ *   kpx_plan_snapshot        TreeArena.snapshot                planner.py:92-102
+ *   kpx_plan_regions         Decomposition state / dump_rows   decomposition.py:66-74, 219-234
+ *   kpx_plan_solution        extract_trajectory (chain walk)   planner.py:325-336
+ *   kpx_plan_trace           IterationTrace records            planner.py:121-131, 290-296
+ *   kpx_plan_items           the Batch of the last iteration   backend.py:47-61
+ *   kpx_plan_load            (no reference equivalent: restores a tree + region state; checkpoint/resume)
+ *   kpx_batch_*              run_trials over many seeds/goals  bench.py:106-150, one launch for Q queries
+ *
+ * Threading: a handle is used by one host thread at a time; different handles
+ * are independent.  All work is stream-ordered on the cudaStream_t passed in
+ * (0 = default stream); calls that return results synchronise that stream.
+ */
+#ifndef KPX_H_
+#define KPX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KPX_MAX_DIM 48      /* reference kernel: 16 (_kernel.pyx:66) */
+#define KPX_MAX_CONTROL 24  /* reference kernel: 8  (_kernel.pyx:67) */
+#define KPX_MAX_CHAIN 4096  /* longest root->goal chain kpx_plan_solution returns */
+
+/* model ids 0..2 = _kernel.pyx:88-130; 3 = stacked 3-D double integrators (n = 6k) */
+enum { KPX_MODEL_DI6 = 0, KPX_MODEL_DUBINS6 = 1, KPX_MODEL_QUAD12 = 2, KPX_MODEL_STACKED_DI = 3 };
+/* arithmetic of the integration / collision / grid-mapping path */
+enum { KPX_F64 = 0, KPX_F32 = 1 };
+/* planner status (core.py:86-90) + RUNNING for stepped runs */
+enum { KPX_SOLVED = 0, KPX_TIMEOUT = 1, KPX_CAPACITY_EXHAUSTED = 2, KPX_ERROR = 3, KPX_RUNNING = 4, KPX_STOPPED = 5 };
+/* node tags (planner.py:31-34) */
+enum { KPX_TAG_EMPTY = 0, KPX_TAG_EXPAND = 1, KPX_TAG_OPEN = 2 };
+/* error codes */
+enum { KPX_OK = 0, KPX_E_ARG = 1, KPX_E_CUDA = 2, KPX_E_LIMIT = 3, KPX_E_STATE = 4 };
+
+/* PlanContext (backend.py:27-44) + PlannerConfig (core.py:142-151), flattened. */
+typedef struct kpx_problem {
+    int32_t model_id;   /* KPX_MODEL_* */
+    int32_t n;          /* state dimension */
+    int32_t nu;         /* control dimension */
+    int32_t n_obs;      /* number of AABB obstacles */
+    int32_t subcells;   /* sub-cells per position dimension */
+    int32_t grid_n;     /* grid spans state dims [0, grid_n); reference: grid_n == n */
+    int32_t lambda_max; /* PlannerConfig.lambda_max */
+    int32_t reserved0;
+    int64_t t_e;        /* tree capacity */
+    double t_prop, check_res, epsilon, delta;
+    double control_lo[KPX_MAX_CONTROL], control_hi[KPX_MAX_CONTROL];
+    double state_lo[KPX_MAX_DIM], state_hi[KPX_MAX_DIM];
+    double grid_lo[KPX_MAX_DIM], grid_width[KPX_MAX_DIM];
+    int64_t grid_cells[KPX_MAX_DIM], grid_strides[KPX_MAX_DIM];
+    const double *obs_min; /* host, (n_obs,3) row-major */
+    const double *obs_max; /* host, (n_obs,3) row-major */
+} kpx_problem;
+
+/* PlanStats (core.py:112-117) + device-side accounting. */
+typedef struct kpx_stats {
+    int32_t status;          /* KPX_SOLVED ... */
+    int32_t iterations;
+    int64_t tree_size;
+    int64_t solution_slot;   /* -1 if none */
+    int64_t chain_len;       /* number of segments root->solution */
+    double device_ms;        /* globaltimer: first iteration start -> result written */
+    double reset_ms;         /* globaltimer: in-kernel workspace reset */
+    uint64_t items;          /* extensions attempted (sum over iterations) */
+    uint64_t substeps;       /* RK4 substeps integrated */
+    uint64_t points;         /* collision points tested */
+    uint64_t launches;       /* kernel launches issued by this call */
+} kpx_stats;
+
+/* IterationTrace (planner.py:121-131). */
+typedef struct kpx_trace {
+    int32_t iteration, branching;
+    int64_t ve_size, vo_size, attempted, valid, staged, appended, tree_size;
+    double elapsed_ms;
+} kpx_trace;
+
+typedef struct kpx_plan kpx_plan;
+typedef struct kpx_batch kpx_batch;
+
+const char *kpx_last_error(void);
+int kpx_version(void);
+/* sizeof of an ABI struct as compiled: 0 kpx_problem, 1 kpx_stats, 2 kpx_trace, 3 kpx_query_result (binding self-check) */
+int kpx_struct_size(int which);
+/* SM count / cooperative-residency facts of the current device (for sizing and for bench.py) */
+int kpx_device_info(int device, int32_t *sm_count, int32_t *max_coop_blocks_f32, int32_t *max_coop_blocks_f64);
+
+/*
+ * Drop-in for _kernel.propagate_batch (_kernel.pyx:299): host arrays in, host
+ * arrays out, same layouts and dtypes as the reference's Batch (backend.py:47):
+ * states (rows,n) f64 row-major, e_slots (m) i64 ascending; outputs for
+ * I = m*lam items: valid u8[I] (init 0), region i64[I] (init -1), sub i64[I]
+ * (init 0), end f64[I,n], control f64[I,nu], dt f64[I], accept_u f64[I].
+ * precision KPX_F64 reproduces the reference bit-for-bit for di6 (<=1e-12 for
+ * the trig models); KPX_F32 integrates in float (end within 1e-5 relative).
+ * Optional o_substeps/o_points (i64[I], may be NULL): work counters per item.
+ * Returns KPX_E_LIMIT if n > KPX_MAX_DIM or nu > KPX_MAX_CONTROL (reference: ValueError).
+ */
+int kpx_propagate_batch(const kpx_problem *prob, const double *states, int64_t state_rows,
+                        const int64_t *e_slots, int64_t m, int32_t lam, uint64_t seed, uint64_t iteration,
+                        int32_t precision, uint8_t *o_valid, int64_t *o_region, int64_t *o_sub,
+                        double *o_end, double *o_control, double *o_dt, double *o_accept,
+                        int64_t *o_substeps, int64_t *o_points, double *o_kernel_ms, void *stream);
+
+/*
+ * One planner = one device-resident arena + region state + scratch.
+ * team_ctas: CTAs cooperating on the query; 0 = whole GPU (cooperative launch).
+ */
+int kpx_plan_create(const kpx_problem *prob, int32_t precision, int32_t team_ctas, int32_t device,
+                    kpx_plan **out);
+void kpx_plan_destroy(kpx_plan *p);
+/* new query on the same problem: seed, start state (n), goal (cx,cy,cz,r) */
+int kpx_plan_reset(kpx_plan *p, uint64_t seed, const double *start, const double *goal4);
+/* replace the obstacle set / goal without reallocating (same n_obs capacity or fewer) */
+int kpx_plan_set_obstacles(kpx_plan *p, int32_t n_obs, const double *obs_min, const double *obs_max);
+/*
+ * Run the device-resident loop.  t_max seconds (device clock), max_iters <= 0
+ * means unlimited; lam_override > 0 forces the branching factor (tests);
+ * stop_flag (device pointer to a 32-bit word, may be NULL) is polled once per
+ * iteration -- nonzero stops the run with KPX_STOPPED (OR-parallel race);
+ * peer_flags/n_peers: device-accessible words this run sets to 1 when it solves.
+ */
+int kpx_plan_run(kpx_plan *p, double t_max, int32_t max_iters, int32_t lam_override,
+                 uint32_t *stop_flag, uint32_t *const *peer_flags, int32_t n_peers,
+                 kpx_stats *out, void *stream);
+/* tree in the reference's snapshot layout (planner.py:92): host buffers sized by tree_size */
+int kpx_plan_snapshot(kpx_plan *p, int64_t rows, double *states, int64_t *parent, double *control,
+                      double *dt, uint8_t *tag, int64_t *region);
+/* region state, each array of n_regions (visited: n_regions*subcells^3) elements; any pointer may be NULL */
+int kpx_plan_regions(kpx_plan *p, int64_t *n_valid, int64_t *n_invalid, int64_t *cov, double *free_vol,
+                     double *score, double *p_accept, uint8_t *visited, uint8_t *avail);
+/* solution chain: for each of chain_len segments the start state (n), control (nu), dt, and the slot */
+int kpx_plan_solution(kpx_plan *p, int64_t max_segments, double *seg_start, double *seg_control,
+                      double *seg_dt, int64_t *seg_slot, double *end_state);
+int kpx_plan_trace(kpx_plan *p, int32_t max_records, kpx_trace *out, int32_t *n_records);
+/* the last iteration's per-item results in Batch layout + keep flag and parent slot (debug/parity) */
+int kpx_plan_items(kpx_plan *p, int64_t max_items, int64_t *n_items, uint8_t *valid, int64_t *region,
+                   int64_t *sub, double *end, uint8_t *keep, int64_t *parent_slot);
+/* restore a tree + region state produced elsewhere (checkpoint/resume; parity tests load oracle states) */
+int kpx_plan_load(kpx_plan *p, uint64_t seed, const double *goal4, int32_t iteration, int64_t rows,
+                  const double *states, const int64_t *parent, const double *control, const double *dt,
+                  const uint8_t *tag, const int64_t *region, const int64_t *n_valid,
+                  const int64_t *n_invalid, const int64_t *cov, const double *score, const double *p_accept,
+                  const uint8_t *visited, const uint8_t *avail);
+
+/*
+ * Many independent queries in one persistent launch: n_teams teams of
+ * team_ctas CTAs each pull queries from a device-side queue; every team owns
+ * one workspace.  Results are written per query.
+ */
+typedef struct kpx_query_result {
+    int32_t status, iterations;
+    int64_t tree_size, solution_slot, chain_len;
+    double device_ms;
+    uint64_t items, substeps, points;
+} kpx_query_result;
+
+int kpx_batch_create(const kpx_problem *prob, int32_t precision, int32_t n_teams, int32_t team_ctas,
+                     int32_t max_chain, int32_t device, kpx_batch **out);
+void kpx_batch_destroy(kpx_batch *b);
+/* seeds[Q], starts[Q,n], goals[Q,4] host arrays; chain buffers (may be NULL) sized Q*max_chain */
+int kpx_batch_run(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const double *starts,
+                  const double *goals, double t_max, kpx_query_result *results, double *chain_start,
+                  double *chain_control, double *chain_dt, double *o_kernel_ms, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KPX_H_ */

@@ -1,0 +1,698 @@
+// kpx_api.cu -- the C ABI declared in include/kpx.h.
+//
+// Owns device memory (one slab per handle, carved into the SoA arena, the region
+// state and the per-iteration scratch), stages the few host inputs, launches the
+// persistent planner kernel and copies results back.  No CPU fallback exists:
+// every entry point either runs the CUDA path or returns an error code.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kpx_launch.h"
+
+using namespace kpx;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e__ = (call);                                                                  \
+        if (e__ != cudaSuccess) return fail(KPX_E_CUDA, "%s: %s", #call, cudaGetErrorString(e__)); \
+    } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int check_problem(const kpx_problem* pr) {
+    if (!pr) return fail(KPX_E_ARG, "problem is null");
+    if (pr->n > KPX_MAX_DIM || pr->nu > KPX_MAX_CONTROL)
+        return fail(KPX_E_LIMIT, "state/control dimension exceeds kernel limits");
+    if (pr->n < 3 || pr->nu < 1 || pr->grid_n < 3 || pr->grid_n > pr->n) return fail(KPX_E_ARG, "bad dimensions");
+    if (pr->model_id < 0 || pr->model_id > KPX_MODEL_STACKED_DI) return fail(KPX_E_ARG, "unknown model id");
+    if (pr->n_obs < 0 || (pr->n_obs > 0 && (!pr->obs_min || !pr->obs_max))) return fail(KPX_E_ARG, "bad obstacles");
+    if (pr->subcells < 1 || pr->lambda_max < 1 || pr->t_e < 1) return fail(KPX_E_ARG, "bad configuration");
+    double regions = 1.0;
+    for (int d = 0; d < pr->grid_n; ++d) regions *= (double)pr->grid_cells[d];
+    if (regions * pr->subcells * pr->subcells * pr->subcells >= 2147483646.0)
+        return fail(KPX_E_LIMIT, "regions x sub-cells must stay below 2^31");
+    if (pr->t_e >= (1ll << 30)) return fail(KPX_E_LIMIT, "t_e too large");
+    return KPX_OK;
+}
+
+// obstacles -> device SoA [minx|miny|minz|maxx|maxy|maxz] in the launch precision
+int upload_obstacles(int precision, int n_obs, const double* omin, const double* omax, void* dev, cudaStream_t st) {
+    if (n_obs == 0) return KPX_OK;
+    if (precision == KPX_F64) {
+        std::vector<double> h(6 * (size_t)n_obs);
+        for (int k = 0; k < n_obs; ++k)
+            for (int a = 0; a < 3; ++a) { h[a * n_obs + k] = omin[3 * k + a]; h[(3 + a) * n_obs + k] = omax[3 * k + a]; }
+        CU(cudaMemcpyAsync(dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    } else {
+        std::vector<float> h(6 * (size_t)n_obs);
+        for (int k = 0; k < n_obs; ++k)
+            for (int a = 0; a < 3; ++a) {
+                h[a * n_obs + k] = (float)omin[3 * k + a];
+                h[(3 + a) * n_obs + k] = (float)omax[3 * k + a];
+            }
+        CU(cudaMemcpyAsync(dev, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    return KPX_OK;
+}
+
+struct Carver {
+    size_t off = 0;
+    size_t take(size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; }
+};
+
+}  // namespace
+
+struct kpx_batch {
+    kpx_problem prob;
+    std::vector<double> obs_min, obs_max;
+    int precision = KPX_F64, n_teams = 1, team_ctas = 1, device = 0;
+    int max_chunks = 0, max_trace = 4096, max_chain = KPX_MAX_CHAIN;
+    bool cooperative = false;
+    size_t rs = 8, smem = 0;
+    int cap = 0, cap_pad = 0, regions = 0, subs = 0;
+    char* slab = nullptr;
+    size_t ws_bytes = 0;
+    std::vector<Workspace> ws_host;
+    Workspace* ws_dev = nullptr;
+    void* obs_dev = nullptr;
+    unsigned int* queue_dev = nullptr;
+    QueryIn* q_dev = nullptr;
+    kpx_query_result* r_dev = nullptr;
+    long long q_cap = 0;
+    double *bc_start = nullptr, *bc_ctrl = nullptr, *bc_dt = nullptr;
+    uint32_t** peers_dev = nullptr;
+    int peers_cap = 0;
+    // single-plan state
+    bool fresh = false;      // reset requested, not yet consumed by a run
+    bool loaded = false;
+    QueryIn q_host;
+    unsigned long long launches = 0;
+};
+
+struct kpx_plan { kpx_batch b; };
+
+namespace {
+
+void destroy_batch(kpx_batch& b) {
+    cudaSetDevice(b.device);
+    cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
+    cudaFree(b.r_dev); cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt); cudaFree(b.peers_dev);
+}
+
+int blocks_per_sm(const kpx_batch& b) {
+    return b.precision == KPX_F64 ? plan_blocks_per_sm_f64(b.prob.model_id, b.prob.n, b.smem)
+                                  : plan_blocks_per_sm_f32(b.prob.model_id, b.prob.n, b.smem);
+}
+
+// allocate everything a batch of n_teams workspaces needs
+int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams, int team_ctas, int max_chain,
+               int device) {
+    int rc = check_problem(prob);
+    if (rc) return rc;
+    if (precision != KPX_F64 && precision != KPX_F32) return fail(KPX_E_ARG, "precision must be KPX_F64 or KPX_F32");
+    CU(cudaSetDevice(device));
+    b.device = device;
+    b.prob = *prob;
+    b.obs_min.assign(prob->obs_min, prob->obs_min + 3 * (size_t)prob->n_obs);
+    b.obs_max.assign(prob->obs_max, prob->obs_max + 3 * (size_t)prob->n_obs);
+    b.prob.obs_min = b.obs_min.data(); b.prob.obs_max = b.obs_max.data();
+    b.precision = precision; b.rs = precision == KPX_F64 ? 8 : 4;
+    b.cap = (int)prob->t_e;
+    b.cap_pad = (int)align_up((size_t)b.cap, kChunk) + kChunk;
+    b.max_chunks = b.cap_pad / kChunk + 1;
+    b.max_chain = max_chain > 0 ? max_chain : KPX_MAX_CHAIN;
+    long long regions = 1;
+    for (int d = 0; d < prob->grid_n; ++d) regions *= prob->grid_cells[d];
+    b.regions = (int)regions;
+    b.subs = prob->subcells * prob->subcells * prob->subcells;
+    b.smem = align_up((size_t)(b.max_chunks + 1) * sizeof(int), 16) + 6 * (size_t)std::max(prob->n_obs, 1) * b.rs;
+    if (b.smem > 200 * 1024) return fail(KPX_E_LIMIT, "t_e / obstacle count need more shared memory than one SM has");
+
+    cudaDeviceProp dp;
+    CU(cudaGetDeviceProperties(&dp, device));
+    const int bps = blocks_per_sm(b);
+    if (bps < 1) return fail(KPX_E_ARG, "no kernel for model_id=%d n=%d", prob->model_id, prob->n);
+    const int max_resident = bps * dp.multiProcessorCount;
+    if (team_ctas <= 0) {           // whole GPU on one query
+        n_teams = 1;
+        team_ctas = max_resident;
+    }
+    if (n_teams < 1) return fail(KPX_E_ARG, "n_teams must be >= 1");
+    b.cooperative = team_ctas > 1;
+    if (b.cooperative && (long long)n_teams * team_ctas > max_resident)
+        return fail(KPX_E_LIMIT, "teams of %d CTAs x %d exceed the %d co-resident CTAs of this device", team_ctas,
+                    n_teams, max_resident);
+    b.n_teams = n_teams; b.team_ctas = team_ctas;
+
+    const int n = prob->n, nu = prob->nu;
+    const size_t cp = (size_t)b.cap_pad, R = (size_t)b.regions, pairs = R * (size_t)b.subs;
+    Carver c;
+    struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, it_end,
+                        it_code, it_rank, it_parent, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
+                        ch_dt, ch_slot, ch_end; } o;
+    o.states = c.take(b.rs * n * cp); o.control = c.take(b.rs * nu * cp); o.dt = c.take(b.rs * cp);
+    o.parent = c.take(4 * cp); o.region = c.take(4 * cp); o.tag = c.take(cp);
+    o.n_valid = c.take(4 * R); o.n_invalid = c.take(4 * R); o.cov = c.take(4 * R); o.avail = c.take(4 * R);
+    o.score = c.take(8 * R); o.claim = c.take(4 * (pairs + 4));
+    o.it_end = c.take(b.rs * n * cp); o.it_code = c.take(4 * cp); o.it_rank = c.take(4 * cp); o.it_parent = c.take(4 * cp);
+    o.e_local = c.take(4 * cp); o.cnt_e = c.take(4 * (size_t)b.max_chunks); o.cnt_k = c.take(4 * (size_t)b.max_chunks);
+    o.partial = c.take(8 * (size_t)team_ctas); o.bar = c.take(256); o.ctl = c.take(sizeof(Ctl));
+    o.trace = c.take(sizeof(kpx_trace) * (size_t)b.max_trace);
+    o.ch_start = c.take(8 * (size_t)b.max_chain * n); o.ch_ctrl = c.take(8 * (size_t)b.max_chain * nu);
+    o.ch_dt = c.take(8 * (size_t)b.max_chain); o.ch_slot = c.take(8 * (size_t)b.max_chain); o.ch_end = c.take(8 * n);
+    b.ws_bytes = align_up(c.off, 4096);
+    if (cudaMalloc(&b.slab, b.ws_bytes * (size_t)n_teams) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(KPX_E_CUDA, "cudaMalloc of %.1f MB for %d workspace(s) failed",
+                    (double)b.ws_bytes * n_teams / 1e6, n_teams);
+    }
+    CU(cudaMemset(b.slab, 0, b.ws_bytes * (size_t)n_teams));
+    b.ws_host.resize(n_teams);
+    for (int t = 0; t < n_teams; ++t) {
+        char* s = b.slab + (size_t)t * b.ws_bytes;
+        Workspace& w = b.ws_host[t];
+        w.states = s + o.states; w.control = s + o.control; w.dt = s + o.dt;
+        w.parent = (int*)(s + o.parent); w.region = (int*)(s + o.region); w.tag = (uint8_t*)(s + o.tag);
+        w.n_valid = (int*)(s + o.n_valid); w.n_invalid = (int*)(s + o.n_invalid); w.cov = (int*)(s + o.cov);
+        w.avail_it = (int*)(s + o.avail); w.score = (double*)(s + o.score); w.claim = (uint32_t*)(s + o.claim);
+        w.it_end = s + o.it_end; w.it_code = (uint32_t*)(s + o.it_code); w.it_rank = (int*)(s + o.it_rank);
+        w.it_parent = (int*)(s + o.it_parent); w.e_local = (int*)(s + o.e_local);
+        w.cnt_expand = (int*)(s + o.cnt_e); w.cnt_keep = (int*)(s + o.cnt_k); w.partial = (double*)(s + o.partial);
+        w.bar = (unsigned int*)(s + o.bar); w.ctl = (Ctl*)(s + o.ctl); w.trace = (kpx_trace*)(s + o.trace);
+        w.chain_start = (double*)(s + o.ch_start); w.chain_control = (double*)(s + o.ch_ctrl);
+        w.chain_dt = (double*)(s + o.ch_dt); w.chain_slot = (long long*)(s + o.ch_slot);
+        w.chain_end = (double*)(s + o.ch_end);
+    }
+    CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
+    CU(cudaMemcpy(b.ws_dev, b.ws_host.data(), sizeof(Workspace) * (size_t)n_teams, cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&b.obs_dev, 6 * (size_t)std::max(prob->n_obs, 1) * b.rs));
+    rc = upload_obstacles(precision, prob->n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, 0);
+    if (rc) return rc;
+    CU(cudaMalloc(&b.queue_dev, 256));
+    CU(cudaMemset(b.queue_dev, 0, 256));
+    return KPX_OK;
+}
+
+int ensure_queries(kpx_batch& b, long long q) {
+    if (q <= b.q_cap) return KPX_OK;
+    cudaFree(b.q_dev); cudaFree(b.r_dev);
+    b.q_dev = nullptr; b.r_dev = nullptr;
+    CU(cudaMalloc(&b.q_dev, sizeof(QueryIn) * (size_t)q));
+    CU(cudaMalloc(&b.r_dev, sizeof(kpx_query_result) * (size_t)q));
+    b.q_cap = q;
+    return KPX_OK;
+}
+
+int launch(kpx_batch& b, const PlanLaunch& L, cudaStream_t st) {
+    cudaError_t e = b.precision == KPX_F64 ? launch_plan_f64(L, st) : launch_plan_f32(L, st);
+    if (e != cudaSuccess) return fail(KPX_E_CUDA, "planner kernel launch: %s", cudaGetErrorString(e));
+    ++b.launches;
+    return KPX_OK;
+}
+
+PlanLaunch base_launch(kpx_batch& b) {
+    PlanLaunch L{};
+    L.prob = &b.prob; L.obs_dev = b.obs_dev; L.ws_dev = b.ws_dev; L.n_teams = b.n_teams; L.team_ctas = b.team_ctas;
+    L.max_chunks = b.max_chunks; L.stride = b.cap_pad; L.max_trace = b.max_trace; L.max_chain = b.max_chain; L.smem = b.smem;
+    L.cooperative = b.cooperative;
+    return L;
+}
+
+template <class T>
+int d2h(std::vector<T>& dst, const void* src, size_t count) {
+    dst.resize(count);
+    CU(cudaMemcpy(dst.data(), src, count * sizeof(T), cudaMemcpyDeviceToHost));
+    return KPX_OK;
+}
+
+// SoA device array of `rows` x `dims` reals -> AoS f64 host
+int soa_to_aos(const kpx_batch& b, const void* dev, int dims, long long rows, double* out) {
+    if (rows == 0) return KPX_OK;
+    std::vector<char> h((size_t)rows * b.rs);
+    for (int d = 0; d < dims; ++d) {
+        CU(cudaMemcpy(h.data(), (const char*)dev + (size_t)d * b.cap_pad * b.rs, (size_t)rows * b.rs,
+                      cudaMemcpyDeviceToHost));
+        if (b.rs == 8) { const double* s = (const double*)h.data(); for (long long i = 0; i < rows; ++i) out[i * dims + d] = s[i]; }
+        else { const float* s = (const float*)h.data(); for (long long i = 0; i < rows; ++i) out[i * dims + d] = (double)s[i]; }
+    }
+    return KPX_OK;
+}
+
+int aos_to_soa(const kpx_batch& b, void* dev, int dims, long long rows, const double* in) {
+    if (rows == 0) return KPX_OK;
+    std::vector<char> h((size_t)rows * b.rs);
+    for (int d = 0; d < dims; ++d) {
+        if (b.rs == 8) { double* s = (double*)h.data(); for (long long i = 0; i < rows; ++i) s[i] = in[i * dims + d]; }
+        else { float* s = (float*)h.data(); for (long long i = 0; i < rows; ++i) s[i] = (float)in[i * dims + d]; }
+        CU(cudaMemcpy((char*)dev + (size_t)d * b.cap_pad * b.rs, h.data(), (size_t)rows * b.rs, cudaMemcpyHostToDevice));
+    }
+    return KPX_OK;
+}
+
+int read_ctl(const kpx_batch& b, Ctl* out) {
+    CU(cudaMemcpy(out, b.ws_host[0].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    return KPX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kpx_last_error(void) { return g_err.c_str(); }
+int kpx_version(void) { return 100; }
+int kpx_struct_size(int which) {
+    switch (which) {
+        case 0: return (int)sizeof(kpx_problem);
+        case 1: return (int)sizeof(kpx_stats);
+        case 2: return (int)sizeof(kpx_trace);
+        case 3: return (int)sizeof(kpx_query_result);
+        default: return -1;
+    }
+}
+
+int kpx_device_info(int device, int32_t* sm_count, int32_t* f32_blocks, int32_t* f64_blocks) {
+    cudaDeviceProp dp;
+    CU(cudaGetDeviceProperties(&dp, device));
+    CU(cudaSetDevice(device));
+    if (sm_count) *sm_count = dp.multiProcessorCount;
+    if (f32_blocks) *f32_blocks = plan_blocks_per_sm_f32(KPX_MODEL_DI6, 6, 4096) * dp.multiProcessorCount;
+    if (f64_blocks) *f64_blocks = plan_blocks_per_sm_f64(KPX_MODEL_DI6, 6, 4096) * dp.multiProcessorCount;
+    return KPX_OK;
+}
+
+int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t state_rows, const int64_t* e_slots,
+                        int64_t m, int32_t lam, uint64_t seed, uint64_t iteration, int32_t precision,
+                        uint8_t* o_valid, int64_t* o_region, int64_t* o_sub, double* o_end, double* o_control,
+                        double* o_dt, double* o_accept, int64_t* o_substeps, int64_t* o_points, double* o_kernel_ms,
+                        void* stream) {
+    int rc = check_problem(prob);
+    if (rc) return rc;
+    if (m < 0 || lam < 1 || state_rows < 0) return fail(KPX_E_ARG, "bad batch shape");
+    if (precision != KPX_F64 && precision != KPX_F32) return fail(KPX_E_ARG, "bad precision");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t items = m * lam;
+    if (o_kernel_ms) *o_kernel_ms = 0.0;
+    if (items == 0) return KPX_OK;
+    for (int64_t i = 0; i < m; ++i)
+        if (e_slots[i] < 0 || e_slots[i] >= state_rows) return fail(KPX_E_ARG, "e_slots[%lld] out of range", (long long)i);
+    const int n = prob->n, nu = prob->nu;
+    const size_t rs = precision == KPX_F64 ? 8 : 4;
+    char* slab = nullptr;
+    Carver c;
+    const size_t o_states = c.take(8 * (size_t)state_rows * n), o_slots = c.take(8 * (size_t)m),
+                 o_obs = c.take(6 * (size_t)std::max(prob->n_obs, 1) * rs), o_v = c.take((size_t)items),
+                 o_r = c.take(8 * (size_t)items), o_s = c.take(8 * (size_t)items), o_e = c.take(8 * (size_t)items * n),
+                 o_c = c.take(8 * (size_t)items * nu), o_d = c.take(8 * (size_t)items), o_a = c.take(8 * (size_t)items),
+                 o_ss = c.take(8 * (size_t)items), o_pp = c.take(8 * (size_t)items);
+    if (cudaMalloc(&slab, c.off) != cudaSuccess) { cudaGetLastError(); return fail(KPX_E_CUDA, "cudaMalloc failed"); }
+    struct Guard { char* p; ~Guard() { cudaFree(p); } } guard{slab};
+    CU(cudaMemcpyAsync(slab + o_states, states, 8 * (size_t)state_rows * n, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(slab + o_slots, e_slots, 8 * (size_t)m, cudaMemcpyHostToDevice, st));
+    rc = upload_obstacles(precision, prob->n_obs, prob->obs_min, prob->obs_max, slab + o_obs, st);
+    if (rc) return rc;
+    BatchLaunch L{};
+    L.prob = prob; L.obs_dev = slab + o_obs; L.states_dev = (const double*)(slab + o_states);
+    L.e_slots_dev = (const long long*)(slab + o_slots); L.items = items; L.lam = lam; L.seed = seed;
+    L.iteration = iteration; L.o_valid = (uint8_t*)(slab + o_v); L.o_region = (long long*)(slab + o_r);
+    L.o_sub = (long long*)(slab + o_s); L.o_end = (double*)(slab + o_e); L.o_control = (double*)(slab + o_c);
+    L.o_dt = (double*)(slab + o_d); L.o_accept = (double*)(slab + o_a);
+    L.o_substeps = (long long*)(slab + o_ss); L.o_points = (long long*)(slab + o_pp);
+    L.grid = (int)std::min<int64_t>((items + kBlock - 1) / kBlock, 148 * 16);
+    L.smem = 6 * (size_t)std::max(prob->n_obs, 1) * rs;
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, st));
+    cudaError_t e = precision == KPX_F64 ? launch_batch_f64(L, st) : launch_batch_f32(L, st);
+    if (e != cudaSuccess) return fail(e == cudaErrorInvalidValue ? KPX_E_ARG : KPX_E_CUDA,
+                                      "propagate kernel launch (model_id=%d n=%d): %s", prob->model_id, n,
+                                      cudaGetErrorString(e));
+    CU(cudaEventRecord(e1, st));
+    CU(cudaMemcpyAsync(o_valid, slab + o_v, (size_t)items, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o_region, slab + o_r, 8 * (size_t)items, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o_sub, slab + o_s, 8 * (size_t)items, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o_end, slab + o_e, 8 * (size_t)items * n, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o_control, slab + o_c, 8 * (size_t)items * nu, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o_dt, slab + o_d, 8 * (size_t)items, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(o_accept, slab + o_a, 8 * (size_t)items, cudaMemcpyDeviceToHost, st));
+    if (o_substeps) CU(cudaMemcpyAsync(o_substeps, slab + o_ss, 8 * (size_t)items, cudaMemcpyDeviceToHost, st));
+    if (o_points) CU(cudaMemcpyAsync(o_points, slab + o_pp, 8 * (size_t)items, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (o_kernel_ms) { float ms = 0; CU(cudaEventElapsedTime(&ms, e0, e1)); *o_kernel_ms = ms; }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    return KPX_OK;
+}
+
+// ------------------------------------------------------------------ single plan
+int kpx_plan_create(const kpx_problem* prob, int32_t precision, int32_t team_ctas, int32_t device, kpx_plan** out) {
+    if (!out) return fail(KPX_E_ARG, "out is null");
+    *out = nullptr;
+    kpx_plan* p = new kpx_plan();
+    int rc = init_batch(p->b, prob, precision, 1, team_ctas, KPX_MAX_CHAIN, device);
+    if (rc) { destroy_batch(p->b); delete p; return rc; }
+    rc = ensure_queries(p->b, 1);
+    if (rc) { destroy_batch(p->b); delete p; return rc; }
+    *out = p;
+    return KPX_OK;
+}
+
+void kpx_plan_destroy(kpx_plan* p) {
+    if (!p) return;
+    destroy_batch(p->b);
+    delete p;
+}
+
+int kpx_plan_reset(kpx_plan* p, uint64_t seed, const double* start, const double* goal4) {
+    if (!p || !start || !goal4) return fail(KPX_E_ARG, "null argument");
+    kpx_batch& b = p->b;
+    memset(&b.q_host, 0, sizeof b.q_host);
+    b.q_host.seed = seed;
+    memcpy(b.q_host.start, start, sizeof(double) * b.prob.n);
+    memcpy(b.q_host.goal, goal4, sizeof(double) * 4);
+    b.fresh = true; b.loaded = false;
+    return KPX_OK;
+}
+
+int kpx_plan_set_obstacles(kpx_plan* p, int32_t n_obs, const double* omin, const double* omax) {
+    if (!p) return fail(KPX_E_ARG, "null plan");
+    kpx_batch& b = p->b;
+    if (n_obs < 0 || n_obs > std::max<int>((int)b.obs_min.size() / 3, 1) || (n_obs && (!omin || !omax)))
+        return fail(KPX_E_ARG, "obstacle count exceeds the capacity the plan was created with");
+    CU(cudaSetDevice(b.device));
+    b.prob.n_obs = n_obs;
+    std::copy(omin, omin + 3 * (size_t)n_obs, b.obs_min.begin());
+    std::copy(omax, omax + 3 * (size_t)n_obs, b.obs_max.begin());
+    return upload_obstacles(b.precision, n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, 0);
+}
+
+int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_override, uint32_t* stop_flag,
+                 uint32_t* const* peer_flags, int32_t n_peers, kpx_stats* out, void* stream) {
+    if (!p || !out) return fail(KPX_E_ARG, "null argument");
+    kpx_batch& b = p->b;
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(b.device));
+    if (!b.fresh && !b.loaded && b.launches == 0) return fail(KPX_E_STATE, "kpx_plan_reset or kpx_plan_load first");
+    PlanLaunch L = base_launch(b);
+    L.n_queries = 1; L.queries_dev = b.q_dev; L.results_dev = nullptr; L.queue_dev = nullptr;
+    L.resume = b.fresh ? 0 : 1;
+    L.max_iters = max_iters; L.lam_override = lam_override; L.t_max_s = t_max; L.stop_flag = stop_flag;
+    if (n_peers > 0) {
+        if (n_peers > b.peers_cap) {
+            cudaFree(b.peers_dev);
+            CU(cudaMalloc(&b.peers_dev, sizeof(uint32_t*) * (size_t)n_peers));
+            b.peers_cap = n_peers;
+        }
+        CU(cudaMemcpyAsync(b.peers_dev, peer_flags, sizeof(uint32_t*) * (size_t)n_peers, cudaMemcpyHostToDevice, st));
+        L.peer_flags = b.peers_dev; L.n_peers = n_peers;
+    }
+    const unsigned long long l0 = b.launches;
+    if (b.fresh) CU(cudaMemcpyAsync(b.q_dev, &b.q_host, sizeof(QueryIn), cudaMemcpyHostToDevice, st));
+    int rc = launch(b, L, st);
+    if (rc) return rc;
+    b.fresh = false;
+    Ctl c;
+    CU(cudaMemcpyAsync(&c, b.ws_host[0].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    out->status = c.status; out->iterations = c.iteration; out->tree_size = c.size;
+    out->solution_slot = c.solution_slot; out->chain_len = c.chain_len;
+    out->device_ms = (double)(c.t_end - c.t_reset_done) * 1e-6;
+    out->reset_ms = (double)(c.t_reset_done - c.t_begin) * 1e-6;
+    out->items = c.sum_items; out->substeps = c.sum_substeps; out->points = c.sum_points;
+    out->launches = b.launches - l0;
+    return KPX_OK;
+}
+
+int kpx_plan_snapshot(kpx_plan* p, int64_t rows, double* states, int64_t* parent, double* control, double* dt,
+                      uint8_t* tag, int64_t* region) {
+    if (!p) return fail(KPX_E_ARG, "null plan");
+    kpx_batch& b = p->b;
+    CU(cudaSetDevice(b.device));
+    Ctl c;
+    int rc = read_ctl(b, &c);
+    if (rc) return rc;
+    if (rows > c.size) return fail(KPX_E_ARG, "rows exceeds tree size %d", c.size);
+    const Workspace& w = b.ws_host[0];
+    if (states && (rc = soa_to_aos(b, w.states, b.prob.n, rows, states))) return rc;
+    if (control && (rc = soa_to_aos(b, w.control, b.prob.nu, rows, control))) return rc;
+    if (dt && (rc = soa_to_aos(b, w.dt, 1, rows, dt))) return rc;
+    std::vector<int> tmp;
+    if (parent) { if ((rc = d2h(tmp, w.parent, (size_t)rows))) return rc; for (int64_t i = 0; i < rows; ++i) parent[i] = tmp[i]; }
+    if (region) { if ((rc = d2h(tmp, w.region, (size_t)rows))) return rc; for (int64_t i = 0; i < rows; ++i) region[i] = tmp[i]; }
+    if (tag && rows) CU(cudaMemcpy(tag, w.tag, (size_t)rows, cudaMemcpyDeviceToHost));
+    return KPX_OK;
+}
+
+int kpx_plan_regions(kpx_plan* p, int64_t* n_valid, int64_t* n_invalid, int64_t* cov, double* free_vol, double* score,
+                     double* p_accept, uint8_t* visited, uint8_t* avail) {
+    if (!p) return fail(KPX_E_ARG, "null plan");
+    kpx_batch& b = p->b;
+    CU(cudaSetDevice(b.device));
+    Ctl c;
+    int rc = read_ctl(b, &c);
+    if (rc) return rc;
+    const Workspace& w = b.ws_host[0];
+    const size_t R = (size_t)b.regions;
+    std::vector<int> nv, ni, cv, av;
+    std::vector<double> sc;
+    if ((rc = d2h(nv, w.n_valid, R)) || (rc = d2h(ni, w.n_invalid, R)) || (rc = d2h(cv, w.cov, R)) ||
+        (rc = d2h(av, w.avail_it, R)) || (rc = d2h(sc, w.score, R))) return rc;
+    const double vol = b.prob.grid_width[0] * b.prob.grid_width[1] * b.prob.grid_width[2];
+    const double eps = b.prob.epsilon, delta = b.prob.delta, total = c.total_prev;
+    for (size_t r = 0; r < R; ++r) {
+        const bool est = av[r] != 0 && av[r] <= c.iteration;   // estimated by the last pass
+        if (n_valid) n_valid[r] = nv[r];
+        if (n_invalid) n_invalid[r] = ni[r];
+        if (cov) cov[r] = cv[r];
+        if (avail) avail[r] = av[r] != 0;
+        if (score) score[r] = est ? sc[r] : 0.0;
+        if (free_vol) free_vol[r] = est ? (delta + nv[r]) * vol / (delta + nv[r] + ni[r]) : 0.0;
+        if (p_accept) {
+            double pa = 1.0;
+            if (est) pa = total <= 0.0 ? std::min(1.0, eps) : std::min(1.0, sc[r] / total + eps);
+            p_accept[r] = pa;
+        }
+    }
+    if (visited) {
+        std::vector<uint32_t> cl;
+        if ((rc = d2h(cl, w.claim, R * (size_t)b.subs))) return rc;
+        for (size_t i = 0; i < cl.size(); ++i) visited[i] = cl[i] == kVisited;
+    }
+    return KPX_OK;
+}
+
+int kpx_plan_solution(kpx_plan* p, int64_t max_segments, double* seg_start, double* seg_control, double* seg_dt,
+                      int64_t* seg_slot, double* end_state) {
+    if (!p) return fail(KPX_E_ARG, "null plan");
+    kpx_batch& b = p->b;
+    CU(cudaSetDevice(b.device));
+    Ctl c;
+    int rc = read_ctl(b, &c);
+    if (rc) return rc;
+    if (c.status != KPX_SOLVED) return fail(KPX_E_STATE, "plan is not solved");
+    if (c.chain_len < 0) return fail(KPX_E_LIMIT, "solution chain longer than KPX_MAX_CHAIN");
+    if (c.chain_len > max_segments) return fail(KPX_E_ARG, "need room for %d segments", c.chain_len);
+    const Workspace& w = b.ws_host[0];
+    const size_t L = (size_t)c.chain_len;
+    if (L) {
+        if (seg_start) CU(cudaMemcpy(seg_start, w.chain_start, 8 * L * b.prob.n, cudaMemcpyDeviceToHost));
+        if (seg_control) CU(cudaMemcpy(seg_control, w.chain_control, 8 * L * b.prob.nu, cudaMemcpyDeviceToHost));
+        if (seg_dt) CU(cudaMemcpy(seg_dt, w.chain_dt, 8 * L, cudaMemcpyDeviceToHost));
+        if (seg_slot) CU(cudaMemcpy(seg_slot, w.chain_slot, 8 * L, cudaMemcpyDeviceToHost));
+        if (end_state) CU(cudaMemcpy(end_state, w.chain_end, 8 * (size_t)b.prob.n, cudaMemcpyDeviceToHost));
+    }
+    return KPX_OK;
+}
+
+int kpx_plan_trace(kpx_plan* p, int32_t max_records, kpx_trace* out, int32_t* n_records) {
+    if (!p || !n_records) return fail(KPX_E_ARG, "null argument");
+    kpx_batch& b = p->b;
+    CU(cudaSetDevice(b.device));
+    Ctl c;
+    int rc = read_ctl(b, &c);
+    if (rc) return rc;
+    const int n = std::min(c.n_trace, max_records);
+    if (n > 0 && out) CU(cudaMemcpy(out, b.ws_host[0].trace, sizeof(kpx_trace) * (size_t)n, cudaMemcpyDeviceToHost));
+    *n_records = n;
+    return KPX_OK;
+}
+
+int kpx_plan_items(kpx_plan* p, int64_t max_items, int64_t* n_items, uint8_t* valid, int64_t* region, int64_t* sub,
+                   double* end, uint8_t* keep, int64_t* parent_slot) {
+    if (!p || !n_items) return fail(KPX_E_ARG, "null argument");
+    kpx_batch& b = p->b;
+    CU(cudaSetDevice(b.device));
+    Ctl c;
+    int rc = read_ctl(b, &c);
+    if (rc) return rc;
+    const int64_t I = c.n_items_last;
+    *n_items = I;
+    if (I > max_items) return fail(KPX_E_ARG, "need room for %lld items", (long long)I);
+    if (I == 0) return KPX_OK;
+    const Workspace& w = b.ws_host[0];
+    std::vector<uint32_t> code;
+    std::vector<int> rank, par;
+    if ((rc = d2h(code, w.it_code, (size_t)I)) || (rc = d2h(rank, w.it_rank, (size_t)I)) ||
+        (rc = d2h(par, w.it_parent, (size_t)I))) return rc;
+    std::vector<double> e;
+    if (end) { e.resize((size_t)I * b.prob.n); if ((rc = soa_to_aos(b, w.it_end, b.prob.n, I, e.data()))) return rc; }
+    for (int64_t i = 0; i < I; ++i) {
+        const bool v = code[i] != kItemInvalid;
+        const uint32_t pair = code[i] & ~kItemGoalBit;
+        if (valid) valid[i] = v;
+        if (region) region[i] = v ? (int64_t)(pair / (uint32_t)b.subs) : -1;
+        if (sub) sub[i] = v ? (int64_t)(pair % (uint32_t)b.subs) : 0;
+        if (keep) keep[i] = v && rank[i] >= 0;
+        if (parent_slot) parent_slot[i] = par[i];
+        if (end) for (int d = 0; d < b.prob.n; ++d) end[i * b.prob.n + d] = v ? e[(size_t)i * b.prob.n + d] : 0.0;
+    }
+    return KPX_OK;
+}
+
+int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t iteration, int64_t rows, const double* states,
+                  const int64_t* parent, const double* control, const double* dt, const uint8_t* tag,
+                  const int64_t* region, const int64_t* n_valid, const int64_t* n_invalid, const int64_t* cov,
+                  const double* score, const double* p_accept, const uint8_t* visited, const uint8_t* avail) {
+    if (!p || !goal4 || !states || !parent || !control || !dt || !tag || !region || !n_valid || !n_invalid || !cov ||
+        !score || !p_accept || !visited || !avail) return fail(KPX_E_ARG, "null argument");
+    kpx_batch& b = p->b;
+    if (rows < 1 || rows > b.cap) return fail(KPX_E_ARG, "rows out of range");
+    CU(cudaSetDevice(b.device));
+    const Workspace& w = b.ws_host[0];
+    int rc;
+    if ((rc = aos_to_soa(b, w.states, b.prob.n, rows, states)) || (rc = aos_to_soa(b, w.control, b.prob.nu, rows, control)) ||
+        (rc = aos_to_soa(b, w.dt, 1, rows, dt))) return rc;
+    std::vector<int> tmp((size_t)rows);
+    for (int64_t i = 0; i < rows; ++i) tmp[i] = (int)parent[i];
+    CU(cudaMemcpy(w.parent, tmp.data(), 4 * (size_t)rows, cudaMemcpyHostToDevice));
+    for (int64_t i = 0; i < rows; ++i) tmp[i] = (int)region[i];
+    CU(cudaMemcpy(w.region, tmp.data(), 4 * (size_t)rows, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(w.tag, tag, (size_t)rows, cudaMemcpyHostToDevice));
+    const size_t R = (size_t)b.regions;
+    std::vector<int> a(R), x(R);
+    double total = 0.0;
+    for (size_t r = 0; r < R; ++r) {
+        // score > 0 <=> the region has been through an estimate pass; regions made available by the
+        // most recent append are estimated from the next iteration on (planner.py:246)
+        a[r] = avail[r] ? (score[r] > 0.0 ? 1 : iteration + 1) : 0;
+        if (avail[r] && score[r] > 0.0) total += score[r];
+    }
+    CU(cudaMemcpy(w.avail_it, a.data(), 4 * R, cudaMemcpyHostToDevice));
+    for (size_t r = 0; r < R; ++r) x[r] = (int)n_valid[r];
+    CU(cudaMemcpy(w.n_valid, x.data(), 4 * R, cudaMemcpyHostToDevice));
+    for (size_t r = 0; r < R; ++r) x[r] = (int)n_invalid[r];
+    CU(cudaMemcpy(w.n_invalid, x.data(), 4 * R, cudaMemcpyHostToDevice));
+    for (size_t r = 0; r < R; ++r) x[r] = (int)cov[r];
+    CU(cudaMemcpy(w.cov, x.data(), 4 * R, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(w.score, score, 8 * R, cudaMemcpyHostToDevice));
+    std::vector<uint32_t> cl(R * (size_t)b.subs);
+    for (size_t i = 0; i < cl.size(); ++i) cl[i] = visited[i] ? kVisited : kUnclaimed;
+    CU(cudaMemcpy(w.claim, cl.data(), 4 * cl.size(), cudaMemcpyHostToDevice));
+    // EXPAND lists per chunk
+    std::vector<int> e_local((size_t)b.cap_pad, 0), cnt((size_t)b.max_chunks, 0);
+    int ve = 0;
+    for (int64_t s = 0; s < rows; ++s)
+        if (tag[s] == KPX_TAG_EXPAND) { const int c = (int)(s / kChunk); e_local[(size_t)c * kChunk + cnt[c]++] = (int)s; ++ve; }
+    CU(cudaMemcpy(w.e_local, e_local.data(), 4 * e_local.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(w.cnt_expand, cnt.data(), 4 * cnt.size(), cudaMemcpyHostToDevice));
+    Ctl c;
+    memset(&c, 0, sizeof c);
+    c.size = (int)rows; c.iteration = iteration; c.status = KPX_RUNNING; c.solution_slot = -1; c.total_prev = total;
+    c.ve = ve; c.first_hit_w = 0x7fffffff; c.rescue_slot = 0x7fffffff;
+    CU(cudaMemcpy(w.ctl, &c, sizeof c, cudaMemcpyHostToDevice));
+    // t_reset_done stays 0: the first resumed launch stamps the start of the run clock itself
+    memset(&b.q_host, 0, sizeof b.q_host);
+    b.q_host.seed = seed;
+    memcpy(b.q_host.goal, goal4, 4 * sizeof(double));
+    CU(cudaMemcpy(b.q_dev, &b.q_host, sizeof(QueryIn), cudaMemcpyHostToDevice));
+    b.loaded = true; b.fresh = false;
+    return KPX_OK;
+}
+
+// ------------------------------------------------------------------ batches
+int kpx_batch_create(const kpx_problem* prob, int32_t precision, int32_t n_teams, int32_t team_ctas, int32_t max_chain,
+                     int32_t device, kpx_batch** out) {
+    if (!out) return fail(KPX_E_ARG, "out is null");
+    *out = nullptr;
+    if (team_ctas < 1) return fail(KPX_E_ARG, "team_ctas must be >= 1 for batches");
+    kpx_batch* b = new kpx_batch();
+    int rc = init_batch(*b, prob, precision, n_teams, team_ctas, max_chain > 0 ? max_chain : 64, device);
+    if (rc) { destroy_batch(*b); delete b; return rc; }
+    *out = b;
+    return KPX_OK;
+}
+
+void kpx_batch_destroy(kpx_batch* b) {
+    if (!b) return;
+    destroy_batch(*b);
+    delete b;
+}
+
+int kpx_batch_run(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const double* starts, const double* goals,
+                  double t_max, kpx_query_result* results, double* chain_start, double* chain_control,
+                  double* chain_dt, double* o_kernel_ms, void* stream) {
+    if (!bp || !seeds || !starts || !goals || !results) return fail(KPX_E_ARG, "null argument");
+    if (n_queries < 1) return fail(KPX_E_ARG, "n_queries must be >= 1");
+    kpx_batch& b = *bp;
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(b.device));
+    int rc = ensure_queries(b, n_queries);
+    if (rc) return rc;
+    const int n = b.prob.n, nu = b.prob.nu;
+    std::vector<QueryIn> q((size_t)n_queries);
+    for (int64_t i = 0; i < n_queries; ++i) {
+        memset(&q[i], 0, sizeof(QueryIn));
+        q[i].seed = seeds[i];
+        memcpy(q[i].start, starts + i * n, sizeof(double) * n);
+        memcpy(q[i].goal, goals + i * 4, sizeof(double) * 4);
+    }
+    const bool want_chain = chain_start && chain_control && chain_dt;
+    if (want_chain && !b.bc_start) {
+        CU(cudaMalloc(&b.bc_start, 8 * (size_t)b.q_cap * b.max_chain * n));
+        CU(cudaMalloc(&b.bc_ctrl, 8 * (size_t)b.q_cap * b.max_chain * nu));
+        CU(cudaMalloc(&b.bc_dt, 8 * (size_t)b.q_cap * b.max_chain));
+    }
+    CU(cudaMemcpyAsync(b.q_dev, q.data(), sizeof(QueryIn) * (size_t)n_queries, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(b.queue_dev, 0, 4, st));
+    PlanLaunch L = base_launch(b);
+    L.n_queries = (int)n_queries; L.queries_dev = b.q_dev; L.results_dev = b.r_dev; L.queue_dev = b.queue_dev;
+    L.resume = 0; L.max_iters = 0; L.lam_override = 0; L.t_max_s = t_max;
+    if (want_chain) { L.b_chain_start = b.bc_start; L.b_chain_control = b.bc_ctrl; L.b_chain_dt = b.bc_dt; }
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, st));
+    rc = launch(b, L, st);
+    if (rc) return rc;
+    CU(cudaEventRecord(e1, st));
+    CU(cudaMemcpyAsync(results, b.r_dev, sizeof(kpx_query_result) * (size_t)n_queries, cudaMemcpyDeviceToHost, st));
+    if (want_chain) {
+        CU(cudaMemcpyAsync(chain_start, b.bc_start, 8 * (size_t)n_queries * b.max_chain * n, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(chain_control, b.bc_ctrl, 8 * (size_t)n_queries * b.max_chain * nu, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(chain_dt, b.bc_dt, 8 * (size_t)n_queries * b.max_chain, cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    if (o_kernel_ms) { float ms = 0; CU(cudaEventElapsedTime(&ms, e0, e1)); *o_kernel_ms = ms; }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    return KPX_OK;
+}
+
+}  // extern "C"

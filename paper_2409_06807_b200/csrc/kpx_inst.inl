@@ -1,0 +1,94 @@
+// kpx_inst.inl -- included by kpx_inst_f64.cu / kpx_inst_f32.cu with KPX_REAL and KPX_SUFFIX set.
+#include "kpx_launch.h"
+
+namespace kpx {
+namespace {
+
+using Real = KPX_REAL;
+
+template <class M>
+cudaError_t do_launch_plan(const PlanLaunch& L, cudaStream_t st) {
+    PlanArgs<Real> A;
+    fill_params<Real>(A.P, *L.prob);
+    A.obs = (const Real*)L.obs_dev; A.ws = L.ws_dev; A.queries = L.queries_dev; A.results = L.results_dev;
+    A.queue = L.queue_dev; A.n_queries = L.n_queries; A.n_teams = L.n_teams; A.team_ctas = L.team_ctas;
+    A.max_chunks = L.max_chunks; A.stride = L.stride; A.max_trace = L.max_trace; A.max_chain = L.max_chain; A.resume = L.resume;
+    A.max_iters = L.max_iters; A.lam_override = L.lam_override; A.t_max_s = L.t_max_s;
+    A.stop_flag = L.stop_flag; A.peer_flags = L.peer_flags; A.n_peers = L.n_peers;
+    A.b_chain_start = L.b_chain_start; A.b_chain_control = L.b_chain_control; A.b_chain_dt = L.b_chain_dt;
+    auto kern = plan_kernel<M, Real>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    if (e != cudaSuccess) return e;
+    const dim3 grid((unsigned)(L.n_teams * L.team_ctas)), block(kBlock);
+    if (L.cooperative) {
+        void* args[] = {(void*)&A};
+        return cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, L.smem, st);
+    }
+    kern<<<grid, block, L.smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+template <class M>
+cudaError_t do_launch_batch(const BatchLaunch& L, cudaStream_t st) {
+    BatchArgs<Real> A;
+    fill_params<Real>(A.P, *L.prob);
+    A.obs = (const Real*)L.obs_dev; A.states = L.states_dev; A.e_slots = L.e_slots_dev; A.items = L.items;
+    A.lam = L.lam; A.seed = L.seed; A.iteration = L.iteration; A.o_valid = L.o_valid; A.o_region = L.o_region;
+    A.o_sub = L.o_sub; A.o_end = L.o_end; A.o_control = L.o_control; A.o_dt = L.o_dt; A.o_accept = L.o_accept;
+    A.o_substeps = L.o_substeps; A.o_points = L.o_points;
+    batch_kernel<M, Real><<<L.grid, kBlock, L.smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+template <class M>
+int do_occupancy(size_t smem) {
+    auto kern = plan_kernel<M, Real>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, smem) != cudaSuccess) return 0;
+    return nb;
+}
+
+#define KPX_DISPATCH(CALL)                                                                   \
+    switch (model_id) {                                                                      \
+        case KPX_MODEL_DI6: if (n == 6) { CALL(ModelDI6); } break;                           \
+        case KPX_MODEL_DUBINS6: if (n == 6) { CALL(ModelDubins6); } break;                   \
+        case KPX_MODEL_QUAD12: if (n == 12) { CALL(ModelQuad12); } break;                    \
+        case KPX_MODEL_STACKED_DI:                                                           \
+            if (n == 6) { CALL(ModelStackedDI<1>); }                                         \
+            else if (n == 12) { CALL(ModelStackedDI<2>); }                                   \
+            else if (n == 24) { CALL(ModelStackedDI<4>); }                                   \
+            else if (n == 48) { CALL(ModelStackedDI<8>); }                                   \
+            break;                                                                           \
+        default: break;                                                                      \
+    }
+
+}  // namespace
+
+#define KPX_CAT2(a, b) a##b
+#define KPX_CAT(a, b) KPX_CAT2(a, b)
+
+cudaError_t KPX_CAT(launch_plan_, KPX_SUFFIX)(const PlanLaunch& L, cudaStream_t st) {
+    const int model_id = L.prob->model_id, n = L.prob->n;
+#define CALL(M) return do_launch_plan<M>(L, st)
+    KPX_DISPATCH(CALL)
+#undef CALL
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t KPX_CAT(launch_batch_, KPX_SUFFIX)(const BatchLaunch& L, cudaStream_t st) {
+    const int model_id = L.prob->model_id, n = L.prob->n;
+#define CALL(M) return do_launch_batch<M>(L, st)
+    KPX_DISPATCH(CALL)
+#undef CALL
+    return cudaErrorInvalidValue;
+}
+
+int KPX_CAT(plan_blocks_per_sm_, KPX_SUFFIX)(int model_id, int n, size_t smem) {
+#define CALL(M) return do_occupancy<M>(smem)
+    KPX_DISPATCH(CALL)
+#undef CALL
+    return 0;
+}
+
+}  // namespace kpx

@@ -1,0 +1,54 @@
+// kpx_launch.h -- host-side seam between the C-ABI (kpx_api.cu) and the two
+// precision instantiation units (kpx_inst_f64.cu built with -fmad=false,
+// kpx_inst_f32.cu with FMA contraction on).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kpx_plan.cuh"
+
+namespace kpx {
+
+struct PlanLaunch {
+    const kpx_problem* prob;
+    const void* obs_dev;            // SoA [6][n_obs] in the launch precision
+    Workspace* ws_dev;
+    const QueryIn* queries_dev;
+    kpx_query_result* results_dev;
+    unsigned int* queue_dev;        // null: single bound query
+    int n_queries, n_teams, team_ctas, max_chunks, max_trace, max_chain, stride;
+    int resume, max_iters, lam_override;
+    double t_max_s;
+    const uint32_t* stop_flag;
+    uint32_t* const* peer_flags;
+    int n_peers;
+    double *b_chain_start, *b_chain_control, *b_chain_dt;
+    size_t smem;
+    bool cooperative;
+};
+
+struct BatchLaunch {
+    const kpx_problem* prob;
+    const void* obs_dev;
+    const double* states_dev;
+    const long long* e_slots_dev;
+    long long items;
+    int lam;
+    unsigned long long seed, iteration;
+    uint8_t* o_valid;
+    long long *o_region, *o_sub;
+    double *o_end, *o_control, *o_dt, *o_accept;
+    long long *o_substeps, *o_points;
+    int grid;
+    size_t smem;
+};
+
+// each returns cudaErrorInvalidValue for an unsupported (model_id, n)
+cudaError_t launch_plan_f64(const PlanLaunch& L, cudaStream_t st);
+cudaError_t launch_plan_f32(const PlanLaunch& L, cudaStream_t st);
+cudaError_t launch_batch_f64(const BatchLaunch& L, cudaStream_t st);
+cudaError_t launch_batch_f32(const BatchLaunch& L, cudaStream_t st);
+// co-resident CTAs per SM of the plan kernel for this model (0 if unsupported)
+int plan_blocks_per_sm_f64(int model_id, int n, size_t smem);
+int plan_blocks_per_sm_f32(int model_id, int n, size_t smem);
+
+}  // namespace kpx

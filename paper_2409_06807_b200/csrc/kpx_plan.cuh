@@ -1,0 +1,726 @@
+// kpx_plan.cuh -- the device-resident Kino-PAX loop as ONE persistent kernel.
+//
+// A "team" of CTAs owns one planning query at a time: the whole grid for a
+// single query (cooperative launch), or 1..k CTAs per query when many
+// independent queries share the GPU.  Team members meet at a
+// sense-reversing barrier in global memory; with one CTA per team it degrades
+// to __syncthreads().  Per iteration (reference planner.py:283-303):
+//
+//   S1  propagate every (EXPAND slot x extension) item, count outcomes per region
+//       (warp-aggregated atomics), claim fresh (region,sub) pairs with atomicMin(w)
+//   --- team barrier ---
+//   S2  resolve first-visit winners (lowest item index), acceptance gate against
+//       LAST iteration's p_accept, per-chunk keep counts + chunk-local ranks,
+//       first goal hit (atomicMin over item index)
+//   --- team barrier ---
+//   S3  ordered append: slot = size + rank (capacity clamp, cut at first goal hit),
+//       mark regions available from the NEXT iteration; estimate sweep 1
+//       (free volume, score) with a fixed-order partial sum per CTA
+//   --- team barrier ---
+//   S4  p_accept on the fly from (score, total); demote / promote every live slot
+//       from its keyed uniforms; per-chunk compaction of the next EXPAND set
+//   --- team barrier ---
+//       scan chunk counts -> |V_E|; rescue rule; termination
+//
+// Ordering rules (ascending slot order of V_E, item w = i*lambda + ext, append in
+// item order) are kept by construction: compaction is chunk-ordered and ranks are
+// chunk prefix + in-chunk rank, so the tree is identical for any team size.
+#pragma once
+#include "kpx_device.cuh"
+
+namespace kpx {
+
+struct Ctl {                      // one per workspace, global memory
+    // persistent run state (valid between launches: stepped runs, resume)
+    int size, iteration, status, solution_slot;
+    double total_prev;            // sum of scores of the last estimate pass
+    int ve;                       // |V_E| for the next iteration
+    int lam_last;
+    // per-iteration exchange words
+    int first_hit_w;              // lowest kept item index that ends in the goal
+    int stop;                     // set by the timekeeper thread
+    unsigned long long rescue_key;
+    int rescue_slot;
+    int n_items_last, n_keep_last;
+    int cnt_valid[2], cnt_open[2];  // by iteration parity (trace only)
+    // cumulative work
+    unsigned long long sum_items, sum_substeps, sum_points;
+    // timing (globaltimer ns)
+    unsigned long long t_begin, t_reset_done, t_end;
+    int n_trace;
+    int chain_len;
+    int cur_query;                // batch mode: query index broadcast to the team
+};
+
+struct Workspace {                // device pointers of one team's state
+    void *states, *control, *dt;  // R[n][cap], R[nu][cap], R[cap]          (tree arena, SoA)
+    int *parent, *region;         // [cap]
+    uint8_t* tag;                 // [cap]
+    int *n_valid, *n_invalid, *cov, *avail_it;   // [R]
+    double* score;                // [R]
+    uint32_t* claim;              // [R * subs]: kUnclaimed | kVisited | lowest claiming item
+    void* it_end;                 // R[n][cap]  end states of this iteration's valid items
+    uint32_t* it_code;            // [cap] kItemInvalid | (goal bit | pair)
+    int *it_rank, *it_parent;     // [cap]
+    int *e_local;                 // [cap]  chunk-major compacted EXPAND slots
+    int *cnt_expand, *cnt_keep;   // [max_chunks]
+    double* partial;              // [team_ctas]
+    unsigned int* bar;            // {count, generation}
+    Ctl* ctl;
+    kpx_trace* trace;             // [max_trace]
+    // solution chain written on success
+    double *chain_start, *chain_control, *chain_dt; long long* chain_slot; double* chain_end;
+};
+
+struct QueryIn { unsigned long long seed; double start[KPX_MAX_DIM]; double goal[4]; };
+
+template <class R>
+struct PlanArgs {
+    Params<R> P;
+    const R* obs;                 // device SoA [6][n_obs]
+    Workspace* ws;                // [n_teams]
+    const QueryIn* queries;       // [n_queries]
+    kpx_query_result* results;    // [n_queries] (may be null)
+    unsigned int* queue;          // next query index (batch mode)
+    int n_queries, n_teams, team_ctas, max_chunks, max_trace, max_chain;
+    int stride;                   // row stride (elements) of every SoA array: capacity padded to a chunk multiple
+    int resume;                   // 1: continue from Ctl (no reset), single query
+    int max_iters, lam_override;
+    double t_max_s;
+    const uint32_t* stop_flag;    // polled once per iteration (may be null)
+    uint32_t* const* peer_flags;  // set to 1 on success (may be null)
+    int n_peers;
+    // batch-mode chain outputs, [n_queries][max_chain][...] (may be null)
+    double *b_chain_start, *b_chain_control, *b_chain_dt;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct Team {
+    int ctas, rank;
+    unsigned int* bar;
+};
+
+// sense-reversing barrier over the team's CTAs (all co-resident: cooperative launch)
+__device__ __forceinline__ void team_sync(const Team& T) {
+    __syncthreads();
+    if (T.ctas > 1) {
+        if (threadIdx.x == 0) {
+            volatile unsigned int* gen_p = T.bar + 1;
+            unsigned int gen = *gen_p;
+            __threadfence();
+            if (atomicAdd(T.bar, 1u) == (unsigned)T.ctas - 1u) {
+                atomicExch(T.bar, 0u);
+                __threadfence();
+                atomicAdd(T.bar + 1, 1u);
+            } else {
+                while (*gen_p == gen) { __nanosleep(20); }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
+}
+
+// ---- block-level helpers (kBlock threads) ----------------------------------
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { int t = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v += t; }
+    return v;
+}
+// exclusive prefix of one value per thread; *total = block sum.  s_w: >= kBlock/32 + 1 ints.
+__device__ __forceinline__ int block_excl_scan(int v, int* s_w, int* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int inc = warp_incl_scan(v);
+    __syncthreads();                       // protect s_w reuse
+    if (lane == 31) s_w[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int x = lane < kBlock / 32 ? s_w[lane] : 0;
+        int xi = warp_incl_scan(x);
+        if (lane < kBlock / 32) s_w[lane] = xi - x;
+        if (lane == kBlock / 32 - 1) s_w[kBlock / 32] = xi;
+    }
+    __syncthreads();
+    *total = s_w[kBlock / 32];
+    return s_w[wid] + inc - v;
+}
+// exclusive scan of a global int array (n <= max_chunks) into shared memory; s_out[n] = total
+__device__ __forceinline__ int scan_counts(const int* __restrict__ g, int n, int* s_out, int* s_w) {
+    int carry = 0;
+    for (int base = 0; base < n; base += kBlock) {
+        int i = base + threadIdx.x;
+        int v = i < n ? __ldcg(g + i) : 0;
+        int tot;
+        int ex = block_excl_scan(v, s_w, &tot);
+        if (i < n) s_out[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) s_out[n] = carry;
+    __syncthreads();
+    return carry;
+}
+__device__ __forceinline__ double block_sum_f64(double v, double* s_d) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) s_d[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (wid == 0) {
+        t = lane < kBlock / 32 ? s_d[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) s_d[0] = t;
+    }
+    __syncthreads();
+    return s_d[0];
+}
+
+// acceptance probability of region r as of the estimate pass of iteration it_ref
+// (decomposition.py:189-203); regions not yet available then keep 1.0.
+__device__ __forceinline__ double p_accept_of(int r, int it_ref, const int* __restrict__ avail_it,
+                                              const double* __restrict__ score, double total, double eps) {
+    int a = __ldcg(avail_it + r);
+    if (a == 0 || a > it_ref) return 1.0;
+    if (total <= 0.0) return eps < 1.0 ? eps : 1.0;
+    double v = __dadd_rn(__ddiv_rn(__ldcg(score + r), total), eps);
+    return v < 1.0 ? v : 1.0;
+}
+
+// warp-aggregated region counters (decomposition.py:117-125): one atomic per distinct key per warp
+__device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __restrict__ n_invalid, int region,
+                                              bool valid, bool active) {
+    unsigned mask = __ballot_sync(0xffffffffu, active && region >= 0);
+    if (active && region >= 0) {
+        int key = region * 2 + (valid ? 1 : 0);
+        unsigned peers = __match_any_sync(mask, key);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd((valid ? n_valid : n_invalid) + region, __popc(peers));
+    }
+}
+
+template <class M, class R>
+__device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
+                          kpx_query_result* res_out, long long query_index, int* s_prefix, const R* s_obs,
+                          int* s_w, double* s_d) {
+    constexpr int N = M::N, NU = M::NU;
+    const Params<R>& P = A.P;
+    const int tid = threadIdx.x;
+    const int cap = (int)P.t_e;
+    const size_t ld = (size_t)A.stride;    // SoA row stride
+    const int RG = P.n_regions, SUBS = P.subs_per_region;
+    const bool keeper = (T.rank == 0 && tid == 0);
+    const long long tthreads = (long long)T.ctas * kBlock;
+    const long long ttid = (long long)T.rank * kBlock + tid;
+    R* const states = (R*)W.states; R* const control = (R*)W.control; R* const dts = (R*)W.dt;
+    R* const it_end = (R*)W.it_end;
+    Ctl* const ctl = W.ctl;
+    const uint64_t seed = Q.seed;
+    R goal[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) goal[i] = (R)Q.goal[i];
+
+    // ------------------------------------------------------------------ reset
+    if (!A.resume) {
+        if (keeper) ctl->t_begin = gtimer();
+        {   // claim table + region arrays, 16-byte stores
+            uint4* c4 = (uint4*)W.claim;
+            long long n4 = ((long long)RG * SUBS) / 4;
+            const uint4 ones = make_uint4(kUnclaimed, kUnclaimed, kUnclaimed, kUnclaimed);
+            for (long long i = ttid; i < n4; i += tthreads) c4[i] = ones;
+            for (long long i = n4 * 4 + ttid; i < (long long)RG * SUBS; i += tthreads) W.claim[i] = kUnclaimed;
+            for (long long i = ttid; i < RG; i += tthreads) {
+                W.n_valid[i] = 0; W.n_invalid[i] = 0; W.cov[i] = 0; W.avail_it[i] = 0; W.score[i] = 0.0;
+            }
+        }
+        if (keeper) {
+            // init_root + make_available (planner.py:169-171)
+            int reg = 0;
+            bool in_goal0;
+            for (int d = 0; d < N; ++d) {
+                R x = (R)Q.start[d];
+                states[(size_t)d * ld] = x;
+                if (d < P.grid_n) {
+                    R rel = (x - P.grid_lo[d]) / P.grid_width[d];
+                    R cl = rel < (R)0 ? (R)0 : (rel > P.grid_cmax[d] ? P.grid_cmax[d] : rel);
+                    reg += (int)MathK<R>::fl(cl) * P.grid_strides[d];
+                }
+            }
+            {
+                double d0 = Q.start[0] - Q.goal[0], d1 = Q.start[1] - Q.goal[1], d2 = Q.start[2] - Q.goal[2];
+                in_goal0 = sqrt(d0 * d0 + d1 * d1 + d2 * d2) <= Q.goal[3];
+            }
+            for (int j = 0; j < NU; ++j) control[(size_t)j * ld] = (R)0;
+            dts[0] = (R)0;
+            W.parent[0] = -1; W.region[0] = reg; W.tag[0] = KPX_TAG_EXPAND;
+            W.cnt_expand[0] = 1; W.e_local[0] = 0;
+            ctl->size = 1; ctl->iteration = 0; ctl->solution_slot = in_goal0 ? 0 : -1;
+            ctl->status = in_goal0 ? KPX_SOLVED : KPX_RUNNING;      // planner.py:278-280
+            ctl->total_prev = 0.0; ctl->ve = 1; ctl->lam_last = 0;
+            ctl->first_hit_w = 0x7fffffff; ctl->stop = 0; ctl->rescue_key = 0ull; ctl->rescue_slot = 0x7fffffff;
+            ctl->n_items_last = 0; ctl->n_keep_last = 0;
+            ctl->cnt_valid[0] = ctl->cnt_valid[1] = ctl->cnt_open[0] = ctl->cnt_open[1] = 0;
+            ctl->sum_items = ctl->sum_substeps = ctl->sum_points = 0ull;
+            ctl->n_trace = 0; ctl->chain_len = 0;
+        }
+        team_sync(T);
+        if (keeper) { W.avail_it[__ldcg(W.region)] = 1; ctl->t_reset_done = gtimer(); }
+        team_sync(T);
+    }
+
+    // ------------------------------------------------ uniform run state (registers)
+    int size = __ldcg(&ctl->size), it = __ldcg(&ctl->iteration), status = __ldcg(&ctl->status);
+    int solution_slot = __ldcg(&ctl->solution_slot);
+    double total_prev = __ldcg(&ctl->total_prev);
+    unsigned long long t_start = 0;         // run clock origin; only the keeper thread uses it
+    if (keeper) {
+        t_start = __ldcg(&ctl->t_reset_done);
+        if (t_start == 0) { t_start = gtimer(); ctl->t_reset_done = t_start; ctl->t_begin = t_start; }  // loaded state
+    }
+    int iters_this_launch = 0;
+    int ve = scan_counts(W.cnt_expand, (size + kChunk - 1) / kChunk, s_prefix, s_w);
+
+    while (status == KPX_RUNNING) {
+        if (A.max_iters > 0 && iters_this_launch >= A.max_iters) break;
+        { const int st = __ldcg(&ctl->stop); if (st) { status = st; break; } }
+        ++iters_this_launch;
+        ++it;
+        const int par = it & 1;
+        int lam = (cap - size) / ve;                                   // planner.py:48
+        lam = lam > P.lambda_max ? P.lambda_max : lam;
+        lam = lam < 1 ? 1 : lam;
+        if (A.lam_override > 0) lam = A.lam_override;
+        const long long items_ll = (long long)ve * lam;
+        if (items_ll > cap) { status = KPX_ERROR; break; }
+        const int items = (int)items_ll;
+        const int n_ich = (items + kChunk - 1) / kChunk;
+        const int n_sch_old = (size + kChunk - 1) / kChunk;
+        const uint64_t h0 = iter_hash(seed, (uint64_t)it);
+
+        // ================================================================= S1
+        {
+            int my_sub = 0, my_pts = 0, my_valid = 0;
+            for (int c = T.rank; c < n_ich; c += T.ctas) {
+#pragma unroll 1
+                for (int k = 0; k < kChunk / kBlock; ++k) {
+                    const int w = c * kChunk + k * kBlock + tid;
+                    const bool active = w < items;
+                    int region = -1; bool valid = false;
+                    if (active) {
+                        const int i = w / lam, ext = w - i * lam;
+                        // i-th EXPAND slot: chunk by binary search over the prefix, then the chunk-local list
+                        int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
+                        while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
+                        const int slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
+                        R u[NU], dt, x0[N];
+                        int S;
+                        sample_control<M, R>(P, h0, slot, ext, u, &dt, &S, nullptr, nullptr);
+#pragma unroll
+                        for (int d = 0; d < N; ++d) x0[d] = __ldcg(states + (size_t)d * ld + slot);
+                        ItemOut<R, N> o;
+                        integrate_and_map<M, R>(P, s_obs, x0, u, dt, S, o);
+                        my_sub += o.substeps; my_pts += o.points;
+                        region = o.region; valid = o.valid;
+                        uint32_t code = kItemInvalid;
+                        if (valid) {
+                            ++my_valid;
+                            const uint32_t pair = (uint32_t)region * (uint32_t)SUBS + (uint32_t)o.sub;
+                            R d0 = o.end[0] - goal[0], d1 = o.end[1] - goal[1], d2 = o.end[2] - goal[2];
+                            const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= goal[3];
+                            code = pair | (hit ? kItemGoalBit : 0u);
+#pragma unroll
+                            for (int d = 0; d < N; ++d) __stcg(it_end + (size_t)d * ld + w, o.end[d]);
+                            if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
+                        }
+                        __stcg(W.it_code + w, code);
+                        __stcg(W.it_parent + w, slot);
+                    }
+                    count_outcome(W.n_valid, W.n_invalid, region, valid, active);
+                }
+            }
+            // work counters: one atomic per warp
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                my_sub += __shfl_xor_sync(0xffffffffu, my_sub, o);
+                my_pts += __shfl_xor_sync(0xffffffffu, my_pts, o);
+                my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
+            }
+            if ((tid & 31) == 0 && (my_sub | my_pts | my_valid)) {
+                atomicAdd(&ctl->sum_substeps, (unsigned long long)my_sub);
+                atomicAdd(&ctl->sum_points, (unsigned long long)my_pts);
+                atomicAdd(&ctl->cnt_valid[par], my_valid);
+            }
+        }
+        team_sync(T);
+
+        // ================================================================= S2
+        for (int c = T.rank; c < n_ich; c += T.ctas) {
+            const int base = c * kChunk + tid * 4;
+            uint32_t code[4];
+            if (base + 3 < items) {
+                const uint4 v = __ldcg((const uint4*)(W.it_code + base));
+                code[0] = v.x; code[1] = v.y; code[2] = v.z; code[3] = v.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) code[j] = base + j < items ? __ldcg(W.it_code + base + j) : kItemInvalid;
+            }
+            bool keep[4];
+            int cnt = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                keep[j] = false;
+                if (code[j] != kItemInvalid) {
+                    const int w = base + j;
+                    const uint32_t pair = code[j] & ~kItemGoalBit;
+                    const int region = (int)(pair / (uint32_t)SUBS);
+                    const bool first = __ldcg(W.claim + pair) == (uint32_t)w;    // lowest item index wins
+                    if (first) { __stcg(W.claim + pair, kVisited); atomicAdd(W.cov + region, 1); }
+                    bool kp = first;
+                    if (!kp) {
+                        const int slot = __ldcg(W.it_parent + w);
+                        const double ua = keyed_uniform(h0, (uint64_t)slot, (uint64_t)(w % lam), PH_ACCEPT);
+                        kp = ua < p_accept_of(region, it - 1, W.avail_it, W.score, total_prev, P.epsilon);
+                    }
+                    keep[j] = kp;
+                    if (kp) {
+                        ++cnt;
+                        if (code[j] & kItemGoalBit) atomicMin(&ctl->first_hit_w, w);
+                    }
+                }
+            }
+            int tot;
+            int ex = block_excl_scan(cnt, s_w, &tot);
+            int4 rk;
+            rk.x = keep[0] ? ex : -1; ex += keep[0];
+            rk.y = keep[1] ? ex : -1; ex += keep[1];
+            rk.z = keep[2] ? ex : -1; ex += keep[2];
+            rk.w = keep[3] ? ex : -1;
+            __stcg((int4*)(W.it_rank + base), rk);        // arrays are padded to a chunk multiple
+            if (tid == 0) __stcg(W.cnt_keep + c, tot);
+        }
+        team_sync(T);
+
+        // ================================================================= S3
+        const int k_keep = scan_counts(W.cnt_keep, n_ich, s_prefix, s_w);
+        const int remaining = cap - size;
+        const int take = k_keep < remaining ? k_keep : remaining;
+        const bool exhausted = k_keep > 0 && take == 0;                     // planner.py:233-235
+        const int w_hit = __ldcg(&ctl->first_hit_w);
+        bool found = false;
+        int n_app = take;
+        if (w_hit != 0x7fffffff) {
+            const int rank_hit = s_prefix[w_hit / kChunk] + __ldcg(W.it_rank + w_hit);
+            if (rank_hit < take) { found = true; n_app = rank_hit + 1; }   // planner.py:237-242
+        }
+        for (int c = T.rank; c < n_ich; c += T.ctas) {
+            const int base = c * kChunk + tid * 4;
+            const int cpre = s_prefix[c];
+            if (cpre >= n_app) break;                                       // later chunks only hold larger ranks
+            const int4 rk = __ldcg((const int4*)(W.it_rank + base));
+            const int r4[4] = {rk.x, rk.y, rk.z, rk.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (r4[j] < 0) continue;
+                const int rank = cpre + r4[j];
+                if (rank >= n_app) continue;
+                const int w = base + j, slot = size + rank;
+                const int par_slot = __ldcg(W.it_parent + w);
+                const uint32_t pair = __ldcg(W.it_code + w) & ~kItemGoalBit;
+                const int region = (int)(pair / (uint32_t)SUBS);
+                R u[NU], dt; int S;
+                sample_control<M, R>(P, h0, par_slot, w % lam, u, &dt, &S, nullptr, nullptr);
+#pragma unroll
+                for (int d = 0; d < N; ++d) states[(size_t)d * ld + slot] = __ldcg(it_end + (size_t)d * ld + w);
+#pragma unroll
+                for (int q = 0; q < NU; ++q) control[(size_t)q * ld + slot] = u[q];
+                dts[slot] = dt;
+                W.parent[slot] = par_slot; W.region[slot] = region; W.tag[slot] = KPX_TAG_EXPAND;
+                if (__ldcg(W.avail_it + region) == 0) __stcg(W.avail_it + region, it + 1);  // planner.py:246
+            }
+        }
+        {   // estimate sweep 1 (decomposition.py:175-187) over regions available before this append
+            double part = 0.0;
+            for (long long r = ttid; r < RG; r += tthreads) {
+                const int a = __ldcg(W.avail_it + r);
+                if (a != 0 && a <= it) {
+                    const double nv = (double)__ldcg(W.n_valid + r), ni = (double)__ldcg(W.n_invalid + r);
+                    // rn intrinsics: never contracted to FMA, so both precision builds agree bit for bit
+                    const double dn = __dadd_rn(P.delta, nv);
+                    const double fv = __ddiv_rn(__dmul_rn(dn, P.vol), __dadd_rn(dn, ni));
+                    const double tt = __dadd_rn(nv, ni);
+                    const double f2 = __dmul_rn(fv, fv);
+                    const double sc = __ddiv_rn(__dmul_rn(f2, f2),
+                                                __dmul_rn(__dadd_rn(1.0, (double)__ldcg(W.cov + r)),
+                                                          __dadd_rn(1.0, __dmul_rn(tt, tt))));
+                    __stcg(W.score + r, sc);
+                    part += sc;
+                }
+            }
+            part = block_sum_f64(part, s_d);
+            if (tid == 0) __stcg(W.partial + T.rank, part);
+        }
+        const int new_size = size + n_app;
+        team_sync(T);
+
+        // ================================================================= S4
+        double total;
+        {
+            double v = 0.0;
+            for (int b = tid; b < T.ctas; b += kBlock) v += __ldcg(W.partial + b);
+            total = block_sum_f64(v, s_d);
+        }
+        {
+            const int n_sch = (new_size + kChunk - 1) / kChunk;
+            int my_open = 0;
+            for (int c = T.rank; c < n_sch; c += T.ctas) {
+                const int base = c * kChunk + tid * 4;
+                int slots[4]; int cnt = 0;
+                uint8_t newtag[4];
+                uint8_t tg[4] = {0, 0, 0, 0}; int rg[4] = {0, 0, 0, 0};
+                if (base + 3 < new_size) {
+                    const uchar4 t4 = __ldcg((const uchar4*)(W.tag + base));
+                    const int4 r4 = __ldcg((const int4*)(W.region + base));
+                    tg[0] = t4.x; tg[1] = t4.y; tg[2] = t4.z; tg[3] = t4.w;
+                    rg[0] = r4.x; rg[1] = r4.y; rg[2] = r4.z; rg[3] = r4.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (base + j < new_size) { tg[j] = __ldcg(W.tag + base + j); rg[j] = __ldcg(W.region + base + j); }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int s = base + j;
+                    newtag[j] = KPX_TAG_EMPTY;
+                    if (s >= new_size) continue;
+                    uint8_t t = tg[j];
+                    if (s < size) {
+                        const double p = p_accept_of(rg[j], it, W.avail_it, W.score, total, P.epsilon);
+                        const uint64_t hs = slot_ext_hash(h0, (uint64_t)s, 0ull);
+                        if (t == KPX_TAG_EXPAND) {                                     // phase A, planner.py:219-225
+                            const double ud = unit53(draw_u64(mix64(hs ^ (uint64_t)PH_DEMOTE), 0));
+                            if (ud >= p) t = KPX_TAG_OPEN;
+                        }
+                        if (t == KPX_TAG_OPEN) {                                       // phase C, planner.py:251-257
+                            const double up = unit53(draw_u64(mix64(hs ^ (uint64_t)PH_PROMOTE), 0));
+                            if (up < p) t = KPX_TAG_EXPAND;
+                        }
+                    } else {
+                        t = KPX_TAG_EXPAND;                                            // appended this iteration
+                    }
+                    newtag[j] = t;
+                    if (t == KPX_TAG_EXPAND) slots[cnt++] = s; else ++my_open;
+                }
+                if (base + 3 < new_size) {
+                    __stcg((uchar4*)(W.tag + base), make_uchar4(newtag[0], newtag[1], newtag[2], newtag[3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) if (base + j < new_size) __stcg(W.tag + base + j, newtag[j]);
+                }
+                int tot;
+                const int ex = block_excl_scan(cnt, s_w, &tot);
+                for (int j = 0; j < cnt; ++j) __stcg(W.e_local + c * kChunk + ex + j, slots[j]);
+                if (tid == 0) __stcg(W.cnt_expand + c, tot);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) my_open += __shfl_xor_sync(0xffffffffu, my_open, o);
+            if ((tid & 31) == 0 && my_open) atomicAdd(&ctl->cnt_open[par], my_open);
+        }
+        if (keeper) {
+            __stcg(&ctl->first_hit_w, 0x7fffffff);
+            atomicAdd(&ctl->sum_items, (unsigned long long)items);
+            const double el = (double)(gtimer() - t_start) * 1e-9;
+            int stop = 0;
+            if (!(el < A.t_max_s)) stop = KPX_TIMEOUT;                               // planner.py:282
+            if (A.stop_flag && *((volatile const uint32_t*)A.stop_flag)) stop = KPX_STOPPED;
+            if (stop) ctl->stop = stop;
+        }
+        team_sync(T);
+
+        // ================================================= epilogue of the iteration
+        ve = scan_counts(W.cnt_expand, (new_size + kChunk - 1) / kChunk, s_prefix, s_w);
+        if (ve == 0) {
+            // rescue rule (planner.py:259-265): OPEN slot with max p_accept, lowest slot on ties
+            unsigned long long best = 0ull;
+            for (long long s = ttid; s < new_size; s += tthreads) {
+                const double p = p_accept_of(__ldcg(W.region + s), it, W.avail_it, W.score, total, P.epsilon);
+                const unsigned long long b = (unsigned long long)__double_as_longlong(p);   // p > 0: bits are ordered
+                best = b > best ? b : best;
+            }
+            atomicMax(&ctl->rescue_key, best);
+            team_sync(T);
+            const unsigned long long kmax = __ldcg(&ctl->rescue_key);
+            for (long long s = ttid; s < new_size; s += tthreads) {
+                const double p = p_accept_of(__ldcg(W.region + s), it, W.avail_it, W.score, total, P.epsilon);
+                if ((unsigned long long)__double_as_longlong(p) == kmax) { atomicMin(&ctl->rescue_slot, (int)s); break; }
+            }
+            team_sync(T);
+            if (keeper) {
+                const int s = __ldcg(&ctl->rescue_slot);
+                W.tag[s] = KPX_TAG_EXPAND;
+                const int c = s / kChunk;
+                W.e_local[c * kChunk] = s; W.cnt_expand[c] = 1;
+                ctl->rescue_key = 0ull; ctl->rescue_slot = 0x7fffffff;
+                atomicAdd(&ctl->cnt_open[par], -1);
+            }
+            team_sync(T);
+            ve = scan_counts(W.cnt_expand, (new_size + kChunk - 1) / kChunk, s_prefix, s_w);
+        }
+        if (keeper) {   // IterationTrace (planner.py:290-296)
+            const int nt = __ldcg(&ctl->n_trace);
+            if (nt < A.max_trace) {
+                kpx_trace tr;
+                tr.iteration = it; tr.branching = lam; tr.ve_size = items / lam; tr.vo_size = __ldcg(&ctl->cnt_open[par]);
+                tr.attempted = items; tr.valid = __ldcg(&ctl->cnt_valid[par]); tr.staged = k_keep; tr.appended = n_app;
+                tr.tree_size = new_size; tr.elapsed_ms = (double)(gtimer() - t_start) * 1e-6;
+                W.trace[nt] = tr;
+                ctl->n_trace = nt + 1;
+            }
+            ctl->cnt_open[par] = 0; ctl->cnt_valid[par] = 0;
+            ctl->n_items_last = items; ctl->n_keep_last = k_keep; ctl->lam_last = lam;
+        }
+        size = new_size;
+        total_prev = total;
+        if (found) { status = KPX_SOLVED; solution_slot = size - 1; }              // planner.py:297-303
+        else if (exhausted) status = KPX_CAPACITY_EXHAUSTED;
+    }
+
+    // ------------------------------------------------------------------ results
+    if (keeper) {
+        ctl->size = size; ctl->iteration = it; ctl->status = status; ctl->solution_slot = solution_slot;
+        ctl->total_prev = total_prev; ctl->ve = ve;
+        int len = 0;
+        if (status == KPX_SOLVED) {
+            // parent chain (planner.py:325-336), written root-first
+            int s = solution_slot;
+            while (s != 0 && len < A.max_chain) { s = __ldcg(W.parent + s); ++len; }
+            if (s != 0) len = -1;                   // chain longer than the buffer: caller falls back to snapshot
+            double* c_start = W.chain_start; double* c_ctrl = W.chain_control; double* c_dt = W.chain_dt;
+            if (res_out && A.b_chain_start) {
+                c_start = A.b_chain_start + (size_t)query_index * A.max_chain * N;
+                c_ctrl = A.b_chain_control + (size_t)query_index * A.max_chain * NU;
+                c_dt = A.b_chain_dt + (size_t)query_index * A.max_chain;
+            }
+            if (len > 0 && c_start) {
+                s = solution_slot;
+                for (int i = len - 1; i >= 0; --i) {
+                    const int par_s = __ldcg(W.parent + s);
+                    for (int d = 0; d < N; ++d) c_start[(size_t)i * N + d] = (double)__ldcg(states + (size_t)d * ld + par_s);
+                    for (int q = 0; q < NU; ++q) c_ctrl[(size_t)i * NU + q] = (double)__ldcg(control + (size_t)q * ld + s);
+                    c_dt[i] = (double)__ldcg(dts + s);
+                    if (!res_out && W.chain_slot) W.chain_slot[i] = s;
+                    s = par_s;
+                }
+                if (!res_out && W.chain_end)
+                    for (int d = 0; d < N; ++d) W.chain_end[d] = (double)__ldcg(states + (size_t)d * ld + solution_slot);
+            }
+            for (int i = 0; i < A.n_peers; ++i) { *((volatile uint32_t*)A.peer_flags[i]) = 1u; }
+            if (A.n_peers) __threadfence_system();
+        }
+        ctl->chain_len = len;
+        ctl->t_end = gtimer();
+        if (res_out) {
+            kpx_query_result r;
+            r.status = status; r.iterations = it; r.tree_size = size; r.solution_slot = solution_slot;
+            r.chain_len = len; r.device_ms = (double)(ctl->t_end - __ldcg(&ctl->t_begin)) * 1e-6;
+            r.items = __ldcg(&ctl->sum_items); r.substeps = __ldcg(&ctl->sum_substeps); r.points = __ldcg(&ctl->sum_points);
+            *res_out = r;
+        }
+    }
+}
+
+template <class M, class R>
+__global__ void __launch_bounds__(kBlock) plan_kernel(const __grid_constant__ PlanArgs<R> A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int* s_prefix = (int*)smem_raw;                                       // [max_chunks + 1]
+    R* s_obs = (R*)(smem_raw + (((size_t)(A.max_chunks + 1) * sizeof(int) + 15) & ~(size_t)15));
+    __shared__ int s_w[kBlock / 32 + 1];
+    __shared__ double s_d[kBlock / 32];
+    __shared__ int s_q;
+
+    for (int i = threadIdx.x; i < 6 * A.P.n_obs; i += kBlock) s_obs[i] = A.obs[i];
+    __syncthreads();
+
+    Team T;
+    T.ctas = A.team_ctas;
+    const int team_id = blockIdx.x / A.team_ctas;
+    T.rank = blockIdx.x - team_id * A.team_ctas;
+    if (team_id >= A.n_teams) return;
+    const Workspace W = A.ws[team_id];
+    T.bar = W.bar;
+
+    if (A.queue == nullptr) {       // single query bound to team 0 (plan handle: stepped / resumable)
+        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_obs, s_w, s_d);
+        return;
+    }
+    for (;;) {                      // batch: teams pull queries until the queue is drained
+        if (T.ctas == 1) {
+            if (threadIdx.x == 0) s_q = (int)atomicAdd(A.queue, 1u);
+            __syncthreads();
+        } else {
+            if (T.rank == 0 && threadIdx.x == 0) __stcg(&W.ctl->cur_query, (int)atomicAdd(A.queue, 1u));
+            team_sync(T);
+            if (threadIdx.x == 0) s_q = __ldcg(&W.ctl->cur_query);
+            __syncthreads();
+            team_sync(T);           // everyone has read the slot before reset rewrites it
+        }
+        const int q = s_q;
+        __syncthreads();
+        if (q >= A.n_queries) return;
+        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_obs, s_w, s_d);
+        team_sync(T);
+    }
+}
+
+// ---- stand-alone propagation batch: the drop-in for _kernel.propagate_batch -------------
+template <class R>
+struct BatchArgs {
+    Params<R> P;
+    const R* obs;              // device SoA [6][n_obs]
+    const double* states;      // (rows, n) f64 row-major, as the reference passes it
+    const long long* e_slots;  // (m)
+    long long items; int lam;
+    unsigned long long seed, iteration;
+    uint8_t* o_valid; long long *o_region, *o_sub; double *o_end, *o_control, *o_dt, *o_accept;
+    long long *o_substeps, *o_points;
+};
+
+template <class M, class R>
+__global__ void __launch_bounds__(kBlock) batch_kernel(const __grid_constant__ BatchArgs<R> A) {
+    constexpr int N = M::N, NU = M::NU;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* s_obs = (R*)smem_raw;
+    for (int i = threadIdx.x; i < 6 * A.P.n_obs; i += kBlock) s_obs[i] = A.obs[i];
+    __syncthreads();
+    const uint64_t h0 = iter_hash(A.seed, A.iteration);
+    for (long long w = (long long)blockIdx.x * kBlock + threadIdx.x; w < A.items; w += (long long)gridDim.x * kBlock) {
+        const long long i = w / A.lam;
+        const int ext = (int)(w - i * A.lam);
+        const long long slot = A.e_slots[i];
+        R u[NU], dt, x0[N]; int S; double u64v[NU], dt64;
+        // the reference hashes the 64-bit slot; planner slots always fit 31 bits
+        sample_control<M, R>(A.P, h0, (int)slot, ext, u, &dt, &S, u64v, &dt64);
+#pragma unroll
+        for (int d = 0; d < N; ++d) x0[d] = (R)A.states[slot * N + d];
+        ItemOut<R, N> o;
+        integrate_and_map<M, R>(A.P, s_obs, x0, u, dt, S, o);
+#pragma unroll
+        for (int d = 0; d < N; ++d) A.o_end[w * N + d] = (double)o.end[d];
+#pragma unroll
+        for (int j = 0; j < NU; ++j) A.o_control[w * NU + j] = u64v[j];
+        A.o_dt[w] = dt64;
+        A.o_valid[w] = o.valid ? 1 : 0;
+        A.o_region[w] = o.region;
+        A.o_sub[w] = o.sub;
+        A.o_accept[w] = keyed_uniform(h0, (uint64_t)slot, (uint64_t)ext, PH_ACCEPT);
+        if (A.o_substeps) A.o_substeps[w] = o.substeps;
+        if (A.o_points) A.o_points[w] = o.points;
+    }
+}
+
+}  // namespace kpx

@@ -1,0 +1,293 @@
+"""GPU parity tests proper: the CUDA path (through the C ABI) against the CPU oracle and the
+golden vectors recorded from the unmodified reference.
+
+Bars (BASELINE.json north_star): RNG draws, controls, durations, collision verdicts, region /
+sub-region indices, region counters, first-visit winners and compaction slots are BIT-EXACT;
+float64 end states are bit-exact for the double integrator and within 1e-12 for the trig models
+(CUDA libm vs glibc, the tolerance the reference uses between its own two backends,
+tests/test_backends.py:44-53); float32 end states agree within 1e-5 relative.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, make_empty_env, small_cfg
+
+pytestmark = pytest.mark.gpu
+
+F32_RTOL = 1e-5      # north_star: "propagated states agree within 1e-5 relative (FP32 vs float64)"
+TRIG_ATOL = 1e-12    # reference's own cross-backend tolerance for trig models
+
+
+def _ctx_from_golden(kp, g, model):
+    from paper_2409_06807_b200.backend import PlanContext
+    return PlanContext(model=model, seed=int(g["seed"]), t_prop=float(g["t_prop"]), state_lo=g["state_lo"],
+                       state_hi=g["state_hi"], obs_min=g["obs_min"], obs_max=g["obs_max"],
+                       check_res=float(g["check_res"]), grid_lo=g["grid_lo"], grid_width=g["grid_width"],
+                       grid_cells=g["grid_cells"], grid_strides=g["grid_strides"], subcells=int(g["subcells"]))
+
+
+def _wrap_diff(a, b, wrap_dims):
+    d = np.abs(a - b)
+    for w in wrap_dims:
+        d[:, w] = np.minimum(d[:, w], np.abs(2 * np.pi - d[:, w]))
+    return d
+
+
+@pytest.mark.parametrize("model_name", ["di6", "dubins6", "quad12"])
+def test_batch_parity_f64_vs_reference_golden(kp, model_name):
+    """tests/test_backends.py:37-54 with the CUDA backend in the compiled backend's place."""
+    g = np.load(os.path.join(GOLDEN, f"batch_{model_name}.npz"))
+    model = kp.get_model(model_name)
+    b = kp.get_backend("cuda").propagate_batch(_ctx_from_golden(kp, g, model), g["states"], g["e_slots"],
+                                               int(g["lam"]), int(g["iteration"]))
+    assert np.array_equal(b.control, g["control"])
+    assert np.array_equal(b.dt, g["dt"])
+    assert np.array_equal(b.accept_u, g["accept_u"])
+    assert np.array_equal(b.valid, g["valid"])
+    assert np.array_equal(b.region, g["region"])
+    assert np.array_equal(b.sub, g["sub"])
+    if model_name == "di6":
+        assert np.array_equal(b.end, g["end"])
+    else:
+        assert np.max(_wrap_diff(b.end, g["end"], model.wrap_dims)) < TRIG_ATOL
+
+
+@pytest.mark.parametrize("model_name", ["di6", "dubins6", "quad12"])
+def test_batch_parity_f32_tolerance(kp, model_name):
+    g = np.load(os.path.join(GOLDEN, f"batch_{model_name}.npz"))
+    model = kp.get_model(model_name)
+    b = kp.get_backend("cuda-f32").propagate_batch(_ctx_from_golden(kp, g, model), g["states"], g["e_slots"],
+                                                   int(g["lam"]), int(g["iteration"]))
+    # sampling is done in float64 on the device even in the float32 build: bit-exact
+    assert np.array_equal(b.control, g["control"]) and np.array_equal(b.dt, g["dt"])
+    assert np.array_equal(b.accept_u, g["accept_u"])
+    scale = np.maximum(np.abs(g["end"]), 1.0)
+    rel = _wrap_diff(b.end, g["end"], model.wrap_dims) / scale
+    assert np.max(rel) < F32_RTOL, np.max(rel)
+    # verdicts / cells may flip only for items that sit within float32 rounding of a boundary
+    agree = (b.valid == g["valid"]) & (b.region == g["region"])
+    assert agree.mean() > 0.995, agree.mean()
+    both = (b.valid == 1) & (g["valid"] == 1) & (b.region == g["region"])
+    assert (b.sub[both] == g["sub"][both]).mean() > 0.99
+
+
+def test_kernel_rng_matches_stream(kp):
+    """tests/test_rng.py:70-102: one item's controls / duration / gate draw equal the scalar stream."""
+    from paper_2409_06807_b200.backend import PlanContext
+    from paper_2409_06807_b200.rng import PHASE_ACCEPT, PHASE_SAMPLE, RngStream
+    model = kp.get_model("di6")
+    ctx = PlanContext(model=model, seed=99, t_prop=1.0, state_lo=np.array([0, 0, 0, -5, -5, -5.0]),
+                      state_hi=np.array([10, 10, 10, 5, 5, 5.0]), obs_min=np.zeros((0, 3)), obs_max=np.zeros((0, 3)),
+                      check_res=0.05, grid_lo=np.array([0, 0, 0, -5, -5, -5.0]), grid_width=np.full(6, 2.5),
+                      grid_cells=np.full(6, 4, dtype=np.int64),
+                      grid_strides=np.array([1024, 256, 64, 16, 4, 1], dtype=np.int64), subcells=4)
+    states = np.array([[1, 1, 1, 0, 0, 0.0]])
+    for name in ("cuda", "cuda-f32"):
+        batch = kp.get_backend(name).propagate_batch(ctx, states, np.array([0], dtype=np.int64), 3, iteration=4)
+        for ext in range(3):
+            s = RngStream(seed=99, iteration=4, slot=0, extension=ext, phase=PHASE_SAMPLE)
+            assert batch.control[ext].tolist() == [s.uniform_in(model.control_lo[j], model.control_hi[j])
+                                                   for j in range(3)]
+            assert batch.dt[ext] == s.duration(1.0)
+            assert batch.accept_u[ext] == RngStream(seed=99, iteration=4, slot=0, extension=ext,
+                                                    phase=PHASE_ACCEPT).uniform()
+
+
+def test_batch_edge_cases(kp, orc):
+    """Empty batch, single item, no obstacles, ragged (non multiple of the block) sizes, dimension limits."""
+    from paper_2409_06807_b200.backend import PlanContext
+    model = kp.get_model("di6")
+    env = make_empty_env(kp)
+    prob = kp.build_problem(small_cfg(kp, model, t_e=100), env, model)
+    ctx = PlanContext(model=model, seed=5, t_prop=1.0, state_lo=prob.state_lo, state_hi=prob.state_hi,
+                      obs_min=env.obstacles_min, obs_max=env.obstacles_max, check_res=0.05, grid_lo=prob.grid.lo,
+                      grid_width=prob.grid.widths, grid_cells=prob.grid.cells, grid_strides=prob.grid.strides,
+                      subcells=4)
+    be = kp.get_backend("cuda")
+    states = np.tile(env.start, (7, 1))
+    empty = be.propagate_batch(ctx, states, np.zeros(0, dtype=np.int64), 4, 1)
+    assert empty.items == 0 and empty.end.shape == (0, 6)
+    octx, keep = orc.ctx_from_problem(prob)
+    for m, lam in ((1, 1), (7, 3), (5, 32)):
+        slots = np.arange(m, dtype=np.int64)
+        a = be.propagate_batch(ctx, states, slots, lam, 2)
+        o = orc.propagate_batch(octx, states, slots, lam, 5, 2)
+        for f in ("valid", "region", "sub", "end", "control", "dt", "accept_u"):
+            assert np.array_equal(getattr(a, f), o[f]), (m, lam, f)
+    with pytest.raises(kp.ConfigError):
+        be.propagate_batch(ctx, states, np.array([9], dtype=np.int64), 1, 1)       # slot outside states
+
+
+def _step_compare(kp, orc, model_name, scene, t_e, seed, backend, max_iters=60, env=None):
+    model = kp.get_model(model_name)
+    env = kp.gen_environment(scene, model, seed=0) if env is None else env
+    cfg = small_cfg(kp, model, t_e=t_e, seed=seed)
+    op = orc.plan_from_problem(kp.build_problem(cfg, env, model))
+    exact = model_name.startswith("di")
+    with kp.KinoPax(cfg, env, model, backend=backend) as eng:
+        for it in range(1, max_iters + 1):
+            st = eng.step()
+            op.step()
+            a, b = eng.snapshot(), op.snapshot()
+            assert a["size"] == b["size"], (it, a["size"], b["size"])
+            for k in ("parent", "tag", "region", "control", "dt"):
+                assert np.array_equal(a[k], b[k]), (it, k)
+            if exact:
+                assert np.array_equal(a["states"], b["states"]), it
+            else:
+                assert np.max(_wrap_diff(a["states"], b["states"], model.wrap_dims)) < 1e-9, it
+            ra, rb = eng.region_state(), op.decomposition()
+            for k in ("n_valid", "n_invalid", "cov", "visited"):
+                assert np.array_equal(getattr(ra, k), rb[k]), (it, k)
+            assert np.array_equal(ra.avail_mask, rb["avail"].astype(bool)), it
+            assert np.allclose(ra.score, rb["score"], rtol=1e-13, atol=0), it
+            assert np.allclose(ra.p_accept, rb["p_accept"], rtol=1e-12, atol=0), it
+            tr, orc_tr = eng.traces()[-1], op.trace()
+            for k in ("iteration", "branching", "ve_size", "vo_size", "attempted", "valid", "staged", "appended",
+                      "tree_size"):
+                assert getattr(tr, k) == orc_tr[k], (it, k)
+            # the kernel's per-item results (valid / region / sub / keep / end) of this iteration
+            items, ob = eng.last_items(), op.last_batch()
+            assert np.array_equal(items["valid"], ob["valid"]), it
+            v = ob["valid"].astype(bool)
+            assert np.array_equal(items["region"][v], ob["region"][v]) and np.array_equal(items["sub"][v], ob["sub"][v])
+            keep = np.zeros(len(v), np.uint8)
+            keep[ob["staged_idx"]] = 1
+            assert np.array_equal(items["keep"], keep), it
+            if st.status != 4:
+                break
+        assert {0: "solved", 1: "timeout", 2: "capacity_exhausted"}[st.status] == op.status
+        if st.status == 0:
+            assert int(st.solution_slot) == int(op.raw.solution_slot)
+        return it
+
+
+@pytest.mark.parametrize("model_name,scene,t_e,seed", [("di6", "forest", 6000, 1), ("di6", "narrow", 3000, 2),
+                                                       ("dubins6", "building", 5000, 2), ("quad12", "narrow", 8000, 3)])
+def test_plan_matches_oracle_every_iteration_f64(kp, orc, model_name, scene, t_e, seed):
+    """Whole-state parity after every iteration: tree, tags, counters, visited bits, scores, p_accept,
+    trace counters, per-item verdicts and the kept set (compaction input) -- the device-side twin of
+    tests/test_backends.py:73-85 (tree_snapshot identical across backends)."""
+    _step_compare(kp, orc, model_name, scene, t_e, seed, "cuda")
+
+
+def test_plan_matches_reference_golden_tree(kp):
+    """Single-launch solve (no stepping) reproduces the tree the reference itself produced."""
+    g = np.load(os.path.join(GOLDEN, "tree_di6_forest_te6000_s1.npz"))
+    model = kp.get_model("di6")
+    res = kp.plan(small_cfg(kp, model, t_e=6000, seed=1), kp.gen_environment("forest", model, 0), model,
+                  backend="cuda", capture_tree=True)
+    s = res.tree_snapshot
+    assert res.solved and s["size"] == int(g["size"])
+    for k in ("states", "parent", "control", "dt", "tag", "region"):
+        assert np.array_equal(s[k], g[k]), k
+    cases = {(c["model"], c["scene"], c["t_e"], c["seed"]): c for c in json.load(open(os.path.join(GOLDEN, "plans.json")))}
+    c = cases[("di6", "forest", 6000, 1)]
+    assert res.stats.iterations == len(c["iterations"]) and res.stats.tree_size == c["iterations"][-1]["tree_size"]
+
+
+def test_team_size_does_not_change_the_tree(kp):
+    """Determinism by construction (reference: thread-count invariance, tests/test_backends.py:88-97)."""
+    model = kp.get_model("di6")
+    env = kp.gen_environment("narrow", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=3000, seed=2)
+    snaps = []
+    for team in (0, 1, 3, 16):
+        with kp.KinoPax(cfg, env, model, backend="cuda", team_ctas=team) as eng:
+            snaps.append(eng.solve(capture_tree=True).tree_snapshot)
+    for s in snaps[1:]:
+        assert s["size"] == snaps[0]["size"]
+        for k in ("states", "parent", "tag", "region", "dt"):
+            assert np.array_equal(s[k], snaps[0][k]), k
+
+
+def test_capacity_exhaustion_start_in_goal_and_enclosed_goal(kp, orc):
+    model = kp.get_model("di6")
+    env = make_empty_env(kp, goal_center=(9.0, 9.0, 9.0))
+    res = kp.plan(small_cfg(kp, model, t_e=40, seed=0), env, model)
+    assert res.status is kp.PlanStatus.CAPACITY_EXHAUSTED and res.stats.tree_size == 40      # tests/test_planner.py:145
+    here = make_empty_env(kp, goal_center=(1.0, 1.0, 1.0))
+    res = kp.plan(small_cfg(kp, model, t_e=100), here, model)
+    assert res.solved and res.stats.iterations == 0 and res.trajectory == []                  # tests/test_planner.py:153
+    # goal sealed inside a box: the run must end by timeout, never claim success
+    sealed = kp.Environment("sealed", np.zeros(3), np.full(3, 10.0), np.array([[7.0, 7, 7]]), np.array([[10.0, 10, 10]]),
+                            env.start, kp.GoalBall(np.array([8.5, 8.5, 8.5]), 0.5))
+    res = kp.plan(small_cfg(kp, model, t_e=3000, t_max=0.05), sealed, model)
+    assert res.status in (kp.PlanStatus.TIMEOUT, kp.PlanStatus.CAPACITY_EXHAUSTED)
+
+
+def test_rescue_rule_matches_oracle(kp, orc):
+    """Tiny epsilon-driven demotion empties V_E quickly; the forced promotion must pick the same slot
+    (tests/test_planner.py:208)."""
+    model = kp.get_model("di6")
+    env = kp.gen_environment("building", model, seed=0)
+    cfg = kp.PlannerConfig(t_e=400, t_prop=1.0, cells_per_dim=2, epsilon=1e-6, seed=11)
+    op = orc.plan_from_problem(kp.build_problem(cfg, env, model))
+    with kp.KinoPax(cfg, env, model, backend="cuda") as eng:
+        for it in range(40):
+            st = eng.step()
+            op.step()
+            a, b = eng.snapshot(), op.snapshot()
+            assert a["size"] == b["size"] and np.array_equal(a["tag"], b["tag"]), it
+            assert (a["tag"] == 1).sum() >= 1
+            if st.status != 4:
+                break
+
+
+@pytest.mark.parametrize("model_name,scene", [("di6", "forest"), ("dubins6", "building"), ("quad12", "forest")])
+def test_solutions_revalidate_f32_and_f64(kp, orc, model_name, scene):
+    """Every returned solution is re-validated (dynamically feasible, collision-free, ends in goal) by the
+    host checker AND by the oracle's restatement of the reference checker, at the planning resolution."""
+    model = kp.get_model(model_name)
+    env = kp.gen_environment(scene, model, seed=0)
+    t_e = 60000 if model_name != "quad12" else 120000
+    for backend in ("cuda", "cuda-f32"):
+        solved = 0
+        for seed in range(4):
+            cfg = small_cfg(kp, model, t_e=t_e, seed=seed)
+            res = kp.plan(cfg, env, model, backend=backend)
+            if not res.solved:
+                continue
+            solved += 1
+            assert kp.ValidityChecker(env, model, 0.05).trajectory_valid(res.trajectory, start=env.start)
+            prob = kp.build_problem(cfg, env, model)
+            ctx, keep = orc.ctx_from_problem(prob)
+            ok, code = orc.trajectory_valid(ctx, [s.start_state for s in res.trajectory],
+                                            [s.control for s in res.trajectory], [s.dt for s in res.trajectory],
+                                            env.start, prob.goal4, 0.05)
+            assert ok, (backend, seed, code)
+        assert solved >= 3, (backend, solved)
+
+
+def test_load_state_resume_equals_uninterrupted(kp, orc):
+    """Checkpoint/resume: load the oracle's state after k iterations, continue on the device, and land on the
+    same tree as an uninterrupted device run."""
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=6000, seed=1)
+    op = orc.plan_from_problem(kp.build_problem(cfg, env, model))
+    for _ in range(4):
+        op.step()
+    with kp.KinoPax(cfg, env, model, backend="cuda") as eng:
+        eng.load_state(op.snapshot(), op.decomposition(), iteration=4)
+        st = eng._run(60.0)
+        resumed = eng.snapshot()
+    full = kp.plan(cfg, env, model, backend="cuda", capture_tree=True).tree_snapshot
+    assert st.status == 0 and resumed["size"] == full["size"]
+    for k in ("states", "parent", "tag", "region"):
+        assert np.array_equal(resumed[k], full[k]), k
+
+
+def test_high_dimensional_stacked_integrators(kp, orc):
+    """Config 4 (12D/24D/48D): device vs oracle, every iteration, float64."""
+    for blocks, t_e in ((2, 3000), (4, 2500), (8, 2000)):
+        model = kp.stacked_double_integrator(blocks)
+        base = kp.gen_environment("forest", "di6", seed=0)
+        start = np.tile(np.array([5.0, 5, 5, 0, 0, 0]), blocks)
+        start[:3] = base.start[:3]
+        env = kp.Environment(f"forest-{model.name}", base.workspace_lo, base.workspace_hi, base.obstacles_min,
+                             base.obstacles_max, start, base.goal)
+        _step_compare(kp, orc, model.name, "forest", t_e, 3, "cuda", max_iters=12, env=env)

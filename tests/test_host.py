@@ -1,0 +1,160 @@
+"""Host-side logic and the C-ABI surface (no GPU needed)."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT, make_empty_env, small_cfg
+
+
+def test_rng_matches_reference_golden(kp):
+    from paper_2409_06807_b200 import rng
+    g = json.load(open(os.path.join(GOLDEN, "rng.json")))
+    for m in g["mix64"]:
+        assert rng.mix64(int(m["z"])) == int(m["mix"])
+        assert int(rng.mix64_np(np.array([int(m["z"])], dtype=np.uint64))[0]) == int(m["mix"])
+    for c in g["stream_cases"]:
+        key = rng.stream_key(c["seed"], c["iteration"], c["slot"], c["ext"], c["phase"])
+        assert key == int(c["key"])
+        kn = rng.stream_keys_np(c["seed"], c["iteration"], np.array([c["slot"]]), np.array([c["ext"]]), c["phase"])
+        assert int(kn[0]) == key
+        for i, (d, u) in enumerate(zip(c["draws"], c["units"])):
+            assert rng.draw_u64(key, i) == int(d)
+            assert rng.u64_to_unit(int(d)) == float.fromhex(u)
+            assert rng.uniforms_np(kn, i)[0] == float.fromhex(u)
+    s = rng.RngStream(seed=11)
+    xs = np.array([s.duration(1.0) for _ in range(2000)])
+    assert np.all((xs > 0.0) & (xs <= 1.0))                       # never exactly zero (tests/test_rng.py:64)
+    assert rng.stream_key(-1, 0, 0, 0, 1) == rng.stream_key((1 << 64) - 1, 0, 0, 0, 1)
+
+
+def test_scenes_match_reference_golden(kp):
+    g = json.load(open(os.path.join(GOLDEN, "scenes.json")))
+    for key, rec in g.items():
+        kind, model, seed = key.split("/")
+        env = kp.gen_environment(kind, model, seed=int(seed))
+        assert env.name == rec["name"]
+        assert env.obstacles_min.tolist() == rec["obs_min"] and env.obstacles_max.tolist() == rec["obs_max"]
+        assert env.start.tolist() == rec["start"]
+        assert env.goal.center.tolist() + [env.goal.radius] == rec["goal"]
+    with pytest.raises(kp.GenerationError):
+        kp.gen_environment("swamp", "di6")
+
+
+def test_config_validation(kp):
+    di6 = kp.get_model("di6")
+    assert kp.validate_config(kp.PlannerConfig(t_e=100), di6).region_count == 4096
+    for bad in (dict(t_e=0), dict(t_e=10, epsilon=0.0), dict(t_e=10, epsilon=1.0), dict(t_e=10, delta=0.0),
+                dict(t_e=10, t_prop=0.0), dict(t_e=10, lambda_max=0), dict(t_e=10, cells_per_dim=0)):
+        with pytest.raises(kp.ConfigError):
+            kp.validate_config(kp.PlannerConfig(**bad), di6)
+    with pytest.raises(kp.ConfigError, match="exceeding the cap"):
+        kp.validate_config(kp.PlannerConfig(t_e=10, cells_per_dim=4), kp.get_model("quad12"))
+    assert kp.suggest_cells_per_dim(12) == 3 and kp.suggest_cells_per_dim(6) == 11
+    assert kp.compute_branching_factor(100, 1, 1, 32) == 32        # Eq. 6 known answers (tests/test_planner.py:17-28)
+    assert kp.compute_branching_factor(100, 90, 20, 32) == 1
+    assert kp.compute_branching_factor(1000, 100, 100, 32) == 9
+
+
+def test_environment_json_roundtrip(kp, tmp_path):
+    env = kp.gen_environment("building", "quad12", seed=0)
+    p = tmp_path / "env.json"
+    kp.save_environment(env, p)
+    back = kp.load_environment(p)
+    assert np.array_equal(back.obstacles_min, env.obstacles_min) and np.array_equal(back.start, env.start)
+    with pytest.raises(kp.EnvironmentIOError):
+        kp.load_environment(tmp_path / "missing.json")
+    p.write_text("{not json")
+    with pytest.raises(kp.EnvironmentFormatError):
+        kp.load_environment(p)
+    doc = kp.environment_to_dict(env)
+    doc["start"][0] = 5.0    # inside the wall
+    doc["start"][1] = 7.0
+    with pytest.raises(kp.EnvironmentFormatError):
+        kp.environment_from_dict(doc)
+
+
+def test_grid_geometry_known_answers(kp):
+    """Mapping rules of decomposition.py:76-106 (C-order strides, clamping, centre -> sub 7 at subcells=2)."""
+    g = kp.GridGeometry(np.array([0, 0, 0, -5, -5, -5.0]), np.array([10, 10, 10, 5, 5, 5.0]), 4, 4)
+    assert g.strides.tolist() == [1024, 256, 64, 16, 4, 1] and g.n_regions == 4096
+    assert g.region_index(np.array([1, 1, 1, 0, 0, 0.0])) == 0 * 1024 + 0 + 0 + 2 * 16 + 2 * 4 + 2
+    assert g.region_index(np.array([10, 10, 10, 5, 5, 5.0])) == 4095           # upper boundary clamps into last cell
+    assert g.region_index(np.array([-3, 0, 0, -9, 0, 0.0])) == g.region_index(np.array([0, 0, 0, -5, 0, 0.0]))
+    g2 = kp.GridGeometry(np.zeros(6), np.full(6, 8.0), 2, 2)
+    r, s = g2.map_states(np.array([[3.0, 3.0, 3.0, 0, 0, 0]]))
+    assert r[0] == 0 and s[0] == 7 and g2.subregion_index(np.array([3.0, 3.0, 3.0, 0, 0, 0]), 0) == 7
+
+
+def test_validity_checker_rules(kp):
+    env = kp.gen_environment("narrow", "di6", seed=0)
+    chk = kp.ValidityChecker(env, kp.get_model("di6"), 0.05)
+    assert not chk.state_valid(np.array([4.75, 5, 5, 0, 0, 0.0]))            # touching a face collides (closed box)
+    assert chk.state_valid(np.array([4.7499, 5, 5, 0, 0, 0.0]))
+    assert not chk.state_valid(np.array([1, 1, 1, 5.0001, 0, 0]))            # velocity box
+    assert chk.state_valid(np.array([0, 0, 0, 5.0, 0, 0]))                   # boundary is valid
+    from paper_2409_06807_b200.validity import densify_steps
+    assert [densify_steps(d, 0.05) for d in (0.0, 0.05, 0.051, 0.1, 0.11, 0.2001)] == [1, 1, 2, 2, 4, 8]
+    assert kp.in_goal(np.array([8.5, 5, 5 - 1.25, 0, 0, 0.0]), env.goal)
+    ball = kp.GoalBall(np.array([0.0, 0, 0]), 1.0)
+    assert ball.contains(np.array([1.0, 0, 0])) and not ball.contains(np.array([1.0000001, 0, 0]))
+
+
+def test_backend_registry_contract(kp, monkeypatch):
+    """backend.py:103-122: explicit name -> env override -> default; unknown names raise ConfigError."""
+    if not kp.cuda_available():
+        pytest.skip("libkpx.so not built")
+    assert kp.get_backend("cuda").name == "cuda" and kp.get_backend("cuda-f32").name == "cuda-f32"
+    assert kp.get_backend(None, kp.get_model("di6")).name == "cuda"
+    monkeypatch.setenv("KINOPAX_BACKEND", "cuda-f32")
+    assert kp.get_backend(None).name == "cuda-f32"
+    with pytest.raises(kp.ConfigError):
+        kp.get_backend("python")            # no CPU backend exists in this package
+    with pytest.raises(kp.ConfigError):
+        kp.get_backend("no-such-backend")
+
+
+def test_problem_flattening(kp):
+    m = kp.get_model("quad12")
+    env = kp.gen_environment("narrow", m, seed=0)
+    prob = kp.build_problem(small_cfg(kp, m, t_e=1000), env, m)
+    assert prob.grid.n_regions == 3 ** 12 and prob.grid.subs_per_region == 64
+    assert prob.state_lo[:3].tolist() == [0, 0, 0] and prob.state_hi[6] == 1.0
+    with pytest.raises(kp.ConfigError):                              # start inside an obstacle
+        bad = kp.Environment(env.name, env.workspace_lo, env.workspace_hi, env.obstacles_min, env.obstacles_max,
+                             np.array([5.0, 5, 5] + [0] * 9, dtype=float), env.goal)
+        kp.build_problem(small_cfg(kp, m, t_e=1000), bad, m)
+    s = kp.stacked_double_integrator(4)
+    assert s.n == 24 and s.control_dim == 12 and s.kernel_id == 3 and s.default_cells_per_dim == 1
+
+
+def test_c_abi_exports_every_declared_symbol(kp):
+    """libkpx.so must load and export exactly what include/kpx.h declares (no compute calls here)."""
+    from paper_2409_06807_b200 import _lib
+    if not os.path.isfile(_lib.LIB_PATH):
+        pytest.skip("libkpx.so not built")
+    header = open(os.path.join(ROOT, "include", "kpx.h")).read()
+    declared = set(re.findall(r"^(?:int|void|const char \*)\s*(kpx_[a-z_0-9]+)\(", header, flags=re.M))
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in kpx.h but not exported"
+    assert declared == set(_lib.EXPORTED_SYMBOLS), declared ^ set(_lib.EXPORTED_SYMBOLS)
+    assert _lib.load().kpx_version() >= 100
+    # struct layouts agree with the compiled header (checked inside load(); sizes are part of the ABI)
+    L = _lib.load()
+    assert [L.kpx_struct_size(i) for i in range(4)] == [ctypes.sizeof(c) for c in
+                                                        (_lib.Problem, _lib.Stats, _lib.Trace, _lib.QueryResult)]
+    assert _lib.QUERY_RESULT_DTYPE.itemsize == ctypes.sizeof(_lib.QueryResult)
+
+
+def test_product_does_not_import_oracle():
+    """The oracle is a checker: nothing under the package may import or load it."""
+    pkg = os.path.join(ROOT, "paper_2409_06807_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".inl")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "kpx_oracle" not in text and "import oracle" not in text and "ref_loader" not in text, f
