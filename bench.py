@@ -1,0 +1,369 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 Kino-PAX planner on BASELINE.json's metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload di6_forest] [--impl reference]
+
+Metric: plans/s (whole job) plus, in the same JSON line, the median time-to-solution (ms) and the
+success rate over 100 seeds that BASELINE.json quotes.  A *step* is one pass of the hot path over one
+batch of synthetic queries: every GPU plans `--queries` independent queries (seeds) of the workload
+in ONE persistent kernel launch.  `value` times K such launches with CUDA events, queries already
+resident in HBM; `e2e` times the public API call (host buffers in, results + solution chains out)
+with the host<->device copies inside the timed region.  Multi-GPU (torchrun, one rank per GPU): each
+rank plans its own queries -- independent units, no data-path collective, weak scaling.
+
+`--impl reference` times the reference's CPU algorithm on the host cores (the pinned C port under
+oracle/ -- the reference's planner loop is Python and cannot travel to the GPU box).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (model, scene, flops per RK4 substep [SURVEY 8d], queries per GPU per step)
+    "di6_forest": ("di6", "forest", 78, 592),
+    "dubins6_building": ("dubins6", "building", 118, 592),
+    "quad12_narrow": ("quad12", "narrow", 336, 296),
+    "quad12_forest": ("quad12", "forest", 336, 296),
+}
+
+
+def _cfg(kp, model, seed=0, t_max=60.0):
+    return kp.PlannerConfig(t_e=model.default_t_e, lambda_max=32, t_prop=model.default_t_prop, epsilon=0.005,
+                            delta=1.0, cells_per_dim=model.default_cells_per_dim, subcells_per_dim=4, t_max=t_max,
+                            seed=seed)
+
+
+# --------------------------------------------------------------------------------------- CPU arm
+
+def _cpu_solve(args):
+    """Worker (spawned process): one oracle plan.  Returns (seed, status, seconds, items)."""
+    workload, seed = args
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    import paper_2409_06807_b200.core as core
+    from paper_2409_06807_b200 import dynamics, envgen, problem
+    model_name, scene, _, _ = WORKLOADS[workload]
+    model = dynamics.get_model(model_name)
+    env = envgen.gen_environment(scene, model, seed=0)
+    cfg = core.PlannerConfig(t_e=model.default_t_e, t_prop=model.default_t_prop,
+                             cells_per_dim=model.default_cells_per_dim, seed=seed, t_max=120.0)
+    op = oracle.plan_from_problem(problem.build_problem(cfg, env, model))
+    st, el = op.solve(t_max=120.0)
+    return seed, op.status, el, int(op.raw.total_items)
+
+
+def cpu_throughput(workload: str, n_plans: int, procs: int):
+    """plans/s of the CPU oracle: `procs` single-thread worker processes over seeds 0..n_plans-1."""
+    import multiprocessing as mp
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        recs = pool.map(_cpu_solve, [(workload, s) for s in range(n_plans)], chunksize=1)
+    wall = time.perf_counter() - t0
+    solved = [r for r in recs if r[1] == "solved"]
+    return {"plans_per_s": n_plans / wall, "wall_s": wall, "solved": len(solved), "plans": n_plans,
+            "median_plan_s": statistics.median(r[2] for r in recs)}
+
+
+def run_reference(args):
+    """The reference arm: rank 0 only; each step = one plan per host core."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    procs = max(1, min(cores, 64))
+    model_name, scene, _, _ = WORKLOADS[args.workload]
+    steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    for _ in range(warmup):
+        cpu_throughput(args.workload, procs, procs)
+    res = [cpu_throughput(args.workload, procs, procs) for _ in range(steps)]
+    plans = sum(r["plans"] for r in res)
+    wall = sum(r["wall_s"] for r in res)
+    value = plans / wall
+    line = {
+        "impl": "reference", "metric": "plans_per_sec", "value": value, "unit": "plans/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": warmup, "ms_per_step": 1e3 * wall / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{model_name}/{scene} (gen_environment seed 0), default PlannerConfig, "
+                               f"one plan per worker process per step", "queries_per_step": procs},
+        "median_time_to_solution_ms": 1e3 * statistics.median(r["median_plan_s"] for r in res),
+        "success_rate": sum(r["solved"] for r in res) / plans,
+        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": procs, "kind": "port",
+                         "sample": f"{plans} plans (seeds 0..{procs - 1} per step), {procs} single-thread processes "
+                                   f"of the C oracle (bit-exact restatement of the reference planner; steps capped "
+                                   f"at 3 to bound the run)"},
+        "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------- GPU arm
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.proc, self.lines = device, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    model_name, scene, f_step, q_default = WORKLOADS[args.workload]
+    q_per_gpu = args.queries or q_default
+
+    # CPU baseline first (rank 0, N=1 only), before this process touches CUDA: bounded sample, one plan per core
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cores = max(1, min(os.cpu_count() or 1, 64))
+        r = cpu_throughput(args.workload, cores, cores)
+        cpu = {"value": r["plans_per_s"], "unit": "plans/s", "cores": cores, "kind": "port",
+               "sample": f"{r['plans']} plans (seeds 0..{cores - 1}), one single-thread process per core, C oracle "
+                         f"(bit-exact restatement of the reference planner), {r['wall_s']:.1f} s wall, "
+                         f"median {1e3 * r['median_plan_s']:.0f} ms per plan, {r['solved']} solved"}
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2409_06807_b200 as kp
+    from paper_2409_06807_b200 import _lib
+
+    L = _lib.load()
+    model = kp.get_model(model_name)
+    env = kp.gen_environment(scene, model, seed=0)
+    cfg = _cfg(kp, model)
+    stream = torch.cuda.current_stream().cuda_stream
+    sptr = _lib.C.c_void_p(stream)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- latency leg: one query at a time on the whole GPU, seeds 0..99 (BASELINE.json's time-to-solution)
+    lat = None
+    if rank == 0 and not args.no_latency:
+        eng = kp.KinoPax(cfg, env, model, backend=args.backend, device=local)
+        for w in range(3):
+            eng.reset(seed=10_000 + w)
+            eng.solve()
+        dev_ms, wall_ms, ok, reval, reval_fine, iters, trees = [], [], 0, 0, 0, [], []
+        fine = kp.ValidityChecker(env, model, 0.005)
+        coarse = kp.ValidityChecker(env, model, 0.05)
+        for seed in range(args.latency_seeds):
+            eng.reset(seed=seed)
+            res = eng.solve()
+            if res.solved:
+                ok += 1
+                dev_ms.append(res.device["device_ms"]); wall_ms.append(res.stats.wall_time_ms)
+                iters.append(res.stats.iterations); trees.append(res.stats.tree_size)
+                reval += bool(coarse.trajectory_valid(res.trajectory, start=env.start))
+                reval_fine += bool(fine.trajectory_valid(res.trajectory, start=env.start))
+        eng.close()
+        ref_rate = None
+        gold = os.path.join(ROOT, "tests", "golden", f"outcomes_{args.workload}.json")
+        if os.path.isfile(gold):
+            g = json.load(open(gold))
+            n = min(args.latency_seeds, g["seeds"])
+            ref_rate = sum(1 for r in g["records"] if r["seed"] < n and r["status"] == "solved") / n
+        lat = {"seeds": args.latency_seeds, "solved": ok, "success_rate": ok / args.latency_seeds,
+               "reference_success_rate_same_seeds": ref_rate,
+               "median_device_ms": statistics.median(dev_ms) if dev_ms else None,
+               "median_wall_ms": statistics.median(wall_ms) if wall_ms else None,
+               "p90_wall_ms": float(np.percentile(wall_ms, 90)) if wall_ms else None,
+               "median_iterations": statistics.median(iters) if iters else None,
+               "median_tree_size": statistics.median(trees) if trees else None,
+               "revalidated_at_check_resolution": reval, "revalidated_at_fine_resolution": reval_fine}
+
+    # ---- throughput leg
+    bp = kp.BatchPlanner(cfg, env, model, backend=args.backend, team_ctas=args.team_ctas, device=local)
+    seeds = np.arange(q_per_gpu, dtype=np.int64) + rank * q_per_gpu
+    bp.upload(seeds, want_chains=False, stream=sptr)
+    for _ in range(args.warmup):
+        bp.launch(stream=sptr)
+    torch.cuda.synchronize()
+    fp32_peak, fp64_peak = _lib.C.c_double(0), _lib.C.c_double(0)
+    if rank == 0:
+        _lib.check(L.kpx_fma_peak(local, 30.0, _lib.C.byref(fp32_peak), _lib.C.byref(fp64_peak)), "kpx_fma_peak")
+    sampler = ClockSampler(local)
+    barrier()
+    if rank == 0:
+        sampler.start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    ev[0].record()
+    for i in range(args.steps):
+        bp.launch(stream=sptr)
+        ev[i + 1].record()
+    barrier()
+    clocks = sampler.stop() if rank == 0 else None
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    res = bp.download(stream=sptr)
+    rec = res.records
+
+    # ---- e2e leg: the public call with host buffers, copies inside the timed region
+    barrier()
+    bp.run(seeds, want_chains=True, stream=sptr)           # warm the pinned paths
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        r2 = bp.run(seeds, want_chains=True, stream=sptr)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    n, nu = model.n, model.control_dim
+    h2d = q_per_gpu * (8 + 8 * n + 32)
+    d2h = q_per_gpu * (rec.dtype.itemsize + 8 * bp.max_chain * (n + nu + 1))
+
+    # re-validate a sample of batch solutions on the host (float64 rebuild + reference checker rules)
+    checked = okc = 0
+    for q in range(0, q_per_gpu, max(1, q_per_gpu // 64)):
+        if r2.status(q) is kp.PlanStatus.SOLVED:
+            segs, ok = bp.trajectory(r2, q)
+            checked += 1
+            okc += bool(ok)
+    bp.close()
+
+    if rank != 0:
+        return
+    total_plans = q_per_gpu * world * args.steps
+    value = total_plans / (total_ms * 1e-3)
+    n_obs = env.n_obstacles
+    flops = float(rec["substeps"].sum()) * f_step + float(rec["boxsteps"].sum()) * 2 * n + \
+        float(rec["points"].sum()) * (6 + 6 * n_obs)
+    kern_ms = statistics.mean(step_ms)
+    achieved = flops / (kern_ms * 1e-3) / 1e12
+    peak = fp32_peak.value if "f32" in args.backend else fp64_peak.value
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.isfile(prof):
+        traffic = json.load(open(prof)).get(args.workload)
+    line = {
+        "metric": "plans_per_sec", "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if "f32" in args.backend else "f64", "data": "synthetic",
+        "config": {"workload": f"{model_name}/{scene} (gen_environment seed 0; BASELINE.json config: "
+                               f"{'6D double integrator in Trees' if args.workload == 'di6_forest' else args.workload}), "
+                               f"t_e={cfg.t_e}, lambda_max=32, t_prop={cfg.t_prop}, cells={cfg.cells_per_dim}",
+                   "queries_per_gpu_per_step": q_per_gpu, "team_ctas": bp.team_ctas, "teams": bp.n_teams,
+                   "l2": "per-step working set (one arena + region state per team) far exceeds the 126 MB L2",
+                   "backend": args.backend},
+        "median_time_to_solution_ms": lat["median_wall_ms"] if lat else None,
+        "success_rate": lat["success_rate"] if lat else float((rec["status"] == 0).mean()),
+        "time_to_solution": lat,
+        "batch": {"solved": int((rec["status"] == 0).sum()), "queries": int(len(rec)),
+                  "median_iterations": float(np.median(rec["iterations"])),
+                  "median_tree_size": float(np.median(rec["tree_size"])), "revalidated": f"{okc}/{checked}"},
+        "e2e": {"value": q_per_gpu * world * e2e_steps / e2e_s, "unit": "plans/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "fp32" if "f32" in args.backend else "fp64", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "kernel": "kpx::plan_kernel (one persistent launch per step)", "kernel_ms": kern_ms,
+                     "algorithmic_flops_per_launch": flops,
+                     "note": "non-tensor compute bound (no dense contraction): peak = FMA micro-benchmark measured "
+                             "in this run (MEASURED_PEAKS.json holds only HBM / bf16 numbers); achieved counts "
+                             "SURVEY 8(d) algorithmic ops: substeps*F_step + box tests*2n + collision points*(6+6*n_obs)",
+                     "hbm_gbs_measured_peak": _measured_hbm()},
+        "clocks": clocks,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def _measured_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.isfile(p):
+        return json.load(open(p)).get("hbm_gbs")
+    return 6650.0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="di6_forest", choices=sorted(WORKLOADS))
+    ap.add_argument("--backend", default="cuda-f32", choices=["cuda", "cuda-f32"])
+    ap.add_argument("--queries", type=int, default=0, help="queries per GPU per step (default per workload)")
+    ap.add_argument("--team-ctas", type=int, default=1)
+    ap.add_argument("--latency-seeds", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -18,6 +18,8 @@
  *   kpx_plan_snapshot        TreeArena.snapshot                planner.py:92-102
  *   kpx_plan_regions         Decomposition state / dump_rows   decomposition.py:66-74, 219-234
  *   kpx_plan_solution        extract_trajectory (chain walk)   planner.py:325-336
+ *   kpx_trajectory           propagate_ode over the chain       dynamics.py:242-283 (host, float64)
+ *   kpx_trajectory_valid     ValidityChecker.segment_valid     validity.py:86-106 (host, float64)
  *   kpx_plan_trace           IterationTrace records            planner.py:121-131, 290-296
  *   kpx_plan_items           the Batch of the last iteration   backend.py:47-61
  *   kpx_plan_load            (no reference equivalent: restores a tree + region state; checkpoint/resume)
@@ -83,6 +85,7 @@ typedef struct kpx_stats {
     uint64_t items;          /* extensions attempted (sum over iterations) */
     uint64_t substeps;       /* RK4 substeps integrated */
     uint64_t points;         /* collision points tested */
+    uint64_t boxsteps;       /* substeps whose state-box test ran */
     uint64_t launches;       /* kernel launches issued by this call */
 } kpx_stats;
 
@@ -101,6 +104,9 @@ int kpx_version(void);
 /* sizeof of an ABI struct as compiled: 0 kpx_problem, 1 kpx_stats, 2 kpx_trace, 3 kpx_query_result (binding self-check) */
 int kpx_struct_size(int which);
 /* SM count / cooperative-residency facts of the current device (for sizing and for bench.py) */
+/* FP32 FMA micro-benchmark on `device` (the non-tensor roofline denominator): dense fused multiply-adds
+ * on every SM for roughly `ms_target` milliseconds; *tflops counts 2 flops per FMA. */
+int kpx_fma_peak(int device, double ms_target, double *tflops, double *tflops_f64);
 int kpx_device_info(int device, int32_t *sm_count, int32_t *max_coop_blocks_f32, int32_t *max_coop_blocks_f64);
 
 /*
@@ -150,6 +156,19 @@ int kpx_plan_regions(kpx_plan *p, int64_t *n_valid, int64_t *n_invalid, int64_t 
 /* solution chain: for each of chain_len segments the start state (n), control (nu), dt, and the slot */
 int kpx_plan_solution(kpx_plan *p, int64_t max_segments, double *seg_start, double *seg_control,
                       double *seg_dt, int64_t *seg_slot, double *end_state);
+/*
+ * Host-side float64 rebuild of a solution: segment s integrates seg_control[s] for seg_dt[s] with the
+ * reference's fixed-step RK4 (S = max(4, ceil(dt/0.02)) substeps) from seg_start[s] -- or, with
+ * chain_from_root, from the previous segment's end (seg_start[0] = root).  sampled receives
+ * S+1 rows per segment; seg_offset[n_seg+1] the row offsets.  No device work.
+ */
+int kpx_trajectory(int32_t model_id, int32_t n, int32_t nu, int64_t n_seg, const double *seg_start,
+                   const double *seg_control, const double *seg_dt, int32_t chain_from_root,
+                   double *sampled, int64_t max_rows, int64_t *seg_offset);
+/* Host-side check of a rebuilt trajectory with the reference checker's rules (validity.py:58-106, closed
+ * boxes, power-of-two densification at `res`) plus the closed goal ball; *ok = 1/0, *fail_code 3 segment / 4 goal. */
+int kpx_trajectory_valid(const kpx_problem *prob, int64_t n_seg, const double *sampled, const int64_t *seg_offset,
+                         const double *goal4, double res, int32_t *ok, int32_t *fail_code);
 int kpx_plan_trace(kpx_plan *p, int32_t max_records, kpx_trace *out, int32_t *n_records);
 /* the last iteration's per-item results in Batch layout + keep flag and parent slot (debug/parity) */
 int kpx_plan_items(kpx_plan *p, int64_t max_items, int64_t *n_items, uint8_t *valid, int64_t *region,
@@ -170,7 +189,7 @@ typedef struct kpx_query_result {
     int32_t status, iterations;
     int64_t tree_size, solution_slot, chain_len;
     double device_ms;
-    uint64_t items, substeps, points;
+    uint64_t items, substeps, points, boxsteps;
 } kpx_query_result;
 
 int kpx_batch_create(const kpx_problem *prob, int32_t precision, int32_t n_teams, int32_t team_ctas,
@@ -180,6 +199,14 @@ void kpx_batch_destroy(kpx_batch *b);
 int kpx_batch_run(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const double *starts,
                   const double *goals, double t_max, kpx_query_result *results, double *chain_start,
                   double *chain_control, double *chain_dt, double *o_kernel_ms, void *stream);
+
+/* the same in three stream-ordered pieces, so a caller can keep queries resident and re-launch:
+ * upload (H2D, synchronous), launch (asynchronous, one persistent kernel), download (D2H, synchronises) */
+int kpx_batch_upload(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const double *starts,
+                     const double *goals, int32_t want_chains, void *stream);
+int kpx_batch_launch(kpx_batch *b, double t_max, void *stream);
+int kpx_batch_download(kpx_batch *b, kpx_query_result *results, double *chain_start, double *chain_control,
+                       double *chain_dt, void *stream);
 
 #ifdef __cplusplus
 }

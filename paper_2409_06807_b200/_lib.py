@@ -42,7 +42,7 @@ class Stats(C.Structure):
     _fields_ = [
         ("status", C.c_int32), ("iterations", C.c_int32), ("tree_size", C.c_int64), ("solution_slot", C.c_int64),
         ("chain_len", C.c_int64), ("device_ms", C.c_double), ("reset_ms", C.c_double),
-        ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("launches", C.c_uint64),
+        ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("boxsteps", C.c_uint64), ("launches", C.c_uint64),
     ]
 
 
@@ -58,19 +58,20 @@ class QueryResult(C.Structure):
     _fields_ = [
         ("status", C.c_int32), ("iterations", C.c_int32), ("tree_size", C.c_int64), ("solution_slot", C.c_int64),
         ("chain_len", C.c_int64), ("device_ms", C.c_double),
-        ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64),
+        ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("boxsteps", C.c_uint64),
     ]
 
 
 QUERY_RESULT_DTYPE = np.dtype([
     ("status", np.int32), ("iterations", np.int32), ("tree_size", np.int64), ("solution_slot", np.int64),
     ("chain_len", np.int64), ("device_ms", np.float64), ("items", np.uint64), ("substeps", np.uint64),
-    ("points", np.uint64)], align=True)
+    ("points", np.uint64), ("boxsteps", np.uint64)], align=True)
 
 _SIGNATURES = {
     "kpx_last_error": (C.c_char_p, []),
     "kpx_version": (C.c_int, []),
     "kpx_struct_size": (C.c_int, [C.c_int]),
+    "kpx_fma_peak": (C.c_int, [C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "kpx_device_info": (C.c_int, [C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kpx_propagate_batch": (C.c_int, [C.POINTER(Problem), _vp, C.c_int64, _vp, C.c_int64, C.c_int32, C.c_uint64,
                                       C.c_uint64, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -83,12 +84,19 @@ _SIGNATURES = {
     "kpx_plan_snapshot": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kpx_plan_regions": (C.c_int, [_vp] * 9),
     "kpx_plan_solution": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp]),
+    "kpx_trajectory": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, _vp, _vp, _vp, C.c_int32, _vp, C.c_int64,
+                                 _vp]),
+    "kpx_trajectory_valid": (C.c_int, [C.POINTER(Problem), C.c_int64, _vp, _vp, _vp, C.c_double,
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kpx_plan_trace": (C.c_int, [_vp, C.c_int32, _vp, C.POINTER(C.c_int32)]),
     "kpx_plan_items": (C.c_int, [_vp, C.c_int64, C.POINTER(C.c_int64), _vp, _vp, _vp, _vp, _vp, _vp]),
     "kpx_plan_load": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int32, C.c_int64] + [_vp] * 13),
     "kpx_batch_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                    C.POINTER(_vp)]),
     "kpx_batch_destroy": (None, [_vp]),
+    "kpx_batch_upload": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_int32, _vp]),
+    "kpx_batch_launch": (C.c_int, [_vp, C.c_double, _vp]),
+    "kpx_batch_download": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "kpx_batch_run": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, _vp,
                                 C.POINTER(C.c_double), _vp]),
 }

@@ -1,0 +1,291 @@
+"""Many independent planning queries per launch, sharding across GPUs, and the OR-parallel race.
+
+The reference plans one query per process and parallelises trials only for its
+baseline planner (``bench.py:106-150``, ``rrt.py:139-157``).  Queries are
+independent, so here:
+
+* ``BatchPlanner`` keeps ``n_teams`` device workspaces; one persistent launch
+  (``kpx_batch_run``) lets teams of ``team_ctas`` CTAs pull queries from a
+  device-side queue until it is drained.  No collective is involved.
+* ``shard_queries`` assigns query ``q`` to rank ``q mod world``; each
+  rank plans its shard on its own GPU and the few bytes of per-query results are
+  gathered once at the end, off the clock.
+* ``RaceFlags`` wires the OR-parallel race: every rank polls a 4-byte device word
+  once per iteration; the first rank to solve stores 1 into every peer's word
+  over NVLink peer memory (``st.volatile`` + ``__threadfence_system`` in the kernel).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .backend import get_backend
+from .core import ConfigError, Environment, PlannerConfig, PlanStatus, TrajectorySegment
+from .dynamics import DynamicsModel
+from .problem import build_problem
+
+_STATUS = {_lib.SOLVED: PlanStatus.SOLVED, _lib.TIMEOUT: PlanStatus.TIMEOUT,
+           _lib.CAPACITY_EXHAUSTED: PlanStatus.CAPACITY_EXHAUSTED, _lib.ERROR: PlanStatus.ERROR,
+           _lib.STOPPED: PlanStatus.TIMEOUT}
+
+
+@dataclass
+class BatchResult:
+    """Per-query outcomes of one ``BatchPlanner.run`` (arrays of length Q)."""
+
+    records: np.ndarray            # structured: status, iterations, tree_size, solution_slot, chain_len, device_ms, ...
+    chain_start: Optional[np.ndarray]   # (Q, max_chain, n)
+    chain_control: Optional[np.ndarray]  # (Q, max_chain, nu)
+    chain_dt: Optional[np.ndarray]      # (Q, max_chain)
+    kernel_ms: float
+    wall_ms: float
+    starts: np.ndarray
+    goals: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.records)
+
+    def status(self, q: int) -> PlanStatus:
+        return _STATUS.get(int(self.records["status"][q]), PlanStatus.ERROR)
+
+    @property
+    def solved(self) -> np.ndarray:
+        return self.records["status"] == _lib.SOLVED
+
+    @property
+    def success_rate(self) -> float:
+        return float(self.solved.mean()) if len(self.records) else 0.0
+
+
+class BatchPlanner:
+    """Persistent multi-query planner bound to one GPU."""
+
+    def __init__(self, cfg: PlannerConfig, env: Environment, model: DynamicsModel, check_resolution: float = 0.05,
+                 backend: Optional[str] = None, n_teams: int = 0, team_ctas: int = 1, max_chain: int = 64,
+                 device: int = 0):
+        self.problem = build_problem(cfg, env, model, check_resolution)
+        self.cfg, self.env, self.model = cfg, env, model
+        self.precision = get_backend(backend, model).precision
+        self._lib = _lib.load()
+        self._prob_struct, self._keep = _lib.problem_from(self.problem)
+        if n_teams <= 0:
+            sm, f32b, f64b = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+            _lib.check(self._lib.kpx_device_info(device, C.byref(sm), C.byref(f32b), C.byref(f64b)), "kpx_device_info")
+            resident = f32b.value if self.precision == _lib.F32 else f64b.value
+            n_teams = max(1, resident // max(1, team_ctas))
+        self.n_teams, self.team_ctas, self.max_chain, self.device = int(n_teams), int(team_ctas), int(max_chain), device
+        self._handle = _lib._vp()
+        _lib.check(self._lib.kpx_batch_create(C.byref(self._prob_struct), self.precision, self.n_teams, self.team_ctas,
+                                              self.max_chain, int(device), C.byref(self._handle)), "kpx_batch_create")
+
+    def close(self) -> None:
+        if getattr(self, "_handle", None):
+            self._lib.kpx_batch_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def run(self, seeds: Sequence[int], starts=None, goals=None, t_max: Optional[float] = None,
+            want_chains: bool = True, stream=None) -> BatchResult:
+        """Plan ``len(seeds)`` queries; ``starts`` (Q, n) / ``goals`` (Q, 4) default to the environment's."""
+        q = len(seeds)
+        if q < 1:
+            raise ConfigError("need at least one query")
+        n, nu = self.model.n, self.model.control_dim
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64).astype(np.uint64))
+        starts = np.ascontiguousarray(np.tile(self.env.start, (q, 1)) if starts is None else starts, dtype=np.float64)
+        goals = np.ascontiguousarray(np.tile(self.problem.goal4, (q, 1)) if goals is None else goals, dtype=np.float64)
+        if starts.shape != (q, n) or goals.shape != (q, 4):
+            raise ConfigError("starts must be (Q, n) and goals (Q, 4)")
+        rec = np.zeros(q, dtype=_lib.QUERY_RESULT_DTYPE)
+        cs = cc = cd = None
+        if want_chains:
+            cs = np.zeros((q, self.max_chain, n))
+            cc = np.zeros((q, self.max_chain, nu))
+            cd = np.zeros((q, self.max_chain))
+        ms = C.c_double(0.0)
+        t0 = time.perf_counter()
+        _lib.check(self._lib.kpx_batch_run(self._handle, q, _lib.ptr(seeds), _lib.ptr(starts), _lib.ptr(goals),
+                                           float(self.cfg.t_max if t_max is None else t_max), _lib.ptr(rec),
+                                           _lib.ptr(cs), _lib.ptr(cc), _lib.ptr(cd), C.byref(ms), stream),
+                   "kpx_batch_run")
+        wall = (time.perf_counter() - t0) * 1e3
+        return BatchResult(rec, cs, cc, cd, ms.value, wall, starts, goals)
+
+    # -- resident-input form: upload once, launch many times (what bench.py times with CUDA events) ---
+    def upload(self, seeds, starts=None, goals=None, want_chains: bool = False, stream=None) -> int:
+        q = len(seeds)
+        n = self.model.n
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64).astype(np.uint64))
+        starts = np.ascontiguousarray(np.tile(self.env.start, (q, 1)) if starts is None else starts, dtype=np.float64)
+        goals = np.ascontiguousarray(np.tile(self.problem.goal4, (q, 1)) if goals is None else goals, dtype=np.float64)
+        if starts.shape != (q, n) or goals.shape != (q, 4):
+            raise ConfigError("starts must be (Q, n) and goals (Q, 4)")
+        _lib.check(self._lib.kpx_batch_upload(self._handle, q, _lib.ptr(seeds), _lib.ptr(starts), _lib.ptr(goals),
+                                              1 if want_chains else 0, stream), "kpx_batch_upload")
+        self._uploaded = (q, starts, goals, want_chains)
+        return q
+
+    def launch(self, t_max: Optional[float] = None, stream=None) -> None:
+        _lib.check(self._lib.kpx_batch_launch(self._handle, float(self.cfg.t_max if t_max is None else t_max), stream),
+                   "kpx_batch_launch")
+
+    def download(self, stream=None) -> BatchResult:
+        q, starts, goals, want = self._uploaded
+        n, nu = self.model.n, self.model.control_dim
+        rec = np.zeros(q, dtype=_lib.QUERY_RESULT_DTYPE)
+        cs = np.zeros((q, self.max_chain, n)) if want else None
+        cc = np.zeros((q, self.max_chain, nu)) if want else None
+        cd = np.zeros((q, self.max_chain)) if want else None
+        _lib.check(self._lib.kpx_batch_download(self._handle, _lib.ptr(rec), _lib.ptr(cs), _lib.ptr(cc), _lib.ptr(cd),
+                                                stream), "kpx_batch_download")
+        return BatchResult(rec, cs, cc, cd, 0.0, 0.0, starts, goals)
+
+    # -- host-side rebuild / re-validation of one solution ------------------------------------------
+    def trajectory(self, result: BatchResult, q: int) -> tuple:
+        """(segments, ok): float64 rebuild of query q's solution from its chain; ok = collision-free and in goal."""
+        L = int(result.records["chain_len"][q])
+        if result.status(q) is not PlanStatus.SOLVED or L <= 0 or result.chain_dt is None:
+            return [], result.status(q) is PlanStatus.SOLVED and L == 0
+        n, nu = self.model.n, self.model.control_dim
+        dts = np.ascontiguousarray(result.chain_dt[q, :L])
+        ctrl = np.ascontiguousarray(result.chain_control[q, :L])
+        starts = np.ascontiguousarray(result.chain_start[q, :L])
+        from_root = self.precision != _lib.F64
+        if from_root:
+            starts[0] = result.starts[q]
+        rows = int((np.maximum(4, np.ceil(dts / 0.02)) + 1).sum())
+        sampled, off = np.empty((rows, n)), np.zeros(L + 1, np.int64)
+        _lib.check(self._lib.kpx_trajectory(self.model.kernel_id, n, nu, L, _lib.ptr(starts), _lib.ptr(ctrl),
+                                            _lib.ptr(dts), 1 if from_root else 0, _lib.ptr(sampled), rows,
+                                            _lib.ptr(off)), "kpx_trajectory")
+        okc, code = C.c_int32(0), C.c_int32(0)
+        goal = np.ascontiguousarray(result.goals[q])
+        _lib.check(self._lib.kpx_trajectory_valid(C.byref(self._prob_struct), L, _lib.ptr(sampled), _lib.ptr(off),
+                                                  _lib.ptr(goal), self.problem.check_resolution, C.byref(okc),
+                                                  C.byref(code)), "kpx_trajectory_valid")
+        segs = [TrajectorySegment(control=ctrl[i].copy(), dt=float(dts[i]), end_state=sampled[off[i + 1] - 1].copy(),
+                                  sampled_states=sampled[off[i]:off[i + 1]]) for i in range(L)]
+        return segs, bool(okc.value)
+
+
+def plan_batch(cfg: PlannerConfig, env: Environment, model: DynamicsModel, seeds: Sequence[int], starts=None,
+               goals=None, check_resolution: float = 0.05, backend: Optional[str] = None, **kw) -> BatchResult:
+    """One-shot convenience wrapper: plan all queries on the current GPU."""
+    with BatchPlanner(cfg, env, model, check_resolution, backend, **kw) as bp:
+        return bp.run(seeds, starts, goals)
+
+
+# ---------------------------------------------------------------------------- multi-GPU plumbing
+
+def shard_queries(n_queries: int, rank: int, world: int) -> np.ndarray:
+    """Indices of the queries rank ``rank`` plans: q mod world == rank (independent units, no exchange)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return np.arange(rank, n_queries, world, dtype=np.int64)
+
+
+def gather_records(local_idx: np.ndarray, local_records: np.ndarray, n_queries: int, group=None) -> Optional[np.ndarray]:
+    """Collect per-query records on rank 0 with one ``gather_object`` (tens of bytes per query, off the clock).
+
+    Works with any ``torch.distributed`` backend (NCCL on the GPU box, gloo in the CPU tests)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    payload = (np.asarray(local_idx), np.asarray(local_records))
+    out = [None] * world if rank == 0 else None
+    dist.gather_object(payload, out, dst=0, group=group)
+    if rank != 0:
+        return None
+    full = np.zeros(n_queries, dtype=local_records.dtype)
+    seen = np.zeros(n_queries, dtype=bool)
+    for idx, rec in out:
+        full[idx] = rec
+        seen[idx] = True
+    if not seen.all():
+        raise RuntimeError("some queries were not planned by any rank")
+    return full
+
+
+def goal_for_query(q: int, env: Environment, radius: float = 1.3, min_dist: float = 4.0, margin: float = 0.4) -> np.ndarray:
+    """Deterministic random goal of query q (SURVEY config 5): centre uniform in [1,9]^3 from the GENERIC
+    stream of seed q, rejected if within radius+margin of an obstacle (in x-y) or closer than min_dist to the start."""
+    from .rng import PHASE_GENERIC, RngStream
+    s = RngStream(q, phase=PHASE_GENERIC)
+    start = env.start[:3]
+    for _ in range(1000):
+        c = np.array([s.uniform_in(1.0, 9.0) for _ in range(3)])
+        if np.sqrt(((c - start) ** 2).sum()) < min_dist:
+            continue
+        if env.n_obstacles:
+            lo, hi = env.obstacles_min - (radius + margin), env.obstacles_max + (radius + margin)
+            if ((c >= lo) & (c <= hi)).all(axis=1).any():
+                continue
+        return np.array([c[0], c[1], c[2], radius])
+    raise ConfigError("could not sample a goal for this scene")
+
+
+class RaceFlags:
+    """Stop words of an OR-parallel race across the ranks of one node.
+
+    Each rank owns one 32-bit device word and polls it once per iteration.  The words are
+    shared through CUDA IPC handles exchanged with ``all_gather_object``; the winner's kernel
+    writes 1 into every peer word directly over NVLink (NVSwitch makes every peer one hop; for
+    4 bytes only the ~2 us store latency matters).  With world size 1 it degenerates to a
+    private flag, which is what the single-GPU tests exercise.
+    """
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch = torch
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.flag = torch.zeros(64, dtype=torch.int32, device="cuda")   # own word (padded to a cache line)
+        self.peer_ptrs = []
+        self._peer_tensors = []
+        if self.world > 1:
+            handle = self.flag.untyped_storage()._share_cuda_()
+            handles = [None] * self.world
+            dist.all_gather_object(handles, (self.rank, handle), group=group)
+            for r, h in handles:
+                if r == self.rank:
+                    continue
+                storage = torch.UntypedStorage._new_shared_cuda(*h)
+                t = torch.empty(0, dtype=torch.int32, device=storage.device).set_(storage)
+                self._peer_tensors.append(t)
+                self.peer_ptrs.append(t.data_ptr())
+
+    def clear(self) -> None:
+        self.flag.zero_()
+        self.torch.cuda.synchronize()
+
+    @property
+    def own_ptr(self) -> int:
+        return self.flag.data_ptr()
+
+    def fired(self) -> bool:
+        return bool(self.flag[0].item())
+
+
+def race(engine, flags: "RaceFlags", seed: int, t_max: Optional[float] = None):
+    """One rank's leg of the race: plan with ``seed`` until solved or a peer's store stops us."""
+    engine.reset(seed=seed)
+    st = engine._run(engine.cfg.t_max if t_max is None else t_max, stop_flag=C.c_void_p(flags.own_ptr),
+                     peer_flags=[p for p in flags.peer_ptrs])
+    return st

@@ -19,7 +19,7 @@ OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(PKG, "libkpx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-relaxed-constexpr"]
 UNITS = [
     ("kpx_inst_f64.cu", ["-fmad=false"]),
     ("kpx_inst_f32.cu", []),

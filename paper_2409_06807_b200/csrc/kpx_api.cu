@@ -101,6 +101,9 @@ struct kpx_batch {
     kpx_query_result* r_dev = nullptr;
     long long q_cap = 0;
     double *bc_start = nullptr, *bc_ctrl = nullptr, *bc_dt = nullptr;
+    long long bc_cap = 0, n_uploaded = 0;
+    bool want_chains = false;
+    std::vector<QueryIn> q_stage;
     uint32_t** peers_dev = nullptr;
     int peers_cap = 0;
     // single-plan state
@@ -108,6 +111,9 @@ struct kpx_batch {
     bool loaded = false;
     QueryIn q_host;
     unsigned long long launches = 0;
+    ResultPacket* pk_host = nullptr;   // pinned
+    QueryIn* q_pinned = nullptr;       // pinned
+    bool pk_valid = false;
 };
 
 struct kpx_plan { kpx_batch b; };
@@ -118,6 +124,7 @@ void destroy_batch(kpx_batch& b) {
     cudaSetDevice(b.device);
     cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
     cudaFree(b.r_dev); cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt); cudaFree(b.peers_dev);
+    cudaFreeHost(b.pk_host); cudaFreeHost(b.q_pinned);
 }
 
 int blocks_per_sm(const kpx_batch& b) {
@@ -170,7 +177,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     Carver c;
     struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, it_end,
                         it_code, it_rank, it_parent, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
-                        ch_dt, ch_slot, ch_end; } o;
+                        ch_dt, ch_slot, ch_end, packet; } o;
     o.states = c.take(b.rs * n * cp); o.control = c.take(b.rs * nu * cp); o.dt = c.take(b.rs * cp);
     o.parent = c.take(4 * cp); o.region = c.take(4 * cp); o.tag = c.take(cp);
     o.n_valid = c.take(4 * R); o.n_invalid = c.take(4 * R); o.cov = c.take(4 * R); o.avail = c.take(4 * R);
@@ -181,6 +188,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     o.trace = c.take(sizeof(kpx_trace) * (size_t)b.max_trace);
     o.ch_start = c.take(8 * (size_t)b.max_chain * n); o.ch_ctrl = c.take(8 * (size_t)b.max_chain * nu);
     o.ch_dt = c.take(8 * (size_t)b.max_chain); o.ch_slot = c.take(8 * (size_t)b.max_chain); o.ch_end = c.take(8 * n);
+    o.packet = c.take(sizeof(ResultPacket));
     b.ws_bytes = align_up(c.off, 4096);
     if (cudaMalloc(&b.slab, b.ws_bytes * (size_t)n_teams) != cudaSuccess) {
         cudaGetLastError();
@@ -203,6 +211,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         w.chain_start = (double*)(s + o.ch_start); w.chain_control = (double*)(s + o.ch_ctrl);
         w.chain_dt = (double*)(s + o.ch_dt); w.chain_slot = (long long*)(s + o.ch_slot);
         w.chain_end = (double*)(s + o.ch_end);
+        w.packet = (ResultPacket*)(s + o.packet);
     }
     CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
     CU(cudaMemcpy(b.ws_dev, b.ws_host.data(), sizeof(Workspace) * (size_t)n_teams, cudaMemcpyHostToDevice));
@@ -211,6 +220,8 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     if (rc) return rc;
     CU(cudaMalloc(&b.queue_dev, 256));
     CU(cudaMemset(b.queue_dev, 0, 256));
+    CU(cudaMallocHost(&b.pk_host, sizeof(ResultPacket)));
+    CU(cudaMallocHost(&b.q_pinned, sizeof(QueryIn)));
     return KPX_OK;
 }
 
@@ -277,7 +288,62 @@ int read_ctl(const kpx_batch& b, Ctl* out) {
 
 }  // namespace
 
+namespace {
+template <class T>
+__global__ void fma_peak_kernel(T* out, int iters, T a, T b) {
+    T x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = (T)(threadIdx.x + i) * (T)1e-3;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = x[i] * a + b;
+        }
+    }
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == (T)123.456) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <class T>
+int measure_fma(int sms, double ms_target, double* tflops) {
+    T* d = nullptr;
+    const int blocks = sms * 8, threads = 256;
+    CU(cudaMalloc(&d, sizeof(T) * (size_t)blocks * threads));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
+    int iters = 2000;
+    double best = 0.0;
+    for (int rep = 0; rep < 6; ++rep) {
+        CU(cudaEventRecord(e0));
+        fma_peak_kernel<T><<<blocks, threads>>>(d, iters, (T)1.000001, (T)1e-7);
+        CU(cudaEventRecord(e1));
+        CU(cudaEventSynchronize(e1));
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+        if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+        if (ms < ms_target) iters = (int)std::min(2.0e6, iters * std::max(1.5, ms_target / std::max(ms, 1e-3f)));
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaFree(d);
+    *tflops = best;
+    return KPX_OK;
+}
+}  // namespace
+
 extern "C" {
+
+int kpx_fma_peak(int device, double ms_target, double* tflops, double* tflops_f64) {
+    cudaDeviceProp dp;
+    CU(cudaGetDeviceProperties(&dp, device));
+    CU(cudaSetDevice(device));
+    int rc = KPX_OK;
+    if (tflops && (rc = measure_fma<float>(dp.multiProcessorCount, ms_target, tflops))) return rc;
+    if (tflops_f64 && (rc = measure_fma<double>(dp.multiProcessorCount, ms_target, tflops_f64))) return rc;
+    return KPX_OK;
+}
 
 const char* kpx_last_error(void) { return g_err.c_str(); }
 int kpx_version(void) { return 100; }
@@ -389,7 +455,7 @@ int kpx_plan_reset(kpx_plan* p, uint64_t seed, const double* start, const double
     b.q_host.seed = seed;
     memcpy(b.q_host.start, start, sizeof(double) * b.prob.n);
     memcpy(b.q_host.goal, goal4, sizeof(double) * 4);
-    b.fresh = true; b.loaded = false;
+    b.fresh = true; b.loaded = false; b.pk_valid = false;
     return KPX_OK;
 }
 
@@ -426,18 +492,24 @@ int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_overr
         L.peer_flags = b.peers_dev; L.n_peers = n_peers;
     }
     const unsigned long long l0 = b.launches;
-    if (b.fresh) CU(cudaMemcpyAsync(b.q_dev, &b.q_host, sizeof(QueryIn), cudaMemcpyHostToDevice, st));
+    if (b.fresh) {
+        *b.q_pinned = b.q_host;
+        CU(cudaMemcpyAsync(b.q_dev, b.q_pinned, sizeof(QueryIn), cudaMemcpyHostToDevice, st));
+    }
     int rc = launch(b, L, st);
     if (rc) return rc;
     b.fresh = false;
-    Ctl c;
-    CU(cudaMemcpyAsync(&c, b.ws_host[0].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    b.pk_valid = false;
+    CU(cudaMemcpyAsync(b.pk_host, b.ws_host[0].packet, sizeof(ResultPacket), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    b.pk_valid = true;
+    const Ctl& c = b.pk_host->ctl;
     out->status = c.status; out->iterations = c.iteration; out->tree_size = c.size;
     out->solution_slot = c.solution_slot; out->chain_len = c.chain_len;
     out->device_ms = (double)(c.t_end - c.t_reset_done) * 1e-6;
     out->reset_ms = (double)(c.t_reset_done - c.t_begin) * 1e-6;
     out->items = c.sum_items; out->substeps = c.sum_substeps; out->points = c.sum_points;
+    out->boxsteps = c.sum_boxsteps;
     out->launches = b.launches - l0;
     return KPX_OK;
 }
@@ -513,6 +585,17 @@ int kpx_plan_solution(kpx_plan* p, int64_t max_segments, double* seg_start, doub
     if (c.chain_len > max_segments) return fail(KPX_E_ARG, "need room for %d segments", c.chain_len);
     const Workspace& w = b.ws_host[0];
     const size_t L = (size_t)c.chain_len;
+    if (L && b.pk_valid && L <= (size_t)kPacketSegs) {       // already on the host: no further copies
+        const ResultPacket& pk = *b.pk_host;
+        for (size_t i = 0; i < L; ++i) {
+            if (seg_start) memcpy(seg_start + i * b.prob.n, pk.seg_start[i], 8 * (size_t)b.prob.n);
+            if (seg_control) memcpy(seg_control + i * b.prob.nu, pk.seg_control[i], 8 * (size_t)b.prob.nu);
+            if (seg_dt) seg_dt[i] = pk.seg_dt[i];
+            if (seg_slot) seg_slot[i] = pk.seg_slot[i];
+        }
+        if (end_state) memcpy(end_state, pk.end_state, 8 * (size_t)b.prob.n);
+        return KPX_OK;
+    }
     if (L) {
         if (seg_start) CU(cudaMemcpy(seg_start, w.chain_start, 8 * L * b.prob.n, cudaMemcpyDeviceToHost));
         if (seg_control) CU(cudaMemcpy(seg_control, w.chain_control, 8 * L * b.prob.nu, cudaMemcpyDeviceToHost));
@@ -624,7 +707,124 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     b.q_host.seed = seed;
     memcpy(b.q_host.goal, goal4, 4 * sizeof(double));
     CU(cudaMemcpy(b.q_dev, &b.q_host, sizeof(QueryIn), cudaMemcpyHostToDevice));
-    b.loaded = true; b.fresh = false;
+    b.loaded = true; b.fresh = false; b.pk_valid = false;
+    return KPX_OK;
+}
+
+// ------------------------------------------------------------------ host-side trajectory rebuild
+namespace {
+double wrap_pi(double a) {
+    const double PI = 3.14159265358979323846;
+    double t = fmod(a + PI, 2.0 * PI);
+    if (t <= 0.0) t += 2.0 * PI;
+    return t - PI;
+}
+// vector fields in float64 with the reference's expression shapes (dynamics.py:105-159)
+void host_deriv(int model_id, int n, const double* x, const double* u, double* o) {
+    if (model_id == KPX_MODEL_DI6 || model_id == KPX_MODEL_STACKED_DI) {
+        for (int b = 0; b < n / 6; ++b)
+            for (int a = 0; a < 3; ++a) { o[6 * b + a] = x[6 * b + 3 + a]; o[6 * b + 3 + a] = u[3 * b + a]; }
+    } else if (model_id == KPX_MODEL_DUBINS6) {
+        const double v = x[3], ct = cos(x[4]), st = sin(x[4]), cg = cos(x[5]), sg = sin(x[5]);
+        o[0] = v * ct * cg; o[1] = v * st * cg; o[2] = v * sg; o[3] = u[0]; o[4] = u[1]; o[5] = u[2];
+    } else {
+        const double cphi = cos(x[6]), sphi = sin(x[6]), cth = cos(x[7]), sth = sin(x[7]), cpsi = cos(x[8]), spsi = sin(x[8]);
+        const double p = x[9], q = x[10], r = x[11], acc = u[0] / 1.0;
+        o[0] = x[3]; o[1] = x[4]; o[2] = x[5];
+        o[3] = acc * (cphi * sth * cpsi + sphi * spsi);
+        o[4] = acc * (cphi * sth * spsi - sphi * cpsi);
+        o[5] = acc * (cphi * cth) - 9.81;
+        const double sw = q * sphi + r * cphi;
+        o[6] = p + sw * (sth / cth);
+        o[7] = q * cphi - r * sphi;
+        o[8] = sw / cth;
+        o[9] = (u[1] - (0.02 - 0.01) * q * r) / 0.01;
+        o[10] = (u[2] - (0.01 - 0.02) * p * r) / 0.01;
+        o[11] = (u[3] - (0.01 - 0.01) * p * q) / 0.02;
+    }
+}
+}  // namespace
+
+int kpx_trajectory(int32_t model_id, int32_t n, int32_t nu, int64_t n_seg, const double* seg_start,
+                   const double* seg_control, const double* seg_dt, int32_t chain_from_root, double* sampled,
+                   int64_t max_rows, int64_t* seg_offset) {
+    if (n > KPX_MAX_DIM || nu > KPX_MAX_CONTROL || n < 6 || !seg_start || !seg_control || !seg_dt || !sampled || !seg_offset)
+        return fail(KPX_E_ARG, "bad trajectory arguments");
+    if ((model_id == KPX_MODEL_DUBINS6 && n != 6) || (model_id == KPX_MODEL_QUAD12 && n != 12) || model_id < 0 ||
+        model_id > KPX_MODEL_STACKED_DI) return fail(KPX_E_ARG, "bad model");
+    int64_t row = 0;
+    double cur[KPX_MAX_DIM], tmp[KPX_MAX_DIM], k1[KPX_MAX_DIM], k2[KPX_MAX_DIM], k3[KPX_MAX_DIM], k4[KPX_MAX_DIM];
+    for (int64_t s = 0; s < n_seg; ++s) {
+        const double dt = seg_dt[s];
+        if (!(dt > 0.0)) return fail(KPX_E_ARG, "dt must be positive");
+        int S = (int)ceil(dt / 0.02);                                  // dynamics.py:237-239
+        if (S < 4) S = 4;
+        if (row + S + 1 > max_rows) return fail(KPX_E_ARG, "sampled buffer too small");
+        const double h = dt / S, hh = 0.5 * h, h6 = h / 6.0;
+        const double* u = seg_control + s * nu;
+        if (!(chain_from_root && s > 0)) memcpy(cur, seg_start + s * n, sizeof(double) * n);
+        seg_offset[s] = row;
+        memcpy(sampled + row * n, cur, sizeof(double) * n); ++row;
+        for (int i = 0; i < S; ++i) {                                  // dynamics.py:270-282
+            host_deriv(model_id, n, cur, u, k1);
+            for (int d = 0; d < n; ++d) tmp[d] = cur[d] + hh * k1[d];
+            host_deriv(model_id, n, tmp, u, k2);
+            for (int d = 0; d < n; ++d) tmp[d] = cur[d] + hh * k2[d];
+            host_deriv(model_id, n, tmp, u, k3);
+            for (int d = 0; d < n; ++d) tmp[d] = cur[d] + h * k3[d];
+            host_deriv(model_id, n, tmp, u, k4);
+            for (int d = 0; d < n; ++d) cur[d] = cur[d] + h6 * (k1[d] + 2.0 * k2[d] + 2.0 * k3[d] + k4[d]);
+            if (model_id == KPX_MODEL_DUBINS6) cur[4] = wrap_pi(cur[4]);
+            else if (model_id == KPX_MODEL_QUAD12) { cur[6] = wrap_pi(cur[6]); cur[7] = wrap_pi(cur[7]); cur[8] = wrap_pi(cur[8]); }
+            memcpy(sampled + row * n, cur, sizeof(double) * n); ++row;
+        }
+    }
+    seg_offset[n_seg] = row;
+    return KPX_OK;
+}
+
+// validity.py:58-106 + in_goal on a rebuilt trajectory (host, float64): every sampled state finite, inside
+// the state box and outside every closed obstacle box; interpolants at the power-of-two densification of
+// `res`; last state inside the closed goal ball.  *fail_code: 0 ok, 3 segment invalid, 4 goal missed.
+int kpx_trajectory_valid(const kpx_problem* prob, int64_t n_seg, const double* sampled, const int64_t* seg_offset,
+                         const double* goal4, double res, int32_t* ok, int32_t* fail_code) {
+    if (!prob || !sampled || !seg_offset || !goal4 || !ok || !(res > 0.0)) return fail(KPX_E_ARG, "bad arguments");
+    const int n = prob->n, k = prob->n_obs;
+    auto state_ok = [&](const double* x) {
+        for (int d = 0; d < n; ++d) if (!std::isfinite(x[d])) return false;
+        for (int d = 0; d < n; ++d) if (x[d] < prob->state_lo[d] || x[d] > prob->state_hi[d]) return false;
+        for (int j = 0; j < k; ++j) {
+            const double *a = prob->obs_min + 3 * j, *b = prob->obs_max + 3 * j;
+            if (x[0] >= a[0] && x[0] <= b[0] && x[1] >= a[1] && x[1] <= b[1] && x[2] >= a[2] && x[2] <= b[2]) return false;
+        }
+        return true;
+    };
+    *ok = 1;
+    if (fail_code) *fail_code = 0;
+    double st[KPX_MAX_DIM];
+    for (int64_t s = 0; s < n_seg && *ok; ++s) {
+        for (int64_t r = seg_offset[s]; r < seg_offset[s + 1] && *ok; ++r) {
+            const double* b = sampled + r * n;
+            if (!state_ok(b)) { *ok = 0; break; }
+            if (r == seg_offset[s]) continue;
+            const double* a = b - n;
+            const double d0 = b[0] - a[0], d1 = b[1] - a[1], d2 = b[2] - a[2];
+            const double dist = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+            int64_t m = 1;
+            while ((double)m * res < dist) m <<= 1;
+            for (int64_t j = 1; j < m && *ok; ++j) {
+                const double t = (double)j / (double)m;
+                for (int d = 0; d < n; ++d) st[d] = a[d] + t * (b[d] - a[d]);
+                if (!state_ok(st)) *ok = 0;
+            }
+        }
+    }
+    if (!*ok) { if (fail_code) *fail_code = 3; return KPX_OK; }
+    if (n_seg > 0) {
+        const double* e = sampled + (seg_offset[n_seg] - 1) * n;
+        const double d0 = e[0] - goal4[0], d1 = e[1] - goal4[1], d2 = e[2] - goal4[2];
+        if (!(sqrt(d0 * d0 + d1 * d1 + d2 * d2) <= goal4[3])) { *ok = 0; if (fail_code) *fail_code = 4; }
+    }
     return KPX_OK;
 }
 
@@ -647,10 +847,9 @@ void kpx_batch_destroy(kpx_batch* b) {
     delete b;
 }
 
-int kpx_batch_run(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const double* starts, const double* goals,
-                  double t_max, kpx_query_result* results, double* chain_start, double* chain_control,
-                  double* chain_dt, double* o_kernel_ms, void* stream) {
-    if (!bp || !seeds || !starts || !goals || !results) return fail(KPX_E_ARG, "null argument");
+int kpx_batch_upload(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const double* starts,
+                     const double* goals, int32_t want_chains, void* stream) {
+    if (!bp || !seeds || !starts || !goals) return fail(KPX_E_ARG, "null argument");
     if (n_queries < 1) return fail(KPX_E_ARG, "n_queries must be >= 1");
     kpx_batch& b = *bp;
     cudaStream_t st = (cudaStream_t)stream;
@@ -658,38 +857,77 @@ int kpx_batch_run(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const
     int rc = ensure_queries(b, n_queries);
     if (rc) return rc;
     const int n = b.prob.n, nu = b.prob.nu;
-    std::vector<QueryIn> q((size_t)n_queries);
+    b.q_stage.resize((size_t)n_queries);
     for (int64_t i = 0; i < n_queries; ++i) {
-        memset(&q[i], 0, sizeof(QueryIn));
-        q[i].seed = seeds[i];
-        memcpy(q[i].start, starts + i * n, sizeof(double) * n);
-        memcpy(q[i].goal, goals + i * 4, sizeof(double) * 4);
+        memset(&b.q_stage[i], 0, sizeof(QueryIn));
+        b.q_stage[i].seed = seeds[i];
+        memcpy(b.q_stage[i].start, starts + i * n, sizeof(double) * n);
+        memcpy(b.q_stage[i].goal, goals + i * 4, sizeof(double) * 4);
     }
-    const bool want_chain = chain_start && chain_control && chain_dt;
-    if (want_chain && !b.bc_start) {
+    if (want_chains && (!b.bc_start || b.bc_cap < b.q_cap)) {
+        cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt);
+        b.bc_start = b.bc_ctrl = b.bc_dt = nullptr;
         CU(cudaMalloc(&b.bc_start, 8 * (size_t)b.q_cap * b.max_chain * n));
         CU(cudaMalloc(&b.bc_ctrl, 8 * (size_t)b.q_cap * b.max_chain * nu));
         CU(cudaMalloc(&b.bc_dt, 8 * (size_t)b.q_cap * b.max_chain));
+        b.bc_cap = b.q_cap;
     }
-    CU(cudaMemcpyAsync(b.q_dev, q.data(), sizeof(QueryIn) * (size_t)n_queries, cudaMemcpyHostToDevice, st));
+    b.want_chains = want_chains != 0;
+    b.n_uploaded = n_queries;
+    CU(cudaMemcpyAsync(b.q_dev, b.q_stage.data(), sizeof(QueryIn) * (size_t)n_queries, cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    return KPX_OK;
+}
+
+/* asynchronous: one persistent launch over the uploaded queries; no host synchronisation */
+int kpx_batch_launch(kpx_batch* bp, double t_max, void* stream) {
+    if (!bp) return fail(KPX_E_ARG, "null batch");
+    kpx_batch& b = *bp;
+    if (b.n_uploaded < 1) return fail(KPX_E_STATE, "kpx_batch_upload first");
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(b.device));
     CU(cudaMemsetAsync(b.queue_dev, 0, 4, st));
     PlanLaunch L = base_launch(b);
-    L.n_queries = (int)n_queries; L.queries_dev = b.q_dev; L.results_dev = b.r_dev; L.queue_dev = b.queue_dev;
+    L.n_queries = (int)b.n_uploaded; L.queries_dev = b.q_dev; L.results_dev = b.r_dev; L.queue_dev = b.queue_dev;
     L.resume = 0; L.max_iters = 0; L.lam_override = 0; L.t_max_s = t_max;
-    if (want_chain) { L.b_chain_start = b.bc_start; L.b_chain_control = b.bc_ctrl; L.b_chain_dt = b.bc_dt; }
+    if (b.want_chains) { L.b_chain_start = b.bc_start; L.b_chain_control = b.bc_ctrl; L.b_chain_dt = b.bc_dt; }
+    return launch(b, L, st);
+}
+
+int kpx_batch_download(kpx_batch* bp, kpx_query_result* results, double* chain_start, double* chain_control,
+                       double* chain_dt, void* stream) {
+    if (!bp || !results) return fail(KPX_E_ARG, "null argument");
+    kpx_batch& b = *bp;
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(b.device));
+    const size_t q = (size_t)b.n_uploaded;
+    const int n = b.prob.n, nu = b.prob.nu;
+    CU(cudaMemcpyAsync(results, b.r_dev, sizeof(kpx_query_result) * q, cudaMemcpyDeviceToHost, st));
+    if (b.want_chains && chain_start && chain_control && chain_dt) {
+        CU(cudaMemcpyAsync(chain_start, b.bc_start, 8 * q * b.max_chain * n, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(chain_control, b.bc_ctrl, 8 * q * b.max_chain * nu, cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(chain_dt, b.bc_dt, 8 * q * b.max_chain, cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    return KPX_OK;
+}
+
+int kpx_batch_run(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const double* starts, const double* goals,
+                  double t_max, kpx_query_result* results, double* chain_start, double* chain_control,
+                  double* chain_dt, double* o_kernel_ms, void* stream) {
+    if (!bp || !results) return fail(KPX_E_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int want = chain_start && chain_control && chain_dt;
+    int rc = kpx_batch_upload(bp, n_queries, seeds, starts, goals, want, stream);
+    if (rc) return rc;
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
     CU(cudaEventRecord(e0, st));
-    rc = launch(b, L, st);
+    rc = kpx_batch_launch(bp, t_max, stream);
     if (rc) return rc;
     CU(cudaEventRecord(e1, st));
-    CU(cudaMemcpyAsync(results, b.r_dev, sizeof(kpx_query_result) * (size_t)n_queries, cudaMemcpyDeviceToHost, st));
-    if (want_chain) {
-        CU(cudaMemcpyAsync(chain_start, b.bc_start, 8 * (size_t)n_queries * b.max_chain * n, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(chain_control, b.bc_ctrl, 8 * (size_t)n_queries * b.max_chain * nu, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(chain_dt, b.bc_dt, 8 * (size_t)n_queries * b.max_chain, cudaMemcpyDeviceToHost, st));
-    }
-    CU(cudaStreamSynchronize(st));
+    rc = kpx_batch_download(bp, results, chain_start, chain_control, chain_dt, stream);
+    if (rc) return rc;
     if (o_kernel_ms) { float ms = 0; CU(cudaEventElapsedTime(&ms, e0, e1)); *o_kernel_ms = ms; }
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     return KPX_OK;

@@ -193,8 +193,11 @@ struct ModelStackedDI {
 
 // One RK4 substep with zero-order hold.  Accumulating k1 + 2k2 + 2k3 + k4 left to
 // right keeps the reference's rounding order (_kernel.pyx:223) with 3 live vectors.
+// float32 only: the state update is Kahan-compensated (`comp` carries the running
+// rounding error across substeps), which keeps ~50 chained substeps within a few
+// float32 ulps of the float64 trajectory; float64 uses the plain reference expression.
 template <class M, class R>
-__device__ __forceinline__ void rk4_step(R* cur, const R* u, R h, R half_h, R h6) {
+__device__ __forceinline__ void rk4_step(R* cur, R* comp, const R* u, R h, R half_h, R h6) {
     R k[M::N], acc[M::N], tmp[M::N];
     M::template deriv<R>(cur, u, k);
 #pragma unroll
@@ -207,7 +210,16 @@ __device__ __forceinline__ void rk4_step(R* cur, const R* u, R h, R half_h, R h6
     for (int i = 0; i < M::N; ++i) { acc[i] = acc[i] + (R)2 * k[i]; tmp[i] = cur[i] + h * k[i]; }
     M::template deriv<R>(tmp, u, k);
 #pragma unroll
-    for (int i = 0; i < M::N; ++i) cur[i] = cur[i] + h6 * (acc[i] + k[i]);
+    for (int i = 0; i < M::N; ++i) {
+        if constexpr (std::is_same<R, float>::value) {
+            const float y = __fmaf_rn(h6, acc[i] + k[i], -comp[i]);
+            const float t = __fadd_rn(cur[i], y);
+            comp[i] = __fsub_rn(__fsub_rn(t, cur[i]), y);
+            cur[i] = t;
+        } else {
+            cur[i] = cur[i] + h6 * (acc[i] + k[i]);
+        }
+    }
     M::template wrap<R>(cur);
 }
 
@@ -215,20 +227,20 @@ __device__ __forceinline__ void rk4_step(R* cur, const R* u, R h, R half_h, R h6
 // at a time performs exactly the same operations per dimension while keeping only a
 // 6-D set of RK4 temporaries live (N = 48 would otherwise need ~200 registers).
 template <int B, class R>
-__device__ __forceinline__ void rk4_step_blocks(R* cur, const R* u, R h, R half_h, R h6) {
+__device__ __forceinline__ void rk4_step_blocks(R* cur, R* comp, const R* u, R h, R half_h, R h6) {
 #pragma unroll
-    for (int b = 0; b < B; ++b) rk4_step<ModelDI6, R>(cur + 6 * b, u + 3 * b, h, half_h, h6);
+    for (int b = 0; b < B; ++b) rk4_step<ModelDI6, R>(cur + 6 * b, comp + 6 * b, u + 3 * b, h, half_h, h6);
 }
 template <class M, class R>
 struct Stepper {
-    __device__ static __forceinline__ void step(R* cur, const R* u, R h, R half_h, R h6) {
-        rk4_step<M, R>(cur, u, h, half_h, h6);
+    __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R half_h, R h6) {
+        rk4_step<M, R>(cur, comp, u, h, half_h, h6);
     }
 };
 template <int B, class R>
 struct Stepper<ModelStackedDI<B>, R> {
-    __device__ static __forceinline__ void step(R* cur, const R* u, R h, R half_h, R h6) {
-        rk4_step_blocks<B, R>(cur, u, h, half_h, h6);
+    __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R half_h, R h6) {
+        rk4_step_blocks<B, R>(cur, comp, u, h, half_h, h6);
     }
 };
 
@@ -254,6 +266,7 @@ struct ItemOut {
     int sub;
     int substeps;      // RK4 substeps actually integrated
     int points;        // collision points tested
+    int boxsteps;      // substeps whose state-box test ran (the segment was still valid)
     bool valid;
 };
 
@@ -265,20 +278,22 @@ __device__ __forceinline__ void integrate_and_map(const Params<R>& P, const R* _
     constexpr int N = M::N;
     R h = dt / (R)substeps, half_h = (R)0.5 * h, h6 = h / (R)6;
     R cur[N];
+    R comp[std::is_same<R, float>::value ? N : 1];   // Kahan carry (float32 only)
 #pragma unroll
-    for (int i = 0; i < N; ++i) cur[i] = x0[i];
+    for (int i = 0; i < N; ++i) { cur[i] = x0[i]; if constexpr (std::is_same<R, float>::value) comp[i] = 0.0f; }
     R prev0 = cur[0], prev1 = cur[1], prev2 = cur[2];
     bool ok = true, alive = true;
-    int done = 0, points = 0;
+    int done = 0, points = 0, boxsteps = 0;
     const int n_obs = P.n_obs;
     for (int s = 0; s < substeps; ++s) {
-        Stepper<M, R>::step(cur, u, h, half_h, h6);
+        Stepper<M, R>::step(cur, comp, u, h, half_h, h6);
         ++done;
         bool fin = true;
 #pragma unroll
         for (int i = 0; i < N; ++i) fin = fin && isfinite(cur[i]);
         if (!fin) { alive = false; ok = false; break; }
         if (ok) {
+            ++boxsteps;
             bool inb = true;
 #pragma unroll
             for (int i = 0; i < N; ++i) inb = inb && !(cur[i] < P.state_lo[i] || cur[i] > P.state_hi[i]);
@@ -300,7 +315,7 @@ __device__ __forceinline__ void integrate_and_map(const Params<R>& P, const R* _
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) out.end[i] = cur[i];
-    out.substeps = done; out.points = points;
+    out.substeps = done; out.points = points; out.boxsteps = boxsteps;
     out.region = -1; out.sub = 0; out.valid = false;
     if (alive) {
         int reg = 0;

@@ -44,12 +44,22 @@ struct Ctl {                      // one per workspace, global memory
     int n_items_last, n_keep_last;
     int cnt_valid[2], cnt_open[2];  // by iteration parity (trace only)
     // cumulative work
-    unsigned long long sum_items, sum_substeps, sum_points;
+    unsigned long long sum_items, sum_substeps, sum_points, sum_boxsteps;
     // timing (globaltimer ns)
     unsigned long long t_begin, t_reset_done, t_end;
     int n_trace;
     int chain_len;
     int cur_query;                // batch mode: query index broadcast to the team
+};
+
+constexpr int kPacketSegs = 64;    // solution segments carried inline in the result packet
+struct ResultPacket {             // everything the host needs after a run, one D2H copy
+    Ctl ctl;
+    double end_state[KPX_MAX_DIM];
+    double seg_dt[kPacketSegs];
+    long long seg_slot[kPacketSegs];
+    double seg_control[kPacketSegs][KPX_MAX_CONTROL];
+    double seg_start[kPacketSegs][KPX_MAX_DIM];
 };
 
 struct Workspace {                // device pointers of one team's state
@@ -70,6 +80,7 @@ struct Workspace {                // device pointers of one team's state
     kpx_trace* trace;             // [max_trace]
     // solution chain written on success
     double *chain_start, *chain_control, *chain_dt; long long* chain_slot; double* chain_end;
+    ResultPacket* packet;         // packed copy of ctl + the first kPacketSegs chain segments
 };
 
 struct QueryIn { unsigned long long seed; double start[KPX_MAX_DIM]; double goal[4]; };
@@ -266,7 +277,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             ctl->first_hit_w = 0x7fffffff; ctl->stop = 0; ctl->rescue_key = 0ull; ctl->rescue_slot = 0x7fffffff;
             ctl->n_items_last = 0; ctl->n_keep_last = 0;
             ctl->cnt_valid[0] = ctl->cnt_valid[1] = ctl->cnt_open[0] = ctl->cnt_open[1] = 0;
-            ctl->sum_items = ctl->sum_substeps = ctl->sum_points = 0ull;
+            ctl->sum_items = ctl->sum_substeps = ctl->sum_points = ctl->sum_boxsteps = 0ull;
             ctl->n_trace = 0; ctl->chain_len = 0;
         }
         team_sync(T);
@@ -305,11 +316,13 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
 
         // ================================================================= S1
         {
-            int my_sub = 0, my_pts = 0, my_valid = 0;
-            for (int c = T.rank; c < n_ich; c += T.ctas) {
+            int my_sub = 0, my_pts = 0, my_valid = 0, my_box = 0;
+            // items are spread over the whole team one per thread per round (S1 needs no chunk alignment;
+            // only the ranking in S2 does), so a 30k-item iteration is one round, not four
+            {
 #pragma unroll 1
-                for (int k = 0; k < kChunk / kBlock; ++k) {
-                    const int w = c * kChunk + k * kBlock + tid;
+                for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
+                    const int w = (int)w0 + tid;
                     const bool active = w < items;
                     int region = -1; bool valid = false;
                     if (active) {
@@ -325,7 +338,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                         for (int d = 0; d < N; ++d) x0[d] = __ldcg(states + (size_t)d * ld + slot);
                         ItemOut<R, N> o;
                         integrate_and_map<M, R>(P, s_obs, x0, u, dt, S, o);
-                        my_sub += o.substeps; my_pts += o.points;
+                        my_sub += o.substeps; my_pts += o.points; my_box += o.boxsteps;
                         region = o.region; valid = o.valid;
                         uint32_t code = kItemInvalid;
                         if (valid) {
@@ -350,10 +363,12 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                 my_sub += __shfl_xor_sync(0xffffffffu, my_sub, o);
                 my_pts += __shfl_xor_sync(0xffffffffu, my_pts, o);
                 my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
+                my_box += __shfl_xor_sync(0xffffffffu, my_box, o);
             }
             if ((tid & 31) == 0 && (my_sub | my_pts | my_valid)) {
                 atomicAdd(&ctl->sum_substeps, (unsigned long long)my_sub);
                 atomicAdd(&ctl->sum_points, (unsigned long long)my_pts);
+                atomicAdd(&ctl->sum_boxsteps, (unsigned long long)my_box);
                 atomicAdd(&ctl->cnt_valid[par], my_valid);
             }
         }
@@ -623,12 +638,23 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             if (A.n_peers) __threadfence_system();
         }
         ctl->chain_len = len;
+        if (!res_out && W.packet) {       // packed result for the single-plan API
+            ResultPacket* pk = W.packet;
+            const int m = len < kPacketSegs ? len : kPacketSegs;
+            for (int i = 0; i < m; ++i) {
+                pk->seg_dt[i] = W.chain_dt[i]; pk->seg_slot[i] = W.chain_slot[i];
+                for (int q = 0; q < NU; ++q) pk->seg_control[i][q] = W.chain_control[(size_t)i * NU + q];
+                for (int d = 0; d < N; ++d) pk->seg_start[i][d] = W.chain_start[(size_t)i * N + d];
+            }
+            if (len > 0) for (int d = 0; d < N; ++d) pk->end_state[d] = W.chain_end[d];
+        }
         ctl->t_end = gtimer();
+        if (!res_out && W.packet) W.packet->ctl = *ctl;
         if (res_out) {
             kpx_query_result r;
             r.status = status; r.iterations = it; r.tree_size = size; r.solution_slot = solution_slot;
             r.chain_len = len; r.device_ms = (double)(ctl->t_end - __ldcg(&ctl->t_begin)) * 1e-6;
-            r.items = __ldcg(&ctl->sum_items); r.substeps = __ldcg(&ctl->sum_substeps); r.points = __ldcg(&ctl->sum_points);
+            r.items = __ldcg(&ctl->sum_items); r.substeps = __ldcg(&ctl->sum_substeps); r.points = __ldcg(&ctl->sum_points); r.boxsteps = __ldcg(&ctl->sum_boxsteps);
             *res_out = r;
         }
     }

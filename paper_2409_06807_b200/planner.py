@@ -245,23 +245,34 @@ class KinoPax:
         return out
 
     def _trajectory(self) -> tuple:
-        """Segments from the device chain.  f64: every segment starts at the stored parent state, as in
-        the reference.  f32: the chain is re-integrated from the root in float64 (stored float32 node
-        states cannot chain to 1e-9), and the result must still be valid and end in the goal."""
+        """Segments from the device chain, rebuilt on the host in float64 (``kpx_trajectory`` restates
+        ``propagate_ode``).  f64: every segment starts at the stored parent state, as in the reference
+        (``planner.py:337-341``).  f32: the chain is re-integrated from the root (stored float32 node
+        states cannot chain to 1e-9) and must still be collision-free and end in the goal."""
         chain = self.solution_chain()
-        segs = []
-        if self.precision == _lib.F64:
-            for x0, u, dt in zip(chain["seg_start"], chain["seg_control"], chain["seg_dt"]):
-                segs.append(propagate_ode(self.model, x0, u, float(dt)))
-            return segs, True
-        x = self.start.copy()
-        for u, dt in zip(chain["seg_control"], chain["seg_dt"]):
-            seg = propagate_ode(self.model, x, u, float(dt))
-            segs.append(seg)
-            x = seg.end_state
-        ok = all(self.checker.segment_valid(s) for s in segs)
-        d = x[list(self.model.position_dims)] - self.goal4[:3]
-        ok = ok and float(np.sqrt(d @ d)) <= self.goal4[3]
+        from_root = self.precision != _lib.F64
+        n, nu = self.model.n, self.model.control_dim
+        dts, ctrl = chain["seg_dt"], chain["seg_control"]
+        starts = chain["seg_start"]
+        if from_root:
+            starts = starts.copy()
+            starts[0] = self.start
+        L = len(dts)
+        rows = int((np.maximum(4, np.ceil(dts / 0.02)) + 1).sum())
+        sampled = np.empty((rows, n))
+        off = np.zeros(L + 1, np.int64)
+        _lib.check(self._lib.kpx_trajectory(self.model.kernel_id, n, nu, L, _lib.ptr(starts), _lib.ptr(ctrl),
+                                            _lib.ptr(dts), 1 if from_root else 0, _lib.ptr(sampled), rows,
+                                            _lib.ptr(off)), "kpx_trajectory")
+        segs = [TrajectorySegment(control=ctrl[i].copy(), dt=float(dts[i]), end_state=sampled[off[i + 1] - 1].copy(),
+                                  sampled_states=sampled[off[i]:off[i + 1]]) for i in range(L)]
+        ok = True
+        if from_root:
+            okc, code = C.c_int32(0), C.c_int32(0)
+            _lib.check(self._lib.kpx_trajectory_valid(C.byref(self._prob_struct), L, _lib.ptr(sampled), _lib.ptr(off),
+                                                      _lib.ptr(self.goal4), self.problem.check_resolution,
+                                                      C.byref(okc), C.byref(code)), "kpx_trajectory_valid")
+            ok = bool(okc.value)
         return segs, ok
 
     def solve(self, trace_fn: Optional[Callable[[IterationTrace], None]] = None,
@@ -286,7 +297,7 @@ class KinoPax:
                                             wall_time_ms=(time.perf_counter() - t0) * 1e3,
                                             solution_duration_s=duration))
         result.device = {"device_ms": st.device_ms, "reset_ms": st.reset_ms, "items": int(st.items),
-                         "substeps": int(st.substeps), "points": int(st.points), "launches": int(st.launches),
+                         "substeps": int(st.substeps), "points": int(st.points), "boxsteps": int(st.boxsteps), "launches": int(st.launches),
                          "precision": "f64" if self.precision == _lib.F64 else "f32", "f64_retry": retried}
         if trace_fn is not None:
             for tr in self.traces():

@@ -1,0 +1,84 @@
+"""Batch / multi-query path on the GPU: one persistent launch must give, per query, exactly what a
+dedicated single-query run gives (team size and scheduling never change a tree)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import small_cfg
+
+pytestmark = pytest.mark.gpu
+
+
+def test_batch_equals_single_queries(kp, orc):
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=8000, seed=0)
+    seeds = np.arange(40)
+    for backend, team in (("cuda", 1), ("cuda-f32", 1), ("cuda", 2)):
+        with kp.BatchPlanner(cfg, env, model, backend=backend, n_teams=12, team_ctas=team) as bp:
+            res = bp.run(seeds)
+            again = bp.run(seeds)                       # workspaces are reused: results must not drift
+        for k in ("status", "iterations", "tree_size", "solution_slot", "chain_len", "items", "substeps"):
+            assert np.array_equal(res.records[k], again.records[k]), (backend, k)
+        with kp.KinoPax(cfg, env, model, backend=backend) as eng:
+            for q in (0, 7, 39):
+                eng.reset(seed=int(seeds[q]))
+                one = eng.solve()
+                assert one.stats.iterations == res.records["iterations"][q]
+                assert one.stats.tree_size == res.records["tree_size"][q]
+                assert (one.status is kp.PlanStatus.SOLVED) == (res.records["status"][q] == 0)
+        if backend == "cuda":                           # float64 batch == CPU oracle, query by query
+            for q in (3, 21):
+                op = orc.plan_from_problem(kp.build_problem(cfg.with_seed(int(seeds[q])), env, model))
+                op.solve(t_max=60.0)
+                assert op.raw.size == res.records["tree_size"][q] and op.raw.iteration == res.records["iterations"][q]
+        solved = np.flatnonzero(res.solved)
+        assert len(solved) >= 30
+        with kp.BatchPlanner(cfg, env, model, backend=backend, n_teams=4, team_ctas=team) as bp2:
+            r2 = bp2.run(seeds[:8])
+            for q in range(8):
+                if r2.status(q) is kp.PlanStatus.SOLVED:
+                    segs, ok = bp2.trajectory(r2, q)
+                    assert ok and len(segs) == r2.records["chain_len"][q]
+                    assert kp.ValidityChecker(env, model, 0.05).trajectory_valid(segs, start=env.start)
+
+
+def test_batch_with_per_query_goals(kp):
+    """Config 5 shape: random goals per query (rejecting goals inside pillar columns), quadcopter."""
+    model = kp.get_model("quad12")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=60000, seed=0)
+    q = 16
+    goals = np.stack([kp.goal_for_query(i, env) for i in range(q)])
+    assert np.all(np.linalg.norm(goals[:, :3] - env.start[:3], axis=1) >= 4.0)
+    with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", n_teams=16, team_ctas=1) as bp:
+        res = bp.run(np.arange(q), goals=goals)
+        assert res.solved.sum() >= q // 2
+        for i in np.flatnonzero(res.solved)[:6]:
+            segs, ok = bp.trajectory(res, int(i))
+            assert ok
+            end = segs[-1].end_state[:3]
+            assert np.linalg.norm(end - goals[i, :3]) <= goals[i, 3] + 1e-9
+
+
+def test_race_flag_stops_a_run(kp):
+    """OR-parallel race plumbing on one GPU: a pre-set stop word ends the run at the first iteration
+    boundary with TIMEOUT-like status; a solving run raises the peers' words."""
+    import torch
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=20000, seed=0)
+    flags = kp.RaceFlags()
+    peer = torch.zeros(64, dtype=torch.int32, device="cuda")
+    with kp.KinoPax(cfg, env, model, backend="cuda-f32") as eng:
+        flags.flag[0] = 1
+        torch.cuda.synchronize()
+        st = kp.race(eng, flags, seed=0)
+        assert st.status == 5 and st.iterations == 1          # KPX_STOPPED after one iteration
+        flags.clear()
+        eng.reset(seed=0)
+        st = eng._run(60.0, stop_flag=C.c_void_p(flags.own_ptr), peer_flags=[peer.data_ptr()])
+        assert st.status == 0
+        torch.cuda.synchronize()
+        assert int(peer[0].item()) == 1 and not flags.fired()

@@ -64,8 +64,13 @@ def test_batch_parity_f32_tolerance(kp, model_name):
     # sampling is done in float64 on the device even in the float32 build: bit-exact
     assert np.array_equal(b.control, g["control"]) and np.array_equal(b.dt, g["dt"])
     assert np.array_equal(b.accept_u, g["accept_u"])
+    # tolerance is stated on the states that can enter the tree (valid in both); an invalid quadcopter item
+    # keeps integrating after leaving the box (reference rule 11) and may pass the tan(pitch) singularity,
+    # where float32 and float64 trajectories legitimately diverge
+    both_valid = (b.valid == 1) & (g["valid"] == 1)
+    assert both_valid.sum() > 0.9 * g["valid"].sum()
     scale = np.maximum(np.abs(g["end"]), 1.0)
-    rel = _wrap_diff(b.end, g["end"], model.wrap_dims) / scale
+    rel = (_wrap_diff(b.end, g["end"], model.wrap_dims) / scale)[both_valid]
     assert np.max(rel) < F32_RTOL, np.max(rel)
     # verdicts / cells may flip only for items that sit within float32 rounding of a boundary
     agree = (b.valid == g["valid"]) & (b.region == g["region"])
@@ -159,7 +164,7 @@ def _step_compare(kp, orc, model_name, scene, t_e, seed, backend, max_iters=60, 
             assert np.array_equal(items["keep"], keep), it
             if st.status != 4:
                 break
-        assert {0: "solved", 1: "timeout", 2: "capacity_exhausted"}[st.status] == op.status
+        assert {0: "solved", 1: "timeout", 2: "capacity_exhausted", 4: "running"}[st.status] == op.status
         if st.status == 0:
             assert int(st.solution_slot) == int(op.raw.solution_slot)
         return it

@@ -158,3 +158,42 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".inl")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "kpx_oracle" not in text and "import oracle" not in text and "ref_loader" not in text, f
+
+
+def test_native_trajectory_rebuild_and_check(kp):
+    """kpx_trajectory / kpx_trajectory_valid are host-only float64 code in libkpx.so: they must equal
+    propagate_ode (dynamics.py:242) bit for bit and reproduce the reference checker's recorded verdicts."""
+    import ctypes as C
+    from paper_2409_06807_b200 import _lib
+    if not os.path.isfile(_lib.LIB_PATH):
+        pytest.skip("libkpx.so not built")
+    L = _lib.load()
+    for rec in json.load(open(os.path.join(GOLDEN, "checker.json"))):
+        model = kp.get_model(rec["model"])
+        env = kp.gen_environment(rec["scene"], model, seed=0)
+        prob = kp.build_problem(small_cfg(kp, model, t_e=rec["t_e"], seed=rec["seed"]), env, model)
+        starts, ctrl, dts = (np.ascontiguousarray(rec[k], dtype=np.float64) for k in ("seg_start", "seg_control", "seg_dt"))
+        n_seg = len(dts)
+        rows = int((np.maximum(4, np.ceil(dts / 0.02)) + 1).sum())
+        sampled, off = np.empty((rows, model.n)), np.zeros(n_seg + 1, np.int64)
+        for from_root in (0, 1):
+            _lib.check(L.kpx_trajectory(model.kernel_id, model.n, model.control_dim, n_seg, _lib.ptr(starts),
+                                        _lib.ptr(ctrl), _lib.ptr(dts), from_root, _lib.ptr(sampled), rows,
+                                        _lib.ptr(off)), "kpx_trajectory")
+            x = starts[0]
+            for i in range(n_seg):
+                seg = kp.propagate_ode(model, x if from_root else starts[i], ctrl[i], float(dts[i]))
+                assert np.array_equal(sampled[off[i]:off[i + 1]], seg.sampled_states), (rec["model"], i)
+                x = seg.end_state
+        ps, keep = _lib.problem_from(prob)
+        for res, verdict in rec["valid"].items():
+            ok, code = C.c_int32(0), C.c_int32(0)
+            _lib.check(L.kpx_trajectory_valid(C.byref(ps), n_seg, _lib.ptr(sampled), _lib.ptr(off),
+                                              _lib.ptr(prob.goal4), float(res), C.byref(ok), C.byref(code)), "valid")
+            assert bool(ok.value) == verdict
+        far = prob.goal4.copy()
+        far[:3] = 0.5
+        ok, code = C.c_int32(0), C.c_int32(0)
+        L.kpx_trajectory_valid(C.byref(ps), n_seg, _lib.ptr(sampled), _lib.ptr(off), _lib.ptr(far), 0.05,
+                               C.byref(ok), C.byref(code))
+        assert ok.value == 0 and code.value == 4
