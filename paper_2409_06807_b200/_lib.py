@@ -19,7 +19,7 @@ SOLVED, TIMEOUT, CAPACITY_EXHAUSTED, ERROR, RUNNING, STOPPED = range(6)
 E_ARG, E_CUDA, E_LIMIT, E_STATE = 1, 2, 3, 4
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libkpx.so")
+LIB_PATH = os.environ.get("KPX_LIB_PATH") or os.path.join(_PKG, "libkpx.so")   # override: tuning variants only
 
 _vp = C.c_void_p
 

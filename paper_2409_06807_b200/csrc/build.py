@@ -35,14 +35,16 @@ def _stale(target: str, sources) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, obj_dir: str = OBJ) -> str:
+    """defines / lib / obj_dir let tuning scripts build side-by-side variants (e.g. -DKPX_MINB_F32_SMALL=3)."""
+    OBJ, LIB = obj_dir, lib  # noqa: N806
     os.makedirs(OBJ, exist_ok=True)
     hdrs = [os.path.join(HERE, h) for h in HEADERS]
     jobs = []
     for src, extra in UNITS:
         obj = os.path.join(OBJ, src.replace(".cu", ".o"))
         if force or _stale(obj, [os.path.join(HERE, src)] + hdrs):
-            cmd = [NVCC] + ARCH + COMMON + extra + (["-Xptxas", "-v"] if verbose else []) + \
+            cmd = [NVCC] + ARCH + COMMON + extra + list(defines) + (["-Xptxas", "-v"] if verbose else []) + \
                   ["-c", os.path.join(HERE, src), "-o", obj]
             jobs.append(cmd)
 
@@ -64,4 +66,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    tag = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--tag=")), None)
+    if tag:
+        print(build(force=True, verbose="-v" in sys.argv, defines=defs, lib=os.path.join(PKG, f"libkpx_{tag}.so"),
+                    obj_dir=os.path.join(HERE, f"_obj_{tag}")))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs))

@@ -55,8 +55,15 @@ int check_problem(const kpx_problem* pr) {
 }
 
 // obstacles -> device SoA [minx|miny|minz|maxx|maxy|maxz] in the launch precision
-int upload_obstacles(int precision, int n_obs, const double* omin, const double* omax, void* dev, cudaStream_t st) {
+int upload_obstacles(const kpx_problem& pr, int precision, int n_obs, const double* omin, const double* omax, void* dev,
+                     uint32_t* occ_dev, cudaStream_t st) {
     if (n_obs == 0) return KPX_OK;
+    {
+        std::vector<uint32_t> masks((size_t)kOccGrid * kOccGrid * kOccGrid);
+        build_occupancy_masks(pr, n_obs, omin, omax, masks.data());
+        CU(cudaMemcpyAsync(occ_dev, masks.data(), masks.size() * 4, cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    }
     if (precision == KPX_F64) {
         std::vector<double> h(6 * (size_t)n_obs);
         for (int k = 0; k < n_obs; ++k)
@@ -96,6 +103,7 @@ struct kpx_batch {
     std::vector<Workspace> ws_host;
     Workspace* ws_dev = nullptr;
     void* obs_dev = nullptr;
+    uint32_t* occ_dev = nullptr;
     unsigned int* queue_dev = nullptr;
     QueryIn* q_dev = nullptr;
     kpx_query_result* r_dev = nullptr;
@@ -122,7 +130,7 @@ namespace {
 
 void destroy_batch(kpx_batch& b) {
     cudaSetDevice(b.device);
-    cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
+    cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.occ_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
     cudaFree(b.r_dev); cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt); cudaFree(b.peers_dev);
     cudaFreeHost(b.pk_host); cudaFreeHost(b.q_pinned);
 }
@@ -153,7 +161,8 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     for (int d = 0; d < prob->grid_n; ++d) regions *= prob->grid_cells[d];
     b.regions = (int)regions;
     b.subs = prob->subcells * prob->subcells * prob->subcells;
-    b.smem = align_up((size_t)(b.max_chunks + 1) * sizeof(int), 16) + 6 * (size_t)std::max(prob->n_obs, 1) * b.rs;
+    b.smem = align_up((size_t)(b.max_chunks + 1) * sizeof(int), 16) + align_up(6 * (size_t)std::max(prob->n_obs, 1) * b.rs, 8) +
+             4 * (size_t)kOccGrid * kOccGrid * kOccGrid;
     if (b.smem > 200 * 1024) return fail(KPX_E_LIMIT, "t_e / obstacle count need more shared memory than one SM has");
 
     cudaDeviceProp dp;
@@ -216,7 +225,8 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
     CU(cudaMemcpy(b.ws_dev, b.ws_host.data(), sizeof(Workspace) * (size_t)n_teams, cudaMemcpyHostToDevice));
     CU(cudaMalloc(&b.obs_dev, 6 * (size_t)std::max(prob->n_obs, 1) * b.rs));
-    rc = upload_obstacles(precision, prob->n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, 0);
+    CU(cudaMalloc(&b.occ_dev, 4 * (size_t)kOccGrid * kOccGrid * kOccGrid));
+    rc = upload_obstacles(b.prob, precision, prob->n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
     if (rc) return rc;
     CU(cudaMalloc(&b.queue_dev, 256));
     CU(cudaMemset(b.queue_dev, 0, 256));
@@ -244,7 +254,7 @@ int launch(kpx_batch& b, const PlanLaunch& L, cudaStream_t st) {
 
 PlanLaunch base_launch(kpx_batch& b) {
     PlanLaunch L{};
-    L.prob = &b.prob; L.obs_dev = b.obs_dev; L.ws_dev = b.ws_dev; L.n_teams = b.n_teams; L.team_ctas = b.team_ctas;
+    L.prob = &b.prob; L.obs_dev = b.obs_dev; L.occ_dev = b.occ_dev; L.ws_dev = b.ws_dev; L.n_teams = b.n_teams; L.team_ctas = b.team_ctas;
     L.max_chunks = b.max_chunks; L.stride = b.cap_pad; L.max_trace = b.max_trace; L.max_chain = b.max_chain; L.smem = b.smem;
     L.cooperative = b.cooperative;
     return L;
@@ -387,7 +397,8 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
     char* slab = nullptr;
     Carver c;
     const size_t o_states = c.take(8 * (size_t)state_rows * n), o_slots = c.take(8 * (size_t)m),
-                 o_obs = c.take(6 * (size_t)std::max(prob->n_obs, 1) * rs), o_v = c.take((size_t)items),
+                 o_obs = c.take(6 * (size_t)std::max(prob->n_obs, 1) * rs),
+                 o_occ = c.take(4 * (size_t)kOccGrid * kOccGrid * kOccGrid), o_v = c.take((size_t)items),
                  o_r = c.take(8 * (size_t)items), o_s = c.take(8 * (size_t)items), o_e = c.take(8 * (size_t)items * n),
                  o_c = c.take(8 * (size_t)items * nu), o_d = c.take(8 * (size_t)items), o_a = c.take(8 * (size_t)items),
                  o_ss = c.take(8 * (size_t)items), o_pp = c.take(8 * (size_t)items);
@@ -395,17 +406,17 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
     struct Guard { char* p; ~Guard() { cudaFree(p); } } guard{slab};
     CU(cudaMemcpyAsync(slab + o_states, states, 8 * (size_t)state_rows * n, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(slab + o_slots, e_slots, 8 * (size_t)m, cudaMemcpyHostToDevice, st));
-    rc = upload_obstacles(precision, prob->n_obs, prob->obs_min, prob->obs_max, slab + o_obs, st);
+    rc = upload_obstacles(*prob, precision, prob->n_obs, prob->obs_min, prob->obs_max, slab + o_obs, (uint32_t*)(slab + o_occ), st);
     if (rc) return rc;
     BatchLaunch L{};
-    L.prob = prob; L.obs_dev = slab + o_obs; L.states_dev = (const double*)(slab + o_states);
+    L.prob = prob; L.obs_dev = slab + o_obs; L.occ_dev = (const uint32_t*)(slab + o_occ); L.states_dev = (const double*)(slab + o_states);
     L.e_slots_dev = (const long long*)(slab + o_slots); L.items = items; L.lam = lam; L.seed = seed;
     L.iteration = iteration; L.o_valid = (uint8_t*)(slab + o_v); L.o_region = (long long*)(slab + o_r);
     L.o_sub = (long long*)(slab + o_s); L.o_end = (double*)(slab + o_e); L.o_control = (double*)(slab + o_c);
     L.o_dt = (double*)(slab + o_d); L.o_accept = (double*)(slab + o_a);
     L.o_substeps = (long long*)(slab + o_ss); L.o_points = (long long*)(slab + o_pp);
     L.grid = (int)std::min<int64_t>((items + kBlock - 1) / kBlock, 148 * 16);
-    L.smem = 6 * (size_t)std::max(prob->n_obs, 1) * rs;
+    L.smem = align_up(6 * (size_t)std::max(prob->n_obs, 1) * rs, 8) + 4 * (size_t)kOccGrid * kOccGrid * kOccGrid;
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
     CU(cudaEventRecord(e0, st));
@@ -468,7 +479,7 @@ int kpx_plan_set_obstacles(kpx_plan* p, int32_t n_obs, const double* omin, const
     b.prob.n_obs = n_obs;
     std::copy(omin, omin + 3 * (size_t)n_obs, b.obs_min.begin());
     std::copy(omax, omax + 3 * (size_t)n_obs, b.obs_max.begin());
-    return upload_obstacles(b.precision, n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, 0);
+    return upload_obstacles(b.prob, b.precision, n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
 }
 
 int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_override, uint32_t* stop_flag,

@@ -18,6 +18,7 @@ namespace kpx {
 
 constexpr int kBlock = 256;          // threads per CTA of every kernel here
 constexpr int kChunk = 4 * kBlock;   // slots / items per ordered-compaction chunk
+constexpr int kOccGrid = 16;         // occupancy-mask grid resolution per axis (16 KB of shared memory)
 constexpr uint32_t kUnclaimed = 0xFFFFFFFFu;
 constexpr uint32_t kVisited = 0xFFFFFFFEu;
 constexpr uint32_t kItemInvalid = 0xFFFFFFFFu;
@@ -61,6 +62,9 @@ struct Params {
     R grid_cmax[KPX_MAX_DIM];             // (R)(cells-1)
     int grid_strides[KPX_MAX_DIM];
     int n_regions, subs_per_region;
+    // occupancy-mask grid over the position box (0 = disabled -> every obstacle is tested)
+    int occ_g;
+    R occ_lo[3], occ_inv[3];
 };
 
 template <class R>
@@ -85,6 +89,33 @@ inline void fill_params(Params<R>& P, const kpx_problem& pr) {
     }
     P.n_regions = (int)regions;
     P.subs_per_region = pr.subcells * pr.subcells * pr.subcells;
+    P.occ_g = (pr.n_obs > 0 && pr.n_obs <= 32) ? kOccGrid : 0;
+    for (int a = 0; a < 3; ++a) {
+        P.occ_lo[a] = (R)pr.state_lo[a];
+        P.occ_inv[a] = (R)((double)kOccGrid / (pr.state_hi[a] - pr.state_lo[a]));
+    }
+}
+
+// Host: cell -> bitmask of the obstacles whose closed box can contain a point of that cell.  One cell of
+// margin on every side absorbs any rounding of the device-side cell lookup, so the mask is conservative
+// and the exact closed-box test on the flagged obstacles gives the same verdict as testing all of them.
+inline void build_occupancy_masks(const kpx_problem& pr, int n_obs, const double* omin, const double* omax,
+                                  uint32_t* masks /* kOccGrid^3 */) {
+    const int G = kOccGrid;
+    for (int i = 0; i < G * G * G; ++i) masks[i] = 0u;
+    for (int k = 0; k < n_obs && k < 32; ++k) {
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            const double cs = (pr.state_hi[a] - pr.state_lo[a]) / G;
+            lo[a] = (int)floor((omin[3 * k + a] - pr.state_lo[a]) / cs) - 1;
+            hi[a] = (int)floor((omax[3 * k + a] - pr.state_lo[a]) / cs) + 1;
+            lo[a] = lo[a] < 0 ? 0 : lo[a];
+            hi[a] = hi[a] > G - 1 ? G - 1 : hi[a];
+        }
+        for (int x = lo[0]; x <= hi[0]; ++x)
+            for (int y = lo[1]; y <= hi[1]; ++y)
+                for (int z = lo[2]; z <= hi[2]; ++z) masks[(x * G + y) * G + z] |= 1u << k;
+    }
 }
 
 // ----------------------------------------------------------------- models ----
@@ -258,6 +289,26 @@ __device__ __forceinline__ bool point_hits(R px, R py, R pz, const R* __restrict
     return h;
 }
 
+// Same verdict through the occupancy grid: look up the point's cell, test only the flagged obstacles.
+template <class R>
+__device__ __forceinline__ bool point_hits_grid(const Params<R>& P, R px, R py, R pz, const R* __restrict__ s_obs,
+                                                const uint32_t* __restrict__ s_occ, int n_obs) {
+    if (P.occ_g == 0) return point_hits<R>(px, py, pz, s_obs, n_obs);
+    int ix = (int)((px - P.occ_lo[0]) * P.occ_inv[0]);
+    int iy = (int)((py - P.occ_lo[1]) * P.occ_inv[1]);
+    int iz = (int)((pz - P.occ_lo[2]) * P.occ_inv[2]);
+    ix = min(max(ix, 0), kOccGrid - 1); iy = min(max(iy, 0), kOccGrid - 1); iz = min(max(iz, 0), kOccGrid - 1);
+    uint32_t m = s_occ[(ix * kOccGrid + iy) * kOccGrid + iz];
+    bool h = false;
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        h = h || (px >= s_obs[k] && px <= s_obs[3 * n_obs + k] && py >= s_obs[n_obs + k] && py <= s_obs[4 * n_obs + k] &&
+                  pz >= s_obs[2 * n_obs + k] && pz <= s_obs[5 * n_obs + k]);
+    }
+    return h;
+}
+
 template <class R, int N>
 struct ItemOut {
     R end[N];
@@ -273,7 +324,8 @@ struct ItemOut {
 // The extension itself.  `u` and `dt` are the sampled control / duration already
 // rounded to R; x0 is the parent state.
 template <class M, class R>
-__device__ __forceinline__ void integrate_and_map(const Params<R>& P, const R* __restrict__ s_obs, const R* x0,
+__device__ __forceinline__ void integrate_and_map(const Params<R>& P, const R* __restrict__ s_obs,
+                                                  const uint32_t* __restrict__ s_occ, const R* x0,
                                                   const R* u, R dt, int substeps, ItemOut<R, M::N>& out) {
     constexpr int N = M::N;
     R h = dt / (R)substeps, half_h = (R)0.5 * h, h6 = h / (R)6;
@@ -303,12 +355,13 @@ __device__ __forceinline__ void integrate_and_map(const Params<R>& P, const R* _
                 R dist = MathK<R>::sq(dx * dx + dy * dy + dz * dz);
                 int steps = 1;
                 while ((R)steps * P.check_res < dist) steps <<= 1;
+                const R inv_steps = (R)1 / (R)steps;          // steps is a power of two: j * inv_steps == j / steps exactly
                 for (int j = 1; j < steps; ++j) {
-                    R t = (R)j / (R)steps;
+                    R t = (R)j * inv_steps;
                     ++points;
-                    if (point_hits<R>(prev0 + t * dx, prev1 + t * dy, prev2 + t * dz, s_obs, n_obs)) { ok = false; break; }
+                    if (point_hits_grid<R>(P, prev0 + t * dx, prev1 + t * dy, prev2 + t * dz, s_obs, s_occ, n_obs)) { ok = false; break; }
                 }
-                if (ok) { ++points; if (point_hits<R>(cur[0], cur[1], cur[2], s_obs, n_obs)) ok = false; }
+                if (ok) { ++points; if (point_hits_grid<R>(P, cur[0], cur[1], cur[2], s_obs, s_occ, n_obs)) ok = false; }
             }
         }
         prev0 = cur[0]; prev1 = cur[1]; prev2 = cur[2];

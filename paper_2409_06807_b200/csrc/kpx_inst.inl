@@ -10,7 +10,7 @@ template <class M>
 cudaError_t do_launch_plan(const PlanLaunch& L, cudaStream_t st) {
     PlanArgs<Real> A;
     fill_params<Real>(A.P, *L.prob);
-    A.obs = (const Real*)L.obs_dev; A.ws = L.ws_dev; A.queries = L.queries_dev; A.results = L.results_dev;
+    A.obs = (const Real*)L.obs_dev; A.occ = L.occ_dev; A.ws = L.ws_dev; A.queries = L.queries_dev; A.results = L.results_dev;
     A.queue = L.queue_dev; A.n_queries = L.n_queries; A.n_teams = L.n_teams; A.team_ctas = L.team_ctas;
     A.max_chunks = L.max_chunks; A.stride = L.stride; A.max_trace = L.max_trace; A.max_chain = L.max_chain; A.resume = L.resume;
     A.max_iters = L.max_iters; A.lam_override = L.lam_override; A.t_max_s = L.t_max_s;
@@ -32,7 +32,7 @@ template <class M>
 cudaError_t do_launch_batch(const BatchLaunch& L, cudaStream_t st) {
     BatchArgs<Real> A;
     fill_params<Real>(A.P, *L.prob);
-    A.obs = (const Real*)L.obs_dev; A.states = L.states_dev; A.e_slots = L.e_slots_dev; A.items = L.items;
+    A.obs = (const Real*)L.obs_dev; A.occ = L.occ_dev; A.states = L.states_dev; A.e_slots = L.e_slots_dev; A.items = L.items;
     A.lam = L.lam; A.seed = L.seed; A.iteration = L.iteration; A.o_valid = L.o_valid; A.o_region = L.o_region;
     A.o_sub = L.o_sub; A.o_end = L.o_end; A.o_control = L.o_control; A.o_dt = L.o_dt; A.o_accept = L.o_accept;
     A.o_substeps = L.o_substeps; A.o_points = L.o_points;

@@ -11,6 +11,7 @@ namespace kpx {
 struct PlanLaunch {
     const kpx_problem* prob;
     const void* obs_dev;            // SoA [6][n_obs] in the launch precision
+    const uint32_t* occ_dev;        // occupancy masks [kOccGrid^3]
     Workspace* ws_dev;
     const QueryIn* queries_dev;
     kpx_query_result* results_dev;
@@ -29,6 +30,7 @@ struct PlanLaunch {
 struct BatchLaunch {
     const kpx_problem* prob;
     const void* obs_dev;
+    const uint32_t* occ_dev;
     const double* states_dev;
     const long long* e_slots_dev;
     long long items;

@@ -28,6 +28,13 @@
 #pragma once
 #include "kpx_device.cuh"
 
+#ifndef KPX_MINB_F32_SMALL
+#define KPX_MINB_F32_SMALL 4
+#endif
+#ifndef KPX_MINB_F32_MID
+#define KPX_MINB_F32_MID 2
+#endif
+
 namespace kpx {
 
 struct Ctl {                      // one per workspace, global memory
@@ -89,6 +96,7 @@ template <class R>
 struct PlanArgs {
     Params<R> P;
     const R* obs;                 // device SoA [6][n_obs]
+    const uint32_t* occ;          // device occupancy masks [kOccGrid^3]
     Workspace* ws;                // [n_teams]
     const QueryIn* queries;       // [n_queries]
     kpx_query_result* results;    // [n_queries] (may be null)
@@ -219,7 +227,7 @@ __device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __
 template <class M, class R>
 __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
                           kpx_query_result* res_out, long long query_index, int* s_prefix, const R* s_obs,
-                          int* s_w, double* s_d) {
+                          const uint32_t* s_occ, int* s_w, double* s_d) {
     constexpr int N = M::N, NU = M::NU;
     const Params<R>& P = A.P;
     const int tid = threadIdx.x;
@@ -337,7 +345,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
 #pragma unroll
                         for (int d = 0; d < N; ++d) x0[d] = __ldcg(states + (size_t)d * ld + slot);
                         ItemOut<R, N> o;
-                        integrate_and_map<M, R>(P, s_obs, x0, u, dt, S, o);
+                        integrate_and_map<M, R>(P, s_obs, s_occ, x0, u, dt, S, o);
                         my_sub += o.substeps; my_pts += o.points; my_box += o.boxsteps;
                         region = o.region; valid = o.valid;
                         uint32_t code = kItemInvalid;
@@ -660,16 +668,22 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
     }
 }
 
+// Resident CTAs per SM each instantiation is compiled for (register budget = 65536 / (kBlock * n)).
+// The propagation loop is latency-bound, so the small float32 models trade registers for warps.
+template <class M, class R> struct MinBlocks { static constexpr int value = sizeof(R) == 4 ? (M::N <= 6 ? KPX_MINB_F32_SMALL : (M::N <= 12 ? KPX_MINB_F32_MID : 1)) : (M::N <= 6 ? 2 : 1); };
+
 template <class M, class R>
-__global__ void __launch_bounds__(kBlock) plan_kernel(const __grid_constant__ PlanArgs<R> A) {
+__global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(const __grid_constant__ PlanArgs<R> A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int* s_prefix = (int*)smem_raw;                                       // [max_chunks + 1]
     R* s_obs = (R*)(smem_raw + (((size_t)(A.max_chunks + 1) * sizeof(int) + 15) & ~(size_t)15));
+    uint32_t* s_occ = (uint32_t*)(s_obs + 6 * (A.P.n_obs > 0 ? A.P.n_obs : 1) + (6 * (A.P.n_obs > 0 ? A.P.n_obs : 1)) % 2);
     __shared__ int s_w[kBlock / 32 + 1];
     __shared__ double s_d[kBlock / 32];
     __shared__ int s_q;
 
     for (int i = threadIdx.x; i < 6 * A.P.n_obs; i += kBlock) s_obs[i] = A.obs[i];
+    if (A.P.occ_g) for (int i = threadIdx.x; i < kOccGrid * kOccGrid * kOccGrid; i += kBlock) s_occ[i] = A.occ[i];
     __syncthreads();
 
     Team T;
@@ -681,7 +695,7 @@ __global__ void __launch_bounds__(kBlock) plan_kernel(const __grid_constant__ Pl
     T.bar = W.bar;
 
     if (A.queue == nullptr) {       // single query bound to team 0 (plan handle: stepped / resumable)
-        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_obs, s_w, s_d);
+        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_obs, s_occ, s_w, s_d);
         return;
     }
     for (;;) {                      // batch: teams pull queries until the queue is drained
@@ -698,7 +712,7 @@ __global__ void __launch_bounds__(kBlock) plan_kernel(const __grid_constant__ Pl
         const int q = s_q;
         __syncthreads();
         if (q >= A.n_queries) return;
-        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_obs, s_w, s_d);
+        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_obs, s_occ, s_w, s_d);
         team_sync(T);
     }
 }
@@ -708,6 +722,7 @@ template <class R>
 struct BatchArgs {
     Params<R> P;
     const R* obs;              // device SoA [6][n_obs]
+    const uint32_t* occ;       // device occupancy masks
     const double* states;      // (rows, n) f64 row-major, as the reference passes it
     const long long* e_slots;  // (m)
     long long items; int lam;
@@ -721,7 +736,9 @@ __global__ void __launch_bounds__(kBlock) batch_kernel(const __grid_constant__ B
     constexpr int N = M::N, NU = M::NU;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* s_obs = (R*)smem_raw;
+    uint32_t* s_occ = (uint32_t*)(s_obs + 6 * (A.P.n_obs > 0 ? A.P.n_obs : 1) + (6 * (A.P.n_obs > 0 ? A.P.n_obs : 1)) % 2);
     for (int i = threadIdx.x; i < 6 * A.P.n_obs; i += kBlock) s_obs[i] = A.obs[i];
+    if (A.P.occ_g) for (int i = threadIdx.x; i < kOccGrid * kOccGrid * kOccGrid; i += kBlock) s_occ[i] = A.occ[i];
     __syncthreads();
     const uint64_t h0 = iter_hash(A.seed, A.iteration);
     for (long long w = (long long)blockIdx.x * kBlock + threadIdx.x; w < A.items; w += (long long)gridDim.x * kBlock) {
@@ -734,7 +751,7 @@ __global__ void __launch_bounds__(kBlock) batch_kernel(const __grid_constant__ B
 #pragma unroll
         for (int d = 0; d < N; ++d) x0[d] = (R)A.states[slot * N + d];
         ItemOut<R, N> o;
-        integrate_and_map<M, R>(A.P, s_obs, x0, u, dt, S, o);
+        integrate_and_map<M, R>(A.P, s_obs, s_occ, x0, u, dt, S, o);
 #pragma unroll
         for (int d = 0; d < N; ++d) A.o_end[w * N + d] = (double)o.end[d];
 #pragma unroll
