@@ -94,6 +94,8 @@ typedef struct kpx_trace {
     int32_t iteration, branching;
     int64_t ve_size, vo_size, attempted, valid, staged, appended, tree_size;
     double elapsed_ms;
+    double phase_ms[6];  /* device time of this iteration's phases: order/S0, propagate/S1, gate/S2, append+estimates/S3,
+                            node sets/S4, epilogue (scan, rescue, trace) */
 } kpx_trace;
 
 typedef struct kpx_plan kpx_plan;

@@ -50,7 +50,7 @@ class Trace(C.Structure):
     _fields_ = [
         ("iteration", C.c_int32), ("branching", C.c_int32), ("ve_size", C.c_int64), ("vo_size", C.c_int64),
         ("attempted", C.c_int64), ("valid", C.c_int64), ("staged", C.c_int64), ("appended", C.c_int64),
-        ("tree_size", C.c_int64), ("elapsed_ms", C.c_double),
+        ("tree_size", C.c_int64), ("elapsed_ms", C.c_double), ("phase_ms", C.c_double * 6),
     ]
 
 

@@ -60,7 +60,8 @@ int upload_obstacles(const kpx_problem& pr, int precision, int n_obs, const doub
     if (n_obs == 0) return KPX_OK;
     {
         std::vector<uint32_t> masks((size_t)kOccGrid * kOccGrid * kOccGrid);
-        build_occupancy_masks(pr, n_obs, omin, omax, masks.data());
+        if (precision == KPX_F64) occupancy_masks_f64(pr, n_obs, omin, omax, masks.data());
+        else occupancy_masks_f32(pr, n_obs, omin, omax, masks.data());
         CU(cudaMemcpyAsync(occ_dev, masks.data(), masks.size() * 4, cudaMemcpyHostToDevice, st));
         CU(cudaStreamSynchronize(st));
     }
@@ -185,13 +186,14 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     const size_t cp = (size_t)b.cap_pad, R = (size_t)b.regions, pairs = R * (size_t)b.subs;
     Carver c;
     struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, it_end,
-                        it_code, it_rank, it_parent, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
+                        it_code, it_rank, it_parent, it_bin, order, bin_cursor, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
                         ch_dt, ch_slot, ch_end, packet; } o;
     o.states = c.take(b.rs * n * cp); o.control = c.take(b.rs * nu * cp); o.dt = c.take(b.rs * cp);
     o.parent = c.take(4 * cp); o.region = c.take(4 * cp); o.tag = c.take(cp);
     o.n_valid = c.take(4 * R); o.n_invalid = c.take(4 * R); o.cov = c.take(4 * R); o.avail = c.take(4 * R);
     o.score = c.take(8 * R); o.claim = c.take(4 * (pairs + 4));
     o.it_end = c.take(b.rs * n * cp); o.it_code = c.take(4 * cp); o.it_rank = c.take(4 * cp); o.it_parent = c.take(4 * cp);
+    o.it_bin = c.take(cp); o.order = c.take(4 * cp); o.bin_cursor = c.take(4 * (size_t)kBins);
     o.e_local = c.take(4 * cp); o.cnt_e = c.take(4 * (size_t)b.max_chunks); o.cnt_k = c.take(4 * (size_t)b.max_chunks);
     o.partial = c.take(8 * (size_t)team_ctas); o.bar = c.take(256); o.ctl = c.take(sizeof(Ctl));
     o.trace = c.take(sizeof(kpx_trace) * (size_t)b.max_trace);
@@ -215,6 +217,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         w.avail_it = (int*)(s + o.avail); w.score = (double*)(s + o.score); w.claim = (uint32_t*)(s + o.claim);
         w.it_end = s + o.it_end; w.it_code = (uint32_t*)(s + o.it_code); w.it_rank = (int*)(s + o.it_rank);
         w.it_parent = (int*)(s + o.it_parent); w.e_local = (int*)(s + o.e_local);
+        w.it_bin = (uint8_t*)(s + o.it_bin); w.order = (int*)(s + o.order); w.bin_cursor = (unsigned int*)(s + o.bin_cursor);
         w.cnt_expand = (int*)(s + o.cnt_e); w.cnt_keep = (int*)(s + o.cnt_k); w.partial = (double*)(s + o.partial);
         w.bar = (unsigned int*)(s + o.bar); w.ctl = (Ctl*)(s + o.ctl); w.trace = (kpx_trace*)(s + o.trace);
         w.chain_start = (double*)(s + o.ch_start); w.chain_control = (double*)(s + o.ch_ctrl);

@@ -96,21 +96,26 @@ inline void fill_params(Params<R>& P, const kpx_problem& pr) {
     }
 }
 
-// Host: cell -> bitmask of the obstacles whose closed box can contain a point of that cell.  One cell of
-// margin on every side absorbs any rounding of the device-side cell lookup, so the mask is conservative
-// and the exact closed-box test on the flagged obstacles gives the same verdict as testing all of them.
-inline void build_occupancy_masks(const kpx_problem& pr, int n_obs, const double* omin, const double* omax,
+// Cell of a coordinate along one axis.  Both operations round monotonically, so p in [omin, omax] implies
+// cell(omin) <= cell(p) <= cell(omax): computing an obstacle's cell range with this very function (same
+// precision, same constants) yields masks that are exactly conservative without any safety margin.
+template <class R>
+__host__ __device__ __forceinline__ int occ_cell(R p, R lo, R inv) {
+    int c = (int)((p - lo) * inv);
+    return c < 0 ? 0 : (c > kOccGrid - 1 ? kOccGrid - 1 : c);
+}
+
+// Host: cell -> bitmask of the obstacles whose closed box (as rounded to R) can contain a point of that cell.
+template <class R>
+inline void build_occupancy_masks(const Params<R>& P, int n_obs, const double* omin, const double* omax,
                                   uint32_t* masks /* kOccGrid^3 */) {
     const int G = kOccGrid;
     for (int i = 0; i < G * G * G; ++i) masks[i] = 0u;
     for (int k = 0; k < n_obs && k < 32; ++k) {
         int lo[3], hi[3];
         for (int a = 0; a < 3; ++a) {
-            const double cs = (pr.state_hi[a] - pr.state_lo[a]) / G;
-            lo[a] = (int)floor((omin[3 * k + a] - pr.state_lo[a]) / cs) - 1;
-            hi[a] = (int)floor((omax[3 * k + a] - pr.state_lo[a]) / cs) + 1;
-            lo[a] = lo[a] < 0 ? 0 : lo[a];
-            hi[a] = hi[a] > G - 1 ? G - 1 : hi[a];
+            lo[a] = occ_cell<R>((R)omin[3 * k + a], P.occ_lo[a], P.occ_inv[a]);
+            hi[a] = occ_cell<R>((R)omax[3 * k + a], P.occ_lo[a], P.occ_inv[a]);
         }
         for (int x = lo[0]; x <= hi[0]; ++x)
             for (int y = lo[1]; y <= hi[1]; ++y)
@@ -294,10 +299,9 @@ template <class R>
 __device__ __forceinline__ bool point_hits_grid(const Params<R>& P, R px, R py, R pz, const R* __restrict__ s_obs,
                                                 const uint32_t* __restrict__ s_occ, int n_obs) {
     if (P.occ_g == 0) return point_hits<R>(px, py, pz, s_obs, n_obs);
-    int ix = (int)((px - P.occ_lo[0]) * P.occ_inv[0]);
-    int iy = (int)((py - P.occ_lo[1]) * P.occ_inv[1]);
-    int iz = (int)((pz - P.occ_lo[2]) * P.occ_inv[2]);
-    ix = min(max(ix, 0), kOccGrid - 1); iy = min(max(iy, 0), kOccGrid - 1); iz = min(max(iz, 0), kOccGrid - 1);
+    const int ix = occ_cell<R>(px, P.occ_lo[0], P.occ_inv[0]);
+    const int iy = occ_cell<R>(py, P.occ_lo[1], P.occ_inv[1]);
+    const int iz = occ_cell<R>(pz, P.occ_lo[2], P.occ_inv[2]);
     uint32_t m = s_occ[(ix * kOccGrid + iy) * kOccGrid + iz];
     bool h = false;
     while (m) {
@@ -353,11 +357,15 @@ __device__ __forceinline__ void integrate_and_map(const Params<R>& P, const R* _
             if (ok && n_obs > 0) {
                 R dx = cur[0] - prev0, dy = cur[1] - prev1, dz = cur[2] - prev2;
                 R dist = MathK<R>::sq(dx * dx + dy * dy + dz * dz);
+                // smallest power of two with steps * res >= dist (validity.py:26-31).  res * 2^k and 2^-k are
+                // exact, so doubling the threshold / halving the fraction reproduces steps * res and j / steps
+                // bit for bit without integer->float conversions.
                 int steps = 1;
-                while ((R)steps * P.check_res < dist) steps <<= 1;
-                const R inv_steps = (R)1 / (R)steps;          // steps is a power of two: j * inv_steps == j / steps exactly
+                R thr = P.check_res, inv_steps = (R)1;
+                while (thr < dist) { thr += thr; inv_steps *= (R)0.5; steps <<= 1; }
+                R t = (R)0;
                 for (int j = 1; j < steps; ++j) {
-                    R t = (R)j * inv_steps;
+                    t += inv_steps;
                     ++points;
                     if (point_hits_grid<R>(P, prev0 + t * dx, prev1 + t * dy, prev2 + t * dz, s_obs, s_occ, n_obs)) { ok = false; break; }
                 }
@@ -418,6 +426,16 @@ __device__ __forceinline__ void sample_control(const Params<R>& P, uint64_t h0, 
     *dt = (R)d;
     int s = (int)ceil(__ddiv_rn((double)(*dt), 0.02));
     *substeps = s < 4 ? 4 : s;
+}
+
+// substep count of item (slot, ext) alone: the duration draw and the same rounding as sample_control
+template <class M, class R>
+__device__ __forceinline__ int substeps_of(const Params<R>& P, uint64_t h0, int slot, int ext) {
+    const uint64_t key = mix64(slot_ext_hash(h0, (uint64_t)slot, (uint64_t)ext) ^ (uint64_t)PH_SAMPLE);
+    const double d = __dmul_rn(__dsub_rn(1.0, unit53(draw_u64(key, (uint64_t)M::NU))), P.t_prop);
+    const R dt = (R)d;
+    const int s = (int)ceil(__ddiv_rn((double)dt, 0.02));
+    return s < 4 ? 4 : s;
 }
 
 }  // namespace kpx

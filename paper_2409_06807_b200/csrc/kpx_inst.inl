@@ -84,6 +84,13 @@ cudaError_t KPX_CAT(launch_batch_, KPX_SUFFIX)(const BatchLaunch& L, cudaStream_
     return cudaErrorInvalidValue;
 }
 
+void KPX_CAT(occupancy_masks_, KPX_SUFFIX)(const kpx_problem& pr, int n_obs, const double* omin, const double* omax,
+                                           uint32_t* masks) {
+    Params<Real> P;
+    fill_params<Real>(P, pr);
+    build_occupancy_masks<Real>(P, n_obs, omin, omax, masks);
+}
+
 int KPX_CAT(plan_blocks_per_sm_, KPX_SUFFIX)(int model_id, int n, size_t smem) {
 #define CALL(M) return do_occupancy<M>(smem)
     KPX_DISPATCH(CALL)

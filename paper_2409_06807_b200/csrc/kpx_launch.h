@@ -49,6 +49,9 @@ cudaError_t launch_plan_f64(const PlanLaunch& L, cudaStream_t st);
 cudaError_t launch_plan_f32(const PlanLaunch& L, cudaStream_t st);
 cudaError_t launch_batch_f64(const BatchLaunch& L, cudaStream_t st);
 cudaError_t launch_batch_f32(const BatchLaunch& L, cudaStream_t st);
+// host: occupancy masks (kOccGrid^3 words) computed with the launch precision's own cell arithmetic
+void occupancy_masks_f64(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);
+void occupancy_masks_f32(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);
 // co-resident CTAs per SM of the plan kernel for this model (0 if unsupported)
 int plan_blocks_per_sm_f64(int model_id, int n, size_t smem);
 int plan_blocks_per_sm_f32(int model_id, int n, size_t smem);

@@ -57,8 +57,10 @@ struct Ctl {                      // one per workspace, global memory
     int n_trace;
     int chain_len;
     int cur_query;                // batch mode: query index broadcast to the team
+    unsigned int unit_next;       // S1: next 32-item unit of the length-sorted order
 };
 
+constexpr int kBins = 64;          // substep-count bins of the S0 counting sort (S >= 63 share the last bin)
 constexpr int kPacketSegs = 64;    // solution segments carried inline in the result packet
 struct ResultPacket {             // everything the host needs after a run, one D2H copy
     Ctl ctl;
@@ -79,6 +81,9 @@ struct Workspace {                // device pointers of one team's state
     void* it_end;                 // R[n][cap]  end states of this iteration's valid items
     uint32_t* it_code;            // [cap] kItemInvalid | (goal bit | pair)
     int *it_rank, *it_parent;     // [cap]
+    uint8_t* it_bin;              // [cap] substep-count bin of each item
+    int* order;                   // [cap] item numbers sorted by substep count, longest first
+    unsigned int* bin_cursor;     // [kBins] per-bin fill cursor / histogram of the current iteration
     int *e_local;                 // [cap]  chunk-major compacted EXPAND slots
     int *cnt_expand, *cnt_keep;   // [max_chunks]
     double* partial;              // [team_ctas]
@@ -124,21 +129,18 @@ struct Team {
     unsigned int* bar;
 };
 
-// sense-reversing barrier over the team's CTAs (all co-resident: cooperative launch)
+// Barrier over the team's CTAs (all co-resident: cooperative launch).  One atomic per CTA: rank 0 adds
+// 2^31 - (ctas-1), everyone else 1, so the word's top bit flips exactly when the last CTA arrives and the
+// low bits return to their old value; each CTA spins until the top bit differs from what its own add saw.
 __device__ __forceinline__ void team_sync(const Team& T) {
     __syncthreads();
     if (T.ctas > 1) {
         if (threadIdx.x == 0) {
-            volatile unsigned int* gen_p = T.bar + 1;
-            unsigned int gen = *gen_p;
             __threadfence();
-            if (atomicAdd(T.bar, 1u) == (unsigned)T.ctas - 1u) {
-                atomicExch(T.bar, 0u);
-                __threadfence();
-                atomicAdd(T.bar + 1, 1u);
-            } else {
-                while (*gen_p == gen) { __nanosleep(20); }
-            }
+            const unsigned int inc = T.rank == 0 ? 0x80000000u - (unsigned)(T.ctas - 1) : 1u;
+            const unsigned int old = atomicAdd(T.bar, inc);
+            volatile unsigned int* w = T.bar;
+            while (((old ^ *w) & 0x80000000u) == 0u) {}
             __threadfence();
         }
         __syncthreads();
@@ -227,7 +229,7 @@ __device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __
 template <class M, class R>
 __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
                           kpx_query_result* res_out, long long query_index, int* s_prefix, const R* s_obs,
-                          const uint32_t* s_occ, int* s_w, double* s_d) {
+                          const uint32_t* s_occ, int* s_w, double* s_d, int* s_bin) {
     constexpr int N = M::N, NU = M::NU;
     const Params<R>& P = A.P;
     const int tid = threadIdx.x;
@@ -286,7 +288,8 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             ctl->n_items_last = 0; ctl->n_keep_last = 0;
             ctl->cnt_valid[0] = ctl->cnt_valid[1] = ctl->cnt_open[0] = ctl->cnt_open[1] = 0;
             ctl->sum_items = ctl->sum_substeps = ctl->sum_points = ctl->sum_boxsteps = 0ull;
-            ctl->n_trace = 0; ctl->chain_len = 0;
+            ctl->n_trace = 0; ctl->chain_len = 0; ctl->unit_next = 0u;
+            for (int b = 0; b < kBins; ++b) W.bin_cursor[b] = 0u;
         }
         team_sync(T);
         if (keeper) { W.avail_it[__ldcg(W.region)] = 1; ctl->t_reset_done = gtimer(); }
@@ -321,49 +324,119 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
         const int n_ich = (items + kChunk - 1) / kChunk;
         const int n_sch_old = (size + kChunk - 1) / kChunk;
         const uint64_t h0 = iter_hash(seed, (uint64_t)it);
+        unsigned long long tp[7];               // keeper: phase boundary timestamps
+        if (keeper) tp[0] = gtimer();
+
+        // ================================================================= S0: order items by length
+        // The substep count S = max(4, ceil(dt/0.02)) of an item follows from its RNG draw alone.  A counting
+        // sort on S (longest first) lets every warp integrate 32 items of nearly equal length, and warps pull
+        // 32-item units from a shared cursor, so neither lanes nor warps idle behind one long extension.
+        // Results stay indexed by the item number w, so nothing downstream sees the processing order.
+        // An iteration that fits in one round (items <= team threads) gains nothing from it and skips S0.
+        const bool sorted = items > tthreads;
+        if (sorted) {
+            for (int b = tid; b < kBins; b += kBlock) { s_bin[b] = 0; s_bin[2 * kBins + b] = 0; }
+            __syncthreads();
+#pragma unroll 1
+            for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
+                const int w = (int)w0 + tid;
+                if (w < items) {
+                    const int i = w / lam, ext = w - i * lam;
+                    // i-th EXPAND slot: chunk by binary search over the prefix, then the chunk-local list
+                    int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
+                    while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
+                    const int slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
+                    int S = substeps_of<M, R>(P, h0, slot, ext);
+                    S = S < kBins - 1 ? S : kBins - 1;
+                    __stcg(W.it_parent + w, slot);
+                    __stcg(W.it_bin + w, (uint8_t)S);
+                    atomicAdd(&s_bin[S], 1);
+                }
+            }
+            __syncthreads();
+            // reserve this CTA's range inside every bin; the cursor ends up holding the global histogram
+            for (int b = tid; b < kBins; b += kBlock) {
+                const int h = s_bin[b];
+                s_bin[kBins + b] = h ? (int)atomicAdd(W.bin_cursor + b, (unsigned)h) : 0;
+            }
+        }
+        if (sorted) team_sync(T);
+        if (sorted) {
+            if (tid < kBins) s_bin[3 * kBins + tid] = (int)__ldcg(W.bin_cursor + tid);
+            __syncthreads();
+            if (tid == 0) {
+                int acc = 0;
+                for (int b = kBins - 1; b >= 0; --b) { const int h = s_bin[3 * kBins + b]; s_bin[3 * kBins + b] = acc; acc += h; }
+            }
+            __syncthreads();
+#pragma unroll 1
+            for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
+                const int w = (int)w0 + tid;
+                if (w < items) {
+                    const int b = (int)__ldcg(W.it_bin + w);
+                    const int pos = s_bin[3 * kBins + b] + s_bin[kBins + b] + atomicAdd(&s_bin[2 * kBins + b], 1);
+                    __stcg(W.order + pos, w);
+                }
+            }
+        }
+        if (sorted) team_sync(T);
+        if (keeper) tp[1] = gtimer();
 
         // ================================================================= S1
         {
             int my_sub = 0, my_pts = 0, my_valid = 0, my_box = 0;
-            // items are spread over the whole team one per thread per round (S1 needs no chunk alignment;
-            // only the ranking in S2 does), so a 30k-item iteration is one round, not four
-            {
+            const int lane = tid & 31;
+            int static_unit = (T.rank * kBlock + tid) >> 5;     // unsorted: unit = this warp's slice of one round
 #pragma unroll 1
-                for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
-                    const int w = (int)w0 + tid;
-                    const bool active = w < items;
-                    int region = -1; bool valid = false;
-                    if (active) {
-                        const int i = w / lam, ext = w - i * lam;
-                        // i-th EXPAND slot: chunk by binary search over the prefix, then the chunk-local list
+            for (;;) {
+                int unit = static_unit;
+                if (sorted) {
+                    if (lane == 0) unit = (int)atomicAdd(&ctl->unit_next, 1u);
+                    unit = __shfl_sync(0xffffffffu, unit, 0);
+                } else {
+                    static_unit = 0x3fffffff;                   // one round only
+                }
+                if ((long long)unit * 32 >= items) break;
+                const int pos = unit * 32 + lane;
+                const bool active = pos < items;
+                int region = -1; bool valid = false;
+                if (active) {
+                    int w, slot;
+                    if (sorted) {
+                        w = __ldcg(W.order + pos);
+                        slot = __ldcg(W.it_parent + w);
+                    } else {
+                        w = pos;
+                        const int i = w / lam;
                         int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
                         while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
-                        const int slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
-                        R u[NU], dt, x0[N];
-                        int S;
-                        sample_control<M, R>(P, h0, slot, ext, u, &dt, &S, nullptr, nullptr);
-#pragma unroll
-                        for (int d = 0; d < N; ++d) x0[d] = __ldcg(states + (size_t)d * ld + slot);
-                        ItemOut<R, N> o;
-                        integrate_and_map<M, R>(P, s_obs, s_occ, x0, u, dt, S, o);
-                        my_sub += o.substeps; my_pts += o.points; my_box += o.boxsteps;
-                        region = o.region; valid = o.valid;
-                        uint32_t code = kItemInvalid;
-                        if (valid) {
-                            ++my_valid;
-                            const uint32_t pair = (uint32_t)region * (uint32_t)SUBS + (uint32_t)o.sub;
-                            R d0 = o.end[0] - goal[0], d1 = o.end[1] - goal[1], d2 = o.end[2] - goal[2];
-                            const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= goal[3];
-                            code = pair | (hit ? kItemGoalBit : 0u);
-#pragma unroll
-                            for (int d = 0; d < N; ++d) __stcg(it_end + (size_t)d * ld + w, o.end[d]);
-                            if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
-                        }
-                        __stcg(W.it_code + w, code);
+                        slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
                         __stcg(W.it_parent + w, slot);
                     }
-                    count_outcome(W.n_valid, W.n_invalid, region, valid, active);
+                    const int ext = w % lam;
+                    R u[NU], dt, x0[N];
+                    int S;
+                    sample_control<M, R>(P, h0, slot, ext, u, &dt, &S, nullptr, nullptr);
+#pragma unroll
+                    for (int d = 0; d < N; ++d) x0[d] = __ldcg(states + (size_t)d * ld + slot);
+                    ItemOut<R, N> o;
+                    integrate_and_map<M, R>(P, s_obs, s_occ, x0, u, dt, S, o);
+                    my_sub += o.substeps; my_pts += o.points; my_box += o.boxsteps;
+                    region = o.region; valid = o.valid;
+                    uint32_t code = kItemInvalid;
+                    if (valid) {
+                        ++my_valid;
+                        const uint32_t pair = (uint32_t)region * (uint32_t)SUBS + (uint32_t)o.sub;
+                        R d0 = o.end[0] - goal[0], d1 = o.end[1] - goal[1], d2 = o.end[2] - goal[2];
+                        const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= goal[3];
+                        code = pair | (hit ? kItemGoalBit : 0u);
+#pragma unroll
+                        for (int d = 0; d < N; ++d) __stcg(it_end + (size_t)d * ld + w, o.end[d]);
+                        if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
+                    }
+                    __stcg(W.it_code + w, code);
                 }
+                count_outcome(W.n_valid, W.n_invalid, region, valid, active);
             }
             // work counters: one atomic per warp
 #pragma unroll
@@ -373,7 +446,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                 my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
                 my_box += __shfl_xor_sync(0xffffffffu, my_box, o);
             }
-            if ((tid & 31) == 0 && (my_sub | my_pts | my_valid)) {
+            if (lane == 0 && (my_sub | my_pts | my_valid)) {
                 atomicAdd(&ctl->sum_substeps, (unsigned long long)my_sub);
                 atomicAdd(&ctl->sum_points, (unsigned long long)my_pts);
                 atomicAdd(&ctl->sum_boxsteps, (unsigned long long)my_box);
@@ -381,6 +454,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             }
         }
         team_sync(T);
+        if (keeper) tp[2] = gtimer();
 
         // ================================================================= S2
         for (int c = T.rank; c < n_ich; c += T.ctas) {
@@ -428,6 +502,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             if (tid == 0) __stcg(W.cnt_keep + c, tot);
         }
         team_sync(T);
+        if (keeper) tp[3] = gtimer();
 
         // ================================================================= S3
         const int k_keep = scan_counts(W.cnt_keep, n_ich, s_prefix, s_w);
@@ -490,6 +565,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
         }
         const int new_size = size + n_app;
         team_sync(T);
+        if (keeper) tp[4] = gtimer();
 
         // ================================================================= S4
         double total;
@@ -556,6 +632,8 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
         }
         if (keeper) {
             __stcg(&ctl->first_hit_w, 0x7fffffff);
+            __stcg(&ctl->unit_next, 0u);
+            for (int b = 0; b < kBins; ++b) __stcg(W.bin_cursor + b, 0u);
             atomicAdd(&ctl->sum_items, (unsigned long long)items);
             const double el = (double)(gtimer() - t_start) * 1e-9;
             int stop = 0;
@@ -564,6 +642,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             if (stop) ctl->stop = stop;
         }
         team_sync(T);
+        if (keeper) tp[5] = gtimer();
 
         // ================================================= epilogue of the iteration
         ve = scan_counts(W.cnt_expand, (new_size + kChunk - 1) / kChunk, s_prefix, s_w);
@@ -600,7 +679,9 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                 kpx_trace tr;
                 tr.iteration = it; tr.branching = lam; tr.ve_size = items / lam; tr.vo_size = __ldcg(&ctl->cnt_open[par]);
                 tr.attempted = items; tr.valid = __ldcg(&ctl->cnt_valid[par]); tr.staged = k_keep; tr.appended = n_app;
-                tr.tree_size = new_size; tr.elapsed_ms = (double)(gtimer() - t_start) * 1e-6;
+                tp[6] = gtimer();
+                tr.tree_size = new_size; tr.elapsed_ms = (double)(tp[6] - t_start) * 1e-6;
+                for (int ph = 0; ph < 6; ++ph) tr.phase_ms[ph] = (double)(tp[ph + 1] - tp[ph]) * 1e-6;
                 W.trace[nt] = tr;
                 ctl->n_trace = nt + 1;
             }
@@ -681,6 +762,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
     __shared__ int s_w[kBlock / 32 + 1];
     __shared__ double s_d[kBlock / 32];
     __shared__ int s_q;
+    __shared__ int s_bin[4 * kBins];      // S0: local histogram | CTA base | local fill | global bin start
 
     for (int i = threadIdx.x; i < 6 * A.P.n_obs; i += kBlock) s_obs[i] = A.obs[i];
     if (A.P.occ_g) for (int i = threadIdx.x; i < kOccGrid * kOccGrid * kOccGrid; i += kBlock) s_occ[i] = A.occ[i];
@@ -695,7 +777,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
     T.bar = W.bar;
 
     if (A.queue == nullptr) {       // single query bound to team 0 (plan handle: stepped / resumable)
-        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_obs, s_occ, s_w, s_d);
+        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_obs, s_occ, s_w, s_d, s_bin);
         return;
     }
     for (;;) {                      // batch: teams pull queries until the queue is drained
@@ -712,7 +794,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
         const int q = s_q;
         __syncthreads();
         if (q >= A.n_queries) return;
-        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_obs, s_occ, s_w, s_d);
+        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_obs, s_occ, s_w, s_d, s_bin);
         team_sync(T);
     }
 }

@@ -59,6 +59,7 @@ class IterationTrace:
     tree_size: int
     elapsed_s: float
     valid: int = 0
+    phase_ms: tuple = ()   # device time per phase: order, propagate, gate, append+estimates, node sets, epilogue
 
 
 class TreeArena:
@@ -210,7 +211,7 @@ class KinoPax:
         cnt = C.c_int32(0)
         _lib.check(self._lib.kpx_plan_trace(self._handle, 4096, buf, C.byref(cnt)), "kpx_plan_trace")
         return [IterationTrace(t.iteration, t.branching, t.ve_size, t.vo_size, t.attempted, t.staged, t.appended,
-                               t.tree_size, t.elapsed_ms * 1e-3, t.valid) for t in buf[: cnt.value]]
+                               t.tree_size, t.elapsed_ms * 1e-3, t.valid, tuple(t.phase_ms)) for t in buf[: cnt.value]]
 
     def load_state(self, snapshot: dict, regions: dict, iteration: int, seed: Optional[int] = None) -> None:
         """Restore a tree + region state (checkpoint/resume; parity tests load oracle states)."""

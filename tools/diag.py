@@ -26,7 +26,9 @@ def run(model_name, scene, backend, seeds=(0, 1, 2), t_e=None, team=0):
             prev = 0.0
             for tr in eng.traces():
                 print(f"   it {tr.iteration:2d} lam {tr.branching:2d} ve {tr.ve_size:6d} items {tr.attempted:7d} valid {tr.valid:7d} "
-                      f"staged {tr.staged:6d} app {tr.appended:6d} tree {tr.tree_size:7d}  +{1e3*tr.elapsed_s-prev:.3f} ms")
+                      f"staged {tr.staged:6d} app {tr.appended:6d} tree {tr.tree_size:7d}  +{1e3*tr.elapsed_s-prev:.3f} ms  "
+                      f"[S0 {1e3*tr.phase_ms[0]:.0f} S1 {1e3*tr.phase_ms[1]:.0f} S2 {1e3*tr.phase_ms[2]:.0f} "
+                      f"S3 {1e3*tr.phase_ms[3]:.0f} S4 {1e3*tr.phase_ms[4]:.0f} epi {1e3*tr.phase_ms[5]:.0f} us]")
                 prev = 1e3 * tr.elapsed_s
     eng.close()
 
