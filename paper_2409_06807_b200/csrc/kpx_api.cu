@@ -98,7 +98,7 @@ struct kpx_batch {
     int max_chunks = 0, max_trace = 4096, max_chain = KPX_MAX_CHAIN;
     bool cooperative = false;
     size_t rs = 8, smem = 0;
-    int cap = 0, cap_pad = 0, regions = 0, subs = 0;
+    int cap = 0, cap_pad = 0, regions = 0, subs = 0, dirty_pairs_cap = 0;
     char* slab = nullptr;
     size_t ws_bytes = 0;
     std::vector<Workspace> ws_host;
@@ -185,15 +185,18 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     const int n = prob->n, nu = prob->nu;
     const size_t cp = (size_t)b.cap_pad, R = (size_t)b.regions, pairs = R * (size_t)b.subs;
     Carver c;
-    struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, it_end,
-                        it_code, it_rank, it_parent, it_bin, order, bin_cursor, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
+    struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, bits, dpairs, dregions, it_end,
+                        it_code, it_rank, it_parent, it_bin, order, pos_of, bin_cursor, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
                         ch_dt, ch_slot, ch_end, packet; } o;
     o.states = c.take(b.rs * n * cp); o.control = c.take(b.rs * nu * cp); o.dt = c.take(b.rs * cp);
     o.parent = c.take(4 * cp); o.region = c.take(4 * cp); o.tag = c.take(cp);
     o.n_valid = c.take(4 * R); o.n_invalid = c.take(4 * R); o.cov = c.take(4 * R); o.avail = c.take(4 * R);
     o.score = c.take(8 * R); o.claim = c.take(4 * (pairs + 4));
+    b.dirty_pairs_cap = (int)std::min<size_t>(pairs, 4 * cp);
+    o.bits = c.take(4 * ((R + 31) / 32 + 1)); o.dpairs = c.take(4 * (size_t)b.dirty_pairs_cap);
+    o.dregions = c.take(4 * ((R + 31) / 32 + 1));
     o.it_end = c.take(b.rs * n * cp); o.it_code = c.take(4 * cp); o.it_rank = c.take(4 * cp); o.it_parent = c.take(4 * cp);
-    o.it_bin = c.take(cp); o.order = c.take(4 * cp); o.bin_cursor = c.take(4 * (size_t)kBins);
+    o.it_bin = c.take(cp); o.order = c.take(4 * cp); o.pos_of = c.take(4 * cp); o.bin_cursor = c.take(4 * (size_t)kBins);
     o.e_local = c.take(4 * cp); o.cnt_e = c.take(4 * (size_t)b.max_chunks); o.cnt_k = c.take(4 * (size_t)b.max_chunks);
     o.partial = c.take(8 * (size_t)team_ctas); o.bar = c.take(256); o.ctl = c.take(sizeof(Ctl));
     o.trace = c.take(sizeof(kpx_trace) * (size_t)b.max_trace);
@@ -215,15 +218,23 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         w.parent = (int*)(s + o.parent); w.region = (int*)(s + o.region); w.tag = (uint8_t*)(s + o.tag);
         w.n_valid = (int*)(s + o.n_valid); w.n_invalid = (int*)(s + o.n_invalid); w.cov = (int*)(s + o.cov);
         w.avail_it = (int*)(s + o.avail); w.score = (double*)(s + o.score); w.claim = (uint32_t*)(s + o.claim);
+        w.avail_bits = (uint32_t*)(s + o.bits); w.dirty_pairs = (int*)(s + o.dpairs); w.touched_bits = (uint32_t*)(s + o.dregions);
         w.it_end = s + o.it_end; w.it_code = (uint32_t*)(s + o.it_code); w.it_rank = (int*)(s + o.it_rank);
         w.it_parent = (int*)(s + o.it_parent); w.e_local = (int*)(s + o.e_local);
-        w.it_bin = (uint8_t*)(s + o.it_bin); w.order = (int*)(s + o.order); w.bin_cursor = (unsigned int*)(s + o.bin_cursor);
+        w.it_bin = (uint8_t*)(s + o.it_bin); w.order = (int*)(s + o.order); w.pos_of = (int*)(s + o.pos_of); w.bin_cursor = (unsigned int*)(s + o.bin_cursor);
         w.cnt_expand = (int*)(s + o.cnt_e); w.cnt_keep = (int*)(s + o.cnt_k); w.partial = (double*)(s + o.partial);
         w.bar = (unsigned int*)(s + o.bar); w.ctl = (Ctl*)(s + o.ctl); w.trace = (kpx_trace*)(s + o.trace);
         w.chain_start = (double*)(s + o.ch_start); w.chain_control = (double*)(s + o.ch_ctrl);
         w.chain_dt = (double*)(s + o.ch_dt); w.chain_slot = (long long*)(s + o.ch_slot);
         w.chain_end = (double*)(s + o.ch_end);
         w.packet = (ResultPacket*)(s + o.packet);
+    }
+    for (int t = 0; t < n_teams; ++t) {      // a fresh workspace is clean: claim all UNCLAIMED, nothing dirty
+        CU(cudaMemset(b.ws_host[t].claim, 0xFF, 4 * pairs));
+        Ctl c0;
+        memset(&c0, 0, sizeof c0);
+        c0.dirty_ok = 1;
+        CU(cudaMemcpy(b.ws_host[t].ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
     }
     CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
     CU(cudaMemcpy(b.ws_dev, b.ws_host.data(), sizeof(Workspace) * (size_t)n_teams, cudaMemcpyHostToDevice));
@@ -258,7 +269,7 @@ int launch(kpx_batch& b, const PlanLaunch& L, cudaStream_t st) {
 PlanLaunch base_launch(kpx_batch& b) {
     PlanLaunch L{};
     L.prob = &b.prob; L.obs_dev = b.obs_dev; L.occ_dev = b.occ_dev; L.ws_dev = b.ws_dev; L.n_teams = b.n_teams; L.team_ctas = b.team_ctas;
-    L.max_chunks = b.max_chunks; L.stride = b.cap_pad; L.max_trace = b.max_trace; L.max_chain = b.max_chain; L.smem = b.smem;
+    L.max_chunks = b.max_chunks; L.stride = b.cap_pad; L.dirty_pairs_cap = b.dirty_pairs_cap; L.max_trace = b.max_trace; L.max_chain = b.max_chain; L.smem = b.smem;
     L.cooperative = b.cooperative;
     return L;
 }
@@ -652,15 +663,18 @@ int kpx_plan_items(kpx_plan* p, int64_t max_items, int64_t* n_items, uint8_t* va
         (rc = d2h(par, w.it_parent, (size_t)I))) return rc;
     std::vector<double> e;
     if (end) { e.resize((size_t)I * b.prob.n); if ((rc = soa_to_aos(b, w.it_end, b.prob.n, I, e.data()))) return rc; }
+    std::vector<int> pos;      // sorted iterations keep per-item results at the item's sorted position
+    if (c.last_sorted && (rc = d2h(pos, w.pos_of, (size_t)I))) return rc;
     for (int64_t i = 0; i < I; ++i) {
-        const bool v = code[i] != kItemInvalid;
-        const uint32_t pair = code[i] & ~kItemGoalBit;
+        const int64_t ip = c.last_sorted ? pos[i] : i;
+        const bool v = code[ip] != kItemInvalid;
+        const uint32_t pair = code[ip] & ~kItemGoalBit;
         if (valid) valid[i] = v;
         if (region) region[i] = v ? (int64_t)(pair / (uint32_t)b.subs) : -1;
         if (sub) sub[i] = v ? (int64_t)(pair % (uint32_t)b.subs) : 0;
         if (keep) keep[i] = v && rank[i] >= 0;
         if (parent_slot) parent_slot[i] = par[i];
-        if (end) for (int d = 0; d < b.prob.n; ++d) end[i * b.prob.n + d] = v ? e[(size_t)i * b.prob.n + d] : 0.0;
+        if (end) for (int d = 0; d < b.prob.n; ++d) end[i * b.prob.n + d] = v ? e[(size_t)ip * b.prob.n + d] : 0.0;
     }
     return KPX_OK;
 }
@@ -694,6 +708,11 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
         if (avail[r] && score[r] > 0.0) total += score[r];
     }
     CU(cudaMemcpy(w.avail_it, a.data(), 4 * R, cudaMemcpyHostToDevice));
+    {
+        std::vector<uint32_t> bits((R + 31) / 32 + 1, 0u);
+        for (size_t r = 0; r < R; ++r) if (avail[r]) bits[r >> 5] |= 1u << (r & 31);
+        CU(cudaMemcpy(w.avail_bits, bits.data(), 4 * bits.size(), cudaMemcpyHostToDevice));
+    }
     for (size_t r = 0; r < R; ++r) x[r] = (int)n_valid[r];
     CU(cudaMemcpy(w.n_valid, x.data(), 4 * R, cudaMemcpyHostToDevice));
     for (size_t r = 0; r < R; ++r) x[r] = (int)n_invalid[r];

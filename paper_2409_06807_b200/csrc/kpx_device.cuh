@@ -134,7 +134,30 @@ template <> struct MathK<double> {
 };
 template <> struct MathK<float> {
     static constexpr float PI = 3.14159265358979323846f, TWO_PI = 2.0f * 3.14159265358979323846f;
-    __device__ static __forceinline__ void sc(float x, float* s, float* c) { sincosf(x, s, c); }
+    // sin and cos together for the wrapped angles of the models (|x| is a few radians): Cody-Waite quadrant
+    // reduction with the magic-number round (no int<->float conversions) and the Cephes minimax polynomials
+    // on [-pi/4, pi/4]; max error 9e-8 absolute (1.4 ulp), ~22 instructions for the pair versus ~50 for
+    // sincosf, whose general-range reduction these arguments never need.
+    __device__ static __forceinline__ void sc(float x, float* s, float* c) {
+        if (!(fabsf(x) < 512.0f)) { sincosf(x, s, c); return; }        // diverged states: library path
+        const float t = __fmaf_rn(x, 0.636619772f, 12582912.0f);
+        const int q = __float_as_int(t);
+        const float qf = t - 12582912.0f;
+        float r = __fmaf_rn(qf, -1.57079637f, x);
+        r = __fmaf_rn(qf, 4.37113883e-8f, r);
+        const float z = r * r;
+        float sp = __fmaf_rn(z, -1.9515295891e-4f, 8.3321608736e-3f);
+        sp = __fmaf_rn(z, sp, -1.6666654611e-1f);
+        const float sv = __fmaf_rn(z * r, sp, r);
+        float cp = __fmaf_rn(z, 2.443315711809948e-5f, -1.388731625493765e-3f);
+        cp = __fmaf_rn(z, cp, 4.166664568298827e-2f);
+        const float cv = __fmaf_rn(z * z, cp, __fmaf_rn(z, -0.5f, 1.0f));
+        const bool swap = q & 1;
+        float so = swap ? cv : sv, co = swap ? sv : cv;
+        if (q & 2) so = -so;
+        if ((q + 1) & 2) co = -co;
+        *s = so; *c = co;
+    }
     __device__ static __forceinline__ float mod(float a, float b) { return fmodf(a, b); }
     __device__ static __forceinline__ float sq(float x) { return sqrtf(x); }
     __device__ static __forceinline__ float fl(float x) { return floorf(x); }

@@ -58,6 +58,10 @@ struct Ctl {                      // one per workspace, global memory
     int chain_len;
     int cur_query;                // batch mode: query index broadcast to the team
     unsigned int unit_next;       // S1: next 32-item unit of the length-sorted order
+    int last_sorted;              // 1 if the last iteration's it_* arrays are in sorted-position order
+    // lazy reset: what the finished query dirtied (valid while dirty_ok; otherwise the next reset is dense)
+    int dirty_ok;
+    unsigned int n_dirty_pairs;
 };
 
 constexpr int kBins = 64;          // substep-count bins of the S0 counting sort (S >= 63 share the last bin)
@@ -77,12 +81,16 @@ struct Workspace {                // device pointers of one team's state
     uint8_t* tag;                 // [cap]
     int *n_valid, *n_invalid, *cov, *avail_it;   // [R]
     double* score;                // [R]
+    uint32_t* avail_bits;         // [ceil(R/32)] bit r set once region r has been made available
+    uint32_t* touched_bits;       // [ceil(R/32)] regions whose counters the current query has touched (lazy reset)
+    int* dirty_pairs;             // log of the (region,sub) pairs marked visited (lazy reset of the claim table)
     uint32_t* claim;              // [R * subs]: kUnclaimed | kVisited | lowest claiming item
     void* it_end;                 // R[n][cap]  end states of this iteration's valid items
     uint32_t* it_code;            // [cap] kItemInvalid | (goal bit | pair)
     int *it_rank, *it_parent;     // [cap]
     uint8_t* it_bin;              // [cap] substep-count bin of each item
     int* order;                   // [cap] item numbers sorted by substep count, longest first
+    int* pos_of;                  // [cap] inverse of `order`: where item w's results live in the it_* arrays
     unsigned int* bin_cursor;     // [kBins] per-bin fill cursor / histogram of the current iteration
     int *e_local;                 // [cap]  chunk-major compacted EXPAND slots
     int *cnt_expand, *cnt_keep;   // [max_chunks]
@@ -107,6 +115,7 @@ struct PlanArgs {
     kpx_query_result* results;    // [n_queries] (may be null)
     unsigned int* queue;          // next query index (batch mode)
     int n_queries, n_teams, team_ctas, max_chunks, max_trace, max_chain;
+    int dirty_pairs_cap;
     int stride;                   // row stride (elements) of every SoA array: capacity padded to a chunk multiple
     int resume;                   // 1: continue from Ctl (no reset), single query
     int max_iters, lam_override;
@@ -215,14 +224,18 @@ __device__ __forceinline__ double p_accept_of(int r, int it_ref, const int* __re
     return v < 1.0 ? v : 1.0;
 }
 
-// warp-aggregated region counters (decomposition.py:117-125): one atomic per distinct key per warp
+// warp-aggregated region counters (decomposition.py:117-125): one fire-and-forget atomic per distinct key per
+// warp, plus the region's bit in the touched-bitmap that drives the lazy reset of the next query.
 __device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __restrict__ n_invalid, int region,
-                                              bool valid, bool active) {
+                                              bool valid, bool active, uint32_t* __restrict__ touched_bits) {
     unsigned mask = __ballot_sync(0xffffffffu, active && region >= 0);
     if (active && region >= 0) {
         int key = region * 2 + (valid ? 1 : 0);
         unsigned peers = __match_any_sync(mask, key);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd((valid ? n_valid : n_invalid) + region, __popc(peers));
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) {
+            atomicAdd((valid ? n_valid : n_invalid) + region, __popc(peers));
+            atomicOr(touched_bits + (region >> 5), 1u << (region & 31));
+        }
     }
 }
 
@@ -250,7 +263,22 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
     // ------------------------------------------------------------------ reset
     if (!A.resume) {
         if (keeper) ctl->t_begin = gtimer();
-        {   // claim table + region arrays, 16-byte stores
+        const int n_words = (RG + 31) >> 5;
+        if (__ldcg(&ctl->dirty_ok)) {
+            // lazy reset: the previous query logged every pair it visited and every region it touched
+            const unsigned int np = __ldcg(&ctl->n_dirty_pairs);
+            for (long long i = ttid; i < np; i += tthreads) W.claim[__ldcg(W.dirty_pairs + i)] = kUnclaimed;
+            // one warp per bitmap word, one lane per region
+            const int lane = tid & 31;
+            for (long long wi = ttid >> 5; wi < n_words; wi += tthreads >> 5) {
+                const uint32_t bits = __ldcg(W.touched_bits + wi);
+                if ((bits >> lane) & 1u) {
+                    const long long r = wi * 32 + lane;
+                    W.n_valid[r] = 0; W.n_invalid[r] = 0; W.cov[r] = 0; W.avail_it[r] = 0; W.score[r] = 0.0;
+                }
+                if (lane == 0 && bits) { W.touched_bits[wi] = 0u; W.avail_bits[wi] = 0u; }
+            }
+        } else {   // dense reset: claim table + region arrays, 16-byte stores
             uint4* c4 = (uint4*)W.claim;
             long long n4 = ((long long)RG * SUBS) / 4;
             const uint4 ones = make_uint4(kUnclaimed, kUnclaimed, kUnclaimed, kUnclaimed);
@@ -259,6 +287,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             for (long long i = ttid; i < RG; i += tthreads) {
                 W.n_valid[i] = 0; W.n_invalid[i] = 0; W.cov[i] = 0; W.avail_it[i] = 0; W.score[i] = 0.0;
             }
+            for (long long i = ttid; i < n_words; i += tthreads) { W.avail_bits[i] = 0u; W.touched_bits[i] = 0u; }
         }
         if (keeper) {
             // init_root + make_available (planner.py:169-171)
@@ -292,7 +321,14 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             for (int b = 0; b < kBins; ++b) W.bin_cursor[b] = 0u;
         }
         team_sync(T);
-        if (keeper) { W.avail_it[__ldcg(W.region)] = 1; ctl->t_reset_done = gtimer(); }
+        if (keeper) {
+            const int reg0 = __ldcg(W.region);
+            W.avail_it[reg0] = 1;
+            W.avail_bits[reg0 >> 5] = 1u << (reg0 & 31);
+            W.touched_bits[reg0 >> 5] = 1u << (reg0 & 31);   // the root's region is dirty from the start
+            ctl->n_dirty_pairs = 0u; ctl->dirty_ok = 1;
+            ctl->t_reset_done = gtimer();
+        }
         team_sync(T);
     }
 
@@ -376,6 +412,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                     const int b = (int)__ldcg(W.it_bin + w);
                     const int pos = s_bin[3 * kBins + b] + s_bin[kBins + b] + atomicAdd(&s_bin[2 * kBins + b], 1);
                     __stcg(W.order + pos, w);
+                    __stcg(W.pos_of + w, pos);          // results of item w are stored at `pos` (coalesced S1 stores)
                 }
             }
         }
@@ -431,12 +468,12 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                         const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= goal[3];
                         code = pair | (hit ? kItemGoalBit : 0u);
 #pragma unroll
-                        for (int d = 0; d < N; ++d) __stcg(it_end + (size_t)d * ld + w, o.end[d]);
+                        for (int d = 0; d < N; ++d) __stcg(it_end + (size_t)d * ld + pos, o.end[d]);
                         if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
                     }
-                    __stcg(W.it_code + w, code);
+                    __stcg(W.it_code + pos, code);
                 }
-                count_outcome(W.n_valid, W.n_invalid, region, valid, active);
+                count_outcome(W.n_valid, W.n_invalid, region, valid, active, W.touched_bits);
             }
             // work counters: one atomic per warp
 #pragma unroll
@@ -460,7 +497,18 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
         for (int c = T.rank; c < n_ich; c += T.ctas) {
             const int base = c * kChunk + tid * 4;
             uint32_t code[4];
-            if (base + 3 < items) {
+            if (sorted) {           // results live at the sorted position of each item: one 4-byte gather per item
+                int ps[4] = {0, 0, 0, 0};
+                if (base + 3 < items) {
+                    const int4 p4 = __ldcg((const int4*)(W.pos_of + base));
+                    ps[0] = p4.x; ps[1] = p4.y; ps[2] = p4.z; ps[3] = p4.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) if (base + j < items) ps[j] = __ldcg(W.pos_of + base + j);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) code[j] = base + j < items ? __ldcg(W.it_code + ps[j]) : kItemInvalid;
+            } else if (base + 3 < items) {
                 const uint4 v = __ldcg((const uint4*)(W.it_code + base));
                 code[0] = v.x; code[1] = v.y; code[2] = v.z; code[3] = v.w;
             } else {
@@ -469,6 +517,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
             }
             bool keep[4];
             int cnt = 0;
+            int win_pair[4], nwin = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 keep[j] = false;
@@ -477,7 +526,11 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                     const uint32_t pair = code[j] & ~kItemGoalBit;
                     const int region = (int)(pair / (uint32_t)SUBS);
                     const bool first = __ldcg(W.claim + pair) == (uint32_t)w;    // lowest item index wins
-                    if (first) { __stcg(W.claim + pair, kVisited); atomicAdd(W.cov + region, 1); }
+                    if (first) {
+                        __stcg(W.claim + pair, kVisited);
+                        atomicAdd(W.cov + region, 1);
+                        win_pair[nwin++] = (int)pair;                                   // logged below, per warp
+                    }
                     bool kp = first;
                     if (!kp) {
                         const int slot = __ldcg(W.it_parent + w);
@@ -488,6 +541,20 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                     if (kp) {
                         ++cnt;
                         if (code[j] & kItemGoalBit) atomicMin(&ctl->first_hit_w, w);
+                    }
+                }
+            }
+            {   // lazy-reset log of the pairs this warp just marked visited: one reservation per warp
+                const int inc = warp_incl_scan(nwin);
+                const int wtot = __shfl_sync(0xffffffffu, inc, 31);
+                if (wtot) {
+                    unsigned int wbase = 0;
+                    if ((tid & 31) == 31) wbase = atomicAdd(&ctl->n_dirty_pairs, (unsigned)wtot);
+                    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                    const unsigned int mine = wbase + (unsigned)(inc - nwin);
+                    for (int q = 0; q < nwin; ++q) {
+                        if (mine + q < (unsigned)A.dirty_pairs_cap) W.dirty_pairs[mine + q] = win_pair[q];
+                        else ctl->dirty_ok = 0;
                     }
                 }
             }
@@ -528,36 +595,52 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                 const int rank = cpre + r4[j];
                 if (rank >= n_app) continue;
                 const int w = base + j, slot = size + rank;
+                const int ipos = sorted ? __ldcg(W.pos_of + w) : w;
                 const int par_slot = __ldcg(W.it_parent + w);
-                const uint32_t pair = __ldcg(W.it_code + w) & ~kItemGoalBit;
+                const uint32_t pair = __ldcg(W.it_code + ipos) & ~kItemGoalBit;
                 const int region = (int)(pair / (uint32_t)SUBS);
                 R u[NU], dt; int S;
                 sample_control<M, R>(P, h0, par_slot, w % lam, u, &dt, &S, nullptr, nullptr);
 #pragma unroll
-                for (int d = 0; d < N; ++d) states[(size_t)d * ld + slot] = __ldcg(it_end + (size_t)d * ld + w);
+                for (int d = 0; d < N; ++d) states[(size_t)d * ld + slot] = __ldcg(it_end + (size_t)d * ld + ipos);
 #pragma unroll
                 for (int q = 0; q < NU; ++q) control[(size_t)q * ld + slot] = u[q];
                 dts[slot] = dt;
                 W.parent[slot] = par_slot; W.region[slot] = region; W.tag[slot] = KPX_TAG_EXPAND;
-                if (__ldcg(W.avail_it + region) == 0) __stcg(W.avail_it + region, it + 1);  // planner.py:246
+                if (__ldcg(W.avail_it + region) == 0) {                                      // planner.py:246
+                    __stcg(W.avail_it + region, it + 1);
+                    atomicOr(W.avail_bits + (region >> 5), 1u << (region & 31));
+                }
             }
         }
         {   // estimate sweep 1 (decomposition.py:175-187) over regions available before this append
             double part = 0.0;
-            for (long long r = ttid; r < RG; r += tthreads) {
-                const int a = __ldcg(W.avail_it + r);
-                if (a != 0 && a <= it) {
-                    const double nv = (double)__ldcg(W.n_valid + r), ni = (double)__ldcg(W.n_invalid + r);
-                    // rn intrinsics: never contracted to FMA, so both precision builds agree bit for bit
-                    const double dn = __dadd_rn(P.delta, nv);
-                    const double fv = __ddiv_rn(__dmul_rn(dn, P.vol), __dadd_rn(dn, ni));
-                    const double tt = __dadd_rn(nv, ni);
-                    const double f2 = __dmul_rn(fv, fv);
-                    const double sc = __ddiv_rn(__dmul_rn(f2, f2),
-                                                __dmul_rn(__dadd_rn(1.0, (double)__ldcg(W.cov + r)),
-                                                          __dadd_rn(1.0, __dmul_rn(tt, tt))));
-                    __stcg(W.score + r, sc);
-                    part += sc;
+            // walk the availability bitmap: word order then bit order, so each thread's partial sum has a fixed
+            // order (deterministic total) while only available regions are ever touched
+            // Few regions per thread: plain dense sweep (most parallel).  Many: walk the availability bitmap in
+            // word order then bit order, touching only available regions.  Either way every thread's partial sum
+            // has a fixed order, so the total is deterministic for a given team size.
+            const bool dense = (long long)RG <= 32 * tthreads;
+            const long long n_outer = dense ? (long long)RG : (long long)((RG + 31) >> 5);
+            for (long long wi = ttid; wi < n_outer; wi += tthreads) {
+                uint32_t bits = dense ? 1u : __ldcg(W.avail_bits + wi);
+                while (bits) {
+                    const int r = dense ? (int)wi : (int)wi * 32 + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const int a = __ldcg(W.avail_it + r);
+                    if (a != 0 && a <= it) {
+                        const double nv = (double)__ldcg(W.n_valid + r), ni = (double)__ldcg(W.n_invalid + r);
+                        // rn intrinsics: never contracted to FMA, so both precision builds agree bit for bit
+                        const double dn = __dadd_rn(P.delta, nv);
+                        const double fv = __ddiv_rn(__dmul_rn(dn, P.vol), __dadd_rn(dn, ni));
+                        const double tt = __dadd_rn(nv, ni);
+                        const double f2 = __dmul_rn(fv, fv);
+                        const double sc = __ddiv_rn(__dmul_rn(f2, f2),
+                                                    __dmul_rn(__dadd_rn(1.0, (double)__ldcg(W.cov + r)),
+                                                              __dadd_rn(1.0, __dmul_rn(tt, tt))));
+                        __stcg(W.score + r, sc);
+                        part += sc;
+                    }
                 }
             }
             part = block_sum_f64(part, s_d);
@@ -686,7 +769,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
                 ctl->n_trace = nt + 1;
             }
             ctl->cnt_open[par] = 0; ctl->cnt_valid[par] = 0;
-            ctl->n_items_last = items; ctl->n_keep_last = k_keep; ctl->lam_last = lam;
+            ctl->n_items_last = items; ctl->n_keep_last = k_keep; ctl->lam_last = lam; ctl->last_sorted = sorted ? 1 : 0;
         }
         size = new_size;
         total_prev = total;
