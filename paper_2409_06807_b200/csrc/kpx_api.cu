@@ -54,29 +54,29 @@ int check_problem(const kpx_problem* pr) {
     return KPX_OK;
 }
 
-// obstacles -> device SoA [minx|miny|minz|maxx|maxy|maxz] in the launch precision
+// obstacles -> device boxes [n_obs][8] = {min xyz, -, max xyz, -} in the launch precision
 int upload_obstacles(const kpx_problem& pr, int precision, int n_obs, const double* omin, const double* omax, void* dev,
                      uint32_t* occ_dev, cudaStream_t st) {
     if (n_obs == 0) return KPX_OK;
     {
-        std::vector<uint32_t> masks((size_t)kOccGrid * kOccGrid * kOccGrid);
+        std::vector<uint32_t> masks(2 * (size_t)kOccCells);      // exact table | dilated table
         if (precision == KPX_F64) occupancy_masks_f64(pr, n_obs, omin, omax, masks.data());
         else occupancy_masks_f32(pr, n_obs, omin, omax, masks.data());
         CU(cudaMemcpyAsync(occ_dev, masks.data(), masks.size() * 4, cudaMemcpyHostToDevice, st));
         CU(cudaStreamSynchronize(st));
     }
     if (precision == KPX_F64) {
-        std::vector<double> h(6 * (size_t)n_obs);
+        std::vector<double> h(8 * (size_t)n_obs, 0.0);
         for (int k = 0; k < n_obs; ++k)
-            for (int a = 0; a < 3; ++a) { h[a * n_obs + k] = omin[3 * k + a]; h[(3 + a) * n_obs + k] = omax[3 * k + a]; }
+            for (int a = 0; a < 3; ++a) { h[8 * k + a] = omin[3 * k + a]; h[8 * k + 4 + a] = omax[3 * k + a]; }
         CU(cudaMemcpyAsync(dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
         CU(cudaStreamSynchronize(st));
     } else {
-        std::vector<float> h(6 * (size_t)n_obs);
+        std::vector<float> h(8 * (size_t)n_obs, 0.0f);
         for (int k = 0; k < n_obs; ++k)
             for (int a = 0; a < 3; ++a) {
-                h[a * n_obs + k] = (float)omin[3 * k + a];
-                h[(3 + a) * n_obs + k] = (float)omax[3 * k + a];
+                h[8 * k + a] = (float)omin[3 * k + a];
+                h[8 * k + 4 + a] = (float)omax[3 * k + a];
             }
         CU(cudaMemcpyAsync(dev, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
         CU(cudaStreamSynchronize(st));
@@ -162,8 +162,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     for (int d = 0; d < prob->grid_n; ++d) regions *= prob->grid_cells[d];
     b.regions = (int)regions;
     b.subs = prob->subcells * prob->subcells * prob->subcells;
-    b.smem = align_up((size_t)(b.max_chunks + 1) * sizeof(int), 16) + align_up(6 * (size_t)std::max(prob->n_obs, 1) * b.rs, 8) +
-             4 * (size_t)kOccGrid * kOccGrid * kOccGrid;
+    b.smem = scene_smem_bytes(prob->n_obs, b.rs) + align_up((size_t)(b.max_chunks + 1) * sizeof(int), 16);
     if (b.smem > 200 * 1024) return fail(KPX_E_LIMIT, "t_e / obstacle count need more shared memory than one SM has");
 
     cudaDeviceProp dp;
@@ -238,8 +237,8 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     }
     CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
     CU(cudaMemcpy(b.ws_dev, b.ws_host.data(), sizeof(Workspace) * (size_t)n_teams, cudaMemcpyHostToDevice));
-    CU(cudaMalloc(&b.obs_dev, 6 * (size_t)std::max(prob->n_obs, 1) * b.rs));
-    CU(cudaMalloc(&b.occ_dev, 4 * (size_t)kOccGrid * kOccGrid * kOccGrid));
+    CU(cudaMalloc(&b.obs_dev, 8 * (size_t)std::max(prob->n_obs, 1) * b.rs));
+    CU(cudaMalloc(&b.occ_dev, 2 * sizeof(uint32_t) * (size_t)kOccCells));
     rc = upload_obstacles(b.prob, precision, prob->n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
     if (rc) return rc;
     CU(cudaMalloc(&b.queue_dev, 256));
@@ -411,8 +410,8 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
     char* slab = nullptr;
     Carver c;
     const size_t o_states = c.take(8 * (size_t)state_rows * n), o_slots = c.take(8 * (size_t)m),
-                 o_obs = c.take(6 * (size_t)std::max(prob->n_obs, 1) * rs),
-                 o_occ = c.take(4 * (size_t)kOccGrid * kOccGrid * kOccGrid), o_v = c.take((size_t)items),
+                 o_obs = c.take(8 * (size_t)std::max(prob->n_obs, 1) * rs),
+                 o_occ = c.take(2 * sizeof(uint32_t) * (size_t)kOccCells), o_v = c.take((size_t)items),
                  o_r = c.take(8 * (size_t)items), o_s = c.take(8 * (size_t)items), o_e = c.take(8 * (size_t)items * n),
                  o_c = c.take(8 * (size_t)items * nu), o_d = c.take(8 * (size_t)items), o_a = c.take(8 * (size_t)items),
                  o_ss = c.take(8 * (size_t)items), o_pp = c.take(8 * (size_t)items);
@@ -430,7 +429,7 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
     L.o_dt = (double*)(slab + o_d); L.o_accept = (double*)(slab + o_a);
     L.o_substeps = (long long*)(slab + o_ss); L.o_points = (long long*)(slab + o_pp);
     L.grid = (int)std::min<int64_t>((items + kBlock - 1) / kBlock, 148 * 16);
-    L.smem = align_up(6 * (size_t)std::max(prob->n_obs, 1) * rs, 8) + 4 * (size_t)kOccGrid * kOccGrid * kOccGrid;
+    L.smem = scene_smem_bytes(prob->n_obs, rs);
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
     CU(cudaEventRecord(e0, st));

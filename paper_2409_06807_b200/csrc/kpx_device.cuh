@@ -10,6 +10,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cmath>
+#include <limits>
 #include <type_traits>
 
 #include "../../include/kpx.h"
@@ -18,7 +20,23 @@ namespace kpx {
 
 constexpr int kBlock = 256;          // threads per CTA of every kernel here
 constexpr int kChunk = 4 * kBlock;   // slots / items per ordered-compaction chunk
-constexpr int kOccGrid = 16;         // occupancy-mask grid resolution per axis (16 KB of shared memory)
+constexpr int kOccGrid = 16;         // occupancy-mask grid resolution per axis (16 KB of shared memory per table)
+constexpr int kOccCells = kOccGrid * kOccGrid * kOccGrid;
+constexpr int kWarps = kBlock / 32;
+constexpr int kCoopSteps = 8;        // segments densified into more points than this take the in-lane walk
+// inlining policy of the propagation path (tuning knobs)
+#ifndef KPX_WALK_ATTR
+#define KPX_WALK_ATTR __forceinline__
+#endif
+#ifndef KPX_COOP_ATTR
+#define KPX_COOP_ATTR __forceinline__
+#endif
+#ifndef KPX_INT_ATTR
+#define KPX_INT_ATTR __forceinline__
+#endif
+#ifndef KPX_FLUSH_AT
+#define KPX_FLUSH_AT 12              // deferred segment walks per warp that trigger a cooperative pass
+#endif
 constexpr uint32_t kUnclaimed = 0xFFFFFFFFu;
 constexpr uint32_t kVisited = 0xFFFFFFFEu;
 constexpr uint32_t kItemInvalid = 0xFFFFFFFFu;
@@ -65,7 +83,20 @@ struct Params {
     // occupancy-mask grid over the position box (0 = disabled -> every obstacle is tested)
     int occ_g;
     R occ_lo[3], occ_inv[3];
+    // d2_thr[k] = largest d2 with sqrt(d2) <= check_res * 2^k: the densification count of a segment
+    // (validity.py:26-31) follows from its squared length by compares alone, bit for bit
+    R d2_thr[4];
 };
+
+// largest x with fl(sqrt(x)) <= thr (sqrt is correctly rounded and monotone on host and device alike)
+template <class R>
+inline R sqrt_threshold(R thr) {
+    R x = thr * thr;
+    const R inf = std::numeric_limits<R>::infinity();
+    while (std::sqrt(x) > thr) x = std::nextafter(x, (R)0);
+    while (std::sqrt(std::nextafter(x, inf)) <= thr) x = std::nextafter(x, inf);
+    return x;
+}
 
 template <class R>
 inline void fill_params(Params<R>& P, const kpx_problem& pr) {
@@ -94,6 +125,8 @@ inline void fill_params(Params<R>& P, const kpx_problem& pr) {
         P.occ_lo[a] = (R)pr.state_lo[a];
         P.occ_inv[a] = (R)((double)kOccGrid / (pr.state_hi[a] - pr.state_lo[a]));
     }
+    R thr = P.check_res;
+    for (int k = 0; k < 4; ++k) { P.d2_thr[k] = thr > (R)0 ? sqrt_threshold<R>(thr) : (R)0; thr += thr; }
 }
 
 // Cell of a coordinate along one axis.  Both operations round monotonically, so p in [omin, omax] implies
@@ -105,12 +138,14 @@ __host__ __device__ __forceinline__ int occ_cell(R p, R lo, R inv) {
     return c < 0 ? 0 : (c > kOccGrid - 1 ? kOccGrid - 1 : c);
 }
 
-// Host: cell -> bitmask of the obstacles whose closed box (as rounded to R) can contain a point of that cell.
+// Host: cell -> bitmask of the obstacles whose closed box (as rounded to R) can contain a point of that cell,
+// followed by the dilated table: cell c -> OR of the masks of the 2x2x2 block of cells starting at c (what a
+// segment whose end points lie in adjacent cells can touch).
 template <class R>
 inline void build_occupancy_masks(const Params<R>& P, int n_obs, const double* omin, const double* omax,
-                                  uint32_t* masks /* kOccGrid^3 */) {
+                                  uint32_t* masks /* 2 * kOccGrid^3 */) {
     const int G = kOccGrid;
-    for (int i = 0; i < G * G * G; ++i) masks[i] = 0u;
+    for (int i = 0; i < 2 * G * G * G; ++i) masks[i] = 0u;
     for (int k = 0; k < n_obs && k < 32; ++k) {
         int lo[3], hi[3];
         for (int a = 0; a < 3; ++a) {
@@ -121,6 +156,17 @@ inline void build_occupancy_masks(const Params<R>& P, int n_obs, const double* o
             for (int y = lo[1]; y <= hi[1]; ++y)
                 for (int z = lo[2]; z <= hi[2]; ++z) masks[(x * G + y) * G + z] |= 1u << k;
     }
+    uint32_t* dil = masks + G * G * G;
+    for (int x = 0; x < G; ++x)
+        for (int y = 0; y < G; ++y)
+            for (int z = 0; z < G; ++z) {
+                uint32_t m = 0u;
+                for (int c = 0; c < 8; ++c) {
+                    const int xx = x + (c & 1), yy = y + ((c >> 1) & 1), zz = z + (c >> 2);
+                    if (xx < G && yy < G && zz < G) m |= masks[(xx * G + yy) * G + zz];
+                }
+                dil[(x * G + y) * G + z] = m;
+            }
 }
 
 // ----------------------------------------------------------------- models ----
@@ -282,57 +328,190 @@ __device__ __forceinline__ void rk4_step(R* cur, R* comp, const R* u, R h, R hal
     M::template wrap<R>(cur);
 }
 
-// Stacked double integrators: the blocks do not couple, so stepping them one 6-D block
-// at a time performs exactly the same operations per dimension while keeping only a
-// 6-D set of RK4 temporaries live (N = 48 would otherwise need ~200 registers).
-template <int B, class R>
-__device__ __forceinline__ void rk4_step_blocks(R* cur, R* comp, const R* u, R h, R half_h, R h6) {
+// float32 double integrator: x' = (v, u) has a nilpotent system matrix, so the four RK4 stages collapse
+// algebraically to  p += h (v + h/2 u),  v += h u  -- the same polynomial RK4 evaluates, in 9 instead of ~45
+// operations per block and with no stage vectors live.  (float64 keeps the staged form: it is pinned bit for
+// bit to the reference's rounding order.)
+__device__ __forceinline__ void di_step_f32(float* cur, float* comp, const float* u, float h, float half_h) {
 #pragma unroll
-    for (int b = 0; b < B; ++b) rk4_step<ModelDI6, R>(cur + 6 * b, comp + 6 * b, u + 3 * b, h, half_h, h6);
+    for (int i = 0; i < 3; ++i) {
+        const float yp = __fmaf_rn(h, __fmaf_rn(half_h, u[i], cur[3 + i]), -comp[i]);
+        const float tp = __fadd_rn(cur[i], yp);
+        comp[i] = __fsub_rn(__fsub_rn(tp, cur[i]), yp);
+        cur[i] = tp;
+        const float yv = __fmaf_rn(h, u[i], -comp[3 + i]);
+        const float tv = __fadd_rn(cur[3 + i], yv);
+        comp[3 + i] = __fsub_rn(__fsub_rn(tv, cur[3 + i]), yv);
+        cur[3 + i] = tv;
+    }
 }
+
+// float32 derives its step constants from h inside the step (h/2 is exact, h/6 is taken as h * (1/6), one
+// rounding away from the quotient) so that only h stays live in the loop; float64 is handed the reference's
+// own h/6 (_kernel.pyx:196-201).
 template <class M, class R>
 struct Stepper {
-    __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R half_h, R h6) {
-        rk4_step<M, R>(cur, comp, u, h, half_h, h6);
+    __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R h6) {
+        if constexpr (std::is_same<R, float>::value) rk4_step<M, R>(cur, comp, u, h, 0.5f * h, h * 0.16666667f);
+        else rk4_step<M, R>(cur, comp, u, h, (R)0.5 * h, h6);
     }
 };
+template <>
+struct Stepper<ModelDI6, float> {
+    __device__ static __forceinline__ void step(float* cur, float* comp, const float* u, float h, float) {
+        di_step_f32(cur, comp, u, h, 0.5f * h);
+    }
+};
+// Stacked double integrators: the blocks do not couple, so stepping them one 6-D block at a time performs
+// exactly the same operations per dimension while keeping only a 6-D set of RK4 temporaries live
+// (N = 48 would otherwise need ~200 registers).
 template <int B, class R>
 struct Stepper<ModelStackedDI<B>, R> {
-    __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R half_h, R h6) {
-        rk4_step_blocks<B, R>(cur, comp, u, h, half_h, h6);
+    __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R h6) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) Stepper<ModelDI6, R>::step(cur + 6 * b, comp + 6 * b, u + 3 * b, h, h6);
     }
 };
 
-// closed-box point test against obstacles staged in shared memory as SoA
-// [minx | miny | minz | maxx | maxy | maxz], each n_obs long (all lanes read the
-// same k -> broadcast).  _kernel.pyx:142-154.
+// ------------------------------------------------------- collision scene ----
+// The scene lives at the START of the dynamic shared memory, at compile-time offsets, so that no kernel keeps
+// a pointer register for it:
+//     [occ: kOccCells u32][occ2: kOccCells u32][coop: kWarps x WarpCoop<R>][boxes: n_obs x 8 R][caller's area]
+extern __shared__ __align__(16) unsigned char kpx_dyn_smem[];
+
+// Per-warp staging of deferred segment walks (see integrate_and_map).
 template <class R>
-__device__ __forceinline__ bool point_hits(R px, R py, R pz, const R* __restrict__ s_obs, int n_obs) {
+struct WarpCoop {
+    R seg[10][32];                       // prev xyz | d xyz | cur xyz | 1/steps, [field][lane]
+    int steps[32];
+    int hit[32];                         // lowest point index of the segment that hits an obstacle
+    int mark_pts[32];                    // the lane's point counter before the staged segment
+    int mark_sub[32];                    // substep index of the staged segment
+    uint16_t list[32 * kCoopSteps];      // (lane | point << 5) of every point to test
+};
+
+template <class R>
+struct Scene {
+    static constexpr size_t kOcc = 0, kOcc2 = sizeof(uint32_t) * kOccCells, kCoop = 2 * sizeof(uint32_t) * kOccCells;
+    static constexpr size_t kBoxes = kCoop + (size_t)kWarps * sizeof(WarpCoop<R>);
+    __device__ static __forceinline__ uint32_t* occ() { return (uint32_t*)(kpx_dyn_smem + kOcc); }
+    __device__ static __forceinline__ uint32_t* occ2() { return (uint32_t*)(kpx_dyn_smem + kOcc2); }
+    __device__ static __forceinline__ WarpCoop<R>& coop() { return ((WarpCoop<R>*)(kpx_dyn_smem + kCoop))[threadIdx.x >> 5]; }
+    // obstacle k: 8 values {min x, min y, min z, -, max x, max y, max z, -}
+    __device__ static __forceinline__ R* boxes() { return (R*)(kpx_dyn_smem + kBoxes); }
+    __host__ __device__ static size_t bytes(int n_obs) {
+        return kBoxes + (((size_t)(n_obs > 0 ? n_obs : 1) * 8 * sizeof(R) + 15) & ~(size_t)15);
+    }
+    // fill from global memory (boxes in the same 8-value layout); ends with __syncthreads()
+    __device__ static __forceinline__ void stage(const Params<R>& P, const R* __restrict__ boxes_g,
+                                                 const uint32_t* __restrict__ occ_g) {
+        R* bx = boxes();
+        for (int i = threadIdx.x; i < 8 * P.n_obs; i += kBlock) bx[i] = boxes_g[i];
+        if (P.occ_g) { uint32_t* o = occ(); for (int i = threadIdx.x; i < 2 * kOccCells; i += kBlock) o[i] = occ_g[i]; }
+        __syncthreads();
+    }
+};
+// bytes of dynamic shared memory the scene needs for element size rs (4 or 8)
+inline size_t scene_smem_bytes(int n_obs, size_t rs) {
+    return rs == 8 ? Scene<double>::bytes(n_obs) : Scene<float>::bytes(n_obs);
+}
+
+template <class R> struct Box { R lx, ly, lz, hx, hy, hz; };
+__device__ __forceinline__ Box<float> load_box(const float* b, int k) {
+    const float4 lo = ((const float4*)b)[2 * k], hi = ((const float4*)b)[2 * k + 1];
+    return Box<float>{lo.x, lo.y, lo.z, hi.x, hi.y, hi.z};
+}
+__device__ __forceinline__ Box<double> load_box(const double* b, int k) {
+    const double2 a = ((const double2*)b)[4 * k], c = ((const double2*)b)[4 * k + 1], d = ((const double2*)b)[4 * k + 2],
+                  e = ((const double2*)b)[4 * k + 3];
+    return Box<double>{a.x, a.y, c.x, d.x, d.y, e.x};
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { int t = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v += t; }
+    return v;
+}
+
+// closed-box point test (_kernel.pyx:142-154): against every obstacle, or -- through the occupancy grid --
+// only against the obstacles flagged for the point's cell.  Same verdict either way.
+template <class R>
+__device__ __forceinline__ bool point_hits(const Params<R>& P, R px, R py, R pz) {
+    const R* bx = Scene<R>::boxes();
     bool h = false;
-    for (int k = 0; k < n_obs; ++k) {
-        bool in = px >= s_obs[k] && px <= s_obs[3 * n_obs + k] && py >= s_obs[n_obs + k] &&
-                  py <= s_obs[4 * n_obs + k] && pz >= s_obs[2 * n_obs + k] && pz <= s_obs[5 * n_obs + k];
-        h = h || in;
+    if (P.occ_g == 0) {
+        for (int k = 0; k < P.n_obs; ++k) {
+            const Box<R> b = load_box(bx, k);
+            h = h || (px >= b.lx && px <= b.hx && py >= b.ly && py <= b.hy && pz >= b.lz && pz <= b.hz);
+        }
+        return h;
+    }
+    const int ix = occ_cell<R>(px, P.occ_lo[0], P.occ_inv[0]);
+    const int iy = occ_cell<R>(py, P.occ_lo[1], P.occ_inv[1]);
+    const int iz = occ_cell<R>(pz, P.occ_lo[2], P.occ_inv[2]);
+    uint32_t m = Scene<R>::occ()[(ix * kOccGrid + iy) * kOccGrid + iz];
+    while (m) {
+        const Box<R> b = load_box(bx, __ffs(m) - 1);
+        m &= m - 1;
+        h = h || (px >= b.lx && px <= b.hx && py >= b.ly && py <= b.hy && pz >= b.lz && pz <= b.hz);
     }
     return h;
 }
 
-// Same verdict through the occupancy grid: look up the point's cell, test only the flagged obstacles.
+// In-lane walk of one segment exactly as the reference orders it (_kernel.pyx:238-253): interior points
+// prev + (j/steps) d for j = 1..steps-1, then the end point itself.  Returns the number of points tested up
+// to and including the first hit, negated if there was a hit.  Out of line: only segments longer than
+// kCoopSteps * check_res and scenes without an occupancy grid come here.
 template <class R>
-__device__ __forceinline__ bool point_hits_grid(const Params<R>& P, R px, R py, R pz, const R* __restrict__ s_obs,
-                                                const uint32_t* __restrict__ s_occ, int n_obs) {
-    if (P.occ_g == 0) return point_hits<R>(px, py, pz, s_obs, n_obs);
-    const int ix = occ_cell<R>(px, P.occ_lo[0], P.occ_inv[0]);
-    const int iy = occ_cell<R>(py, P.occ_lo[1], P.occ_inv[1]);
-    const int iz = occ_cell<R>(pz, P.occ_lo[2], P.occ_inv[2]);
-    uint32_t m = s_occ[(ix * kOccGrid + iy) * kOccGrid + iz];
-    bool h = false;
-    while (m) {
-        const int k = __ffs(m) - 1;
-        m &= m - 1;
-        h = h || (px >= s_obs[k] && px <= s_obs[3 * n_obs + k] && py >= s_obs[n_obs + k] && py <= s_obs[4 * n_obs + k] &&
-                  pz >= s_obs[2 * n_obs + k] && pz <= s_obs[5 * n_obs + k]);
+__device__ KPX_WALK_ATTR int walk_segment(const Params<R>* Pp, R p0, R p1, R p2, R dx, R dy, R dz, R c0, R c1, R c2, R d2) {
+    const Params<R>& P = *Pp;
+    const R dist = MathK<R>::sq(d2);
+    // smallest power of two with steps * res >= dist (validity.py:26-31).  res * 2^k and 2^-k are exact, so
+    // doubling the threshold / halving the fraction reproduces steps * res and j / steps bit for bit.
+    int steps = 1;
+    R thr = P.check_res, inv_steps = (R)1;
+    while (thr < dist) { thr += thr; inv_steps *= (R)0.5; steps <<= 1; }
+    R t = (R)0;
+    for (int j = 1; j < steps; ++j) {
+        t += inv_steps;
+        if (point_hits<R>(P, p0 + t * dx, p1 + t * dy, p2 + t * dz)) return -j;
     }
+    return point_hits<R>(P, c0, c1, c2) ? -steps : steps;
+}
+
+// Cooperative pass over the warp's deferred segments: every (segment, point) pair becomes one unit of work
+// spread over all 32 lanes.  A segment's outcome is the lowest point index that hits (the reference stops at
+// it); returns that index for the calling lane's own segment, or 0x7fffffff if it is free (or the lane holds
+// none).  Must be called by all 32 lanes.
+template <class R>
+__device__ KPX_COOP_ATTR int coop_walk(const Params<R>* Pp, bool pend) {
+    const Params<R>& P = *Pp;
+    WarpCoop<R>& C = Scene<R>::coop();
+    const int lane = threadIdx.x & 31;
+    const int cnt = pend ? C.steps[lane] : 0;
+    const int incl = warp_incl_scan(cnt);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (pend) {
+        C.hit[lane] = 0x7fffffff;
+        const int base = incl - cnt;
+        for (int j = 1; j <= cnt; ++j) C.list[base + j - 1] = (uint16_t)(lane | (j << 5));
+    }
+    __syncwarp();
+    for (int q = lane; q < total; q += 32) {
+        const int e = C.list[q], J = e & 31, j = e >> 5;
+        R px, py, pz;
+        if (j == C.steps[J]) {
+            px = C.seg[6][J]; py = C.seg[7][J]; pz = C.seg[8][J];
+        } else {
+            const R t = (R)j * C.seg[9][J];          // j / steps, exact (steps is a power of two)
+            px = C.seg[0][J] + t * C.seg[3][J]; py = C.seg[1][J] + t * C.seg[4][J]; pz = C.seg[2][J] + t * C.seg[5][J];
+        }
+        if (point_hits<R>(P, px, py, pz)) atomicMin(&C.hit[J], j);
+    }
+    __syncwarp();
+    const int h = pend ? C.hit[lane] : 0x7fffffff;
+    __syncwarp();
     return h;
 }
 
@@ -348,58 +527,159 @@ struct ItemOut {
     bool valid;
 };
 
-// The extension itself.  `u` and `dt` are the sampled control / duration already
-// rounded to R; x0 is the parent state.
+// The extension itself, warp-synchronous: ALL 32 lanes of the warp call it together (`active` = this lane
+// holds an item).  `u` and `dt` are the sampled control / duration already rounded to R; x0 is the parent state.
+//
+// Per substep, in the reference's order (_kernel.pyx:226-256): finite -> state box -> obstacle walk.  The
+// verdict of an item is the AND of those tests over all substeps and the integration never depends on it, so
+// the walk -- the only expensive, ragged part -- is restructured without changing any verdict or counter:
+//   1. the number of points follows from the squared length by compares (Params::d2_thr);
+//   2. every point of the walk lies inside the segment's axis-aligned box [min(prev,cur), max(prev,cur)]
+//      (prev + t d is monotone in t under rounding and t <= 3/4 for interior points), and the cell lookup is
+//      monotone, so the points' cells lie in the cell range of (prev, cur).  One lookup -- the cell's own mask
+//      when both ends share a cell, the dilated mask of the lower cell otherwise -- yields a superset of the
+//      obstacles any point could hit; comparing the segment box with those obstacle boxes (same floats,
+//      exact compares) clears almost every segment without walking it;
+//   3. a segment that survives is staged in shared memory and the lane carries on, as if it were free;
+//      once KPX_FLUSH_AT lanes of the warp hold one (or a lane needs a second slot, or the item ends) the
+//      warp walks all staged points together (coop_walk).  A hit rewinds the lane's counters to their values
+//      at that point and clears `ok`, which is all the reference's early-out would have produced.
+// Counters: while a lane is ok its box test has run on every substep so far, so `boxsteps` is just where ok
+// flipped (box_end); `substeps` is where the lane stopped (S, cut short by a non-finite state).
 template <class M, class R>
-__device__ __forceinline__ void integrate_and_map(const Params<R>& P, const R* __restrict__ s_obs,
-                                                  const uint32_t* __restrict__ s_occ, const R* x0,
-                                                  const R* u, R dt, int substeps, ItemOut<R, M::N>& out) {
+__device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, const R* x0, const R* u, R dt,
+                                                  int substeps, ItemOut<R, M::N>& out) {
     constexpr int N = M::N;
-    R h = dt / (R)substeps, half_h = (R)0.5 * h, h6 = h / (R)6;
+    constexpr unsigned FULL = 0xffffffffu;
+    int S = active ? substeps : 0;
+    const int Smax = __reduce_max_sync(FULL, S);
+    const R h = dt / (R)(S > 0 ? S : 1);
+    const R h6 = std::is_same<R, float>::value ? (R)0 : h / (R)6;      // float32 re-derives it per step
     R cur[N];
     R comp[std::is_same<R, float>::value ? N : 1];   // Kahan carry (float32 only)
 #pragma unroll
     for (int i = 0; i < N; ++i) { cur[i] = x0[i]; if constexpr (std::is_same<R, float>::value) comp[i] = 0.0f; }
-    R prev0 = cur[0], prev1 = cur[1], prev2 = cur[2];
-    bool ok = true, alive = true;
-    int done = 0, points = 0, boxsteps = 0;
+    bool ok = active, alive = active, pend = false;
+    int points = 0, box_end = -1;
     const int n_obs = P.n_obs;
-    for (int s = 0; s < substeps; ++s) {
-        Stepper<M, R>::step(cur, comp, u, h, half_h, h6);
-        ++done;
-        bool fin = true;
+    const bool grid = P.occ_g != 0 && n_obs > 0;           // warp-uniform
+    int pcx = 0, pcy = 0, pcz = 0;
+    if (grid) {
+        pcx = occ_cell<R>(cur[0], P.occ_lo[0], P.occ_inv[0]);
+        pcy = occ_cell<R>(cur[1], P.occ_lo[1], P.occ_inv[1]);
+        pcz = occ_cell<R>(cur[2], P.occ_lo[2], P.occ_inv[2]);
+    }
+#pragma unroll 1
+    for (int s = 0; s < Smax; ++s) {
+        bool run = s < S;
+        const R q0 = cur[0], q1 = cur[1], q2 = cur[2];      // start of this substep's segment
+        if (run) {
+            Stepper<M, R>::step(cur, comp, u, h, h6);
+            bool fin = true;
 #pragma unroll
-        for (int i = 0; i < N; ++i) fin = fin && isfinite(cur[i]);
-        if (!fin) { alive = false; ok = false; break; }
-        if (ok) {
-            ++boxsteps;
+            for (int i = 0; i < N; ++i) fin = fin && isfinite(cur[i]);
+            if (!fin) {                                     // _kernel.pyx:226-232: stop integrating
+                if (ok) box_end = s;
+                alive = false; ok = false; run = false; S = s + 1;
+            }
+        }
+        bool cand = false;
+        int steps = 1;
+        R dx = (R)0, dy = (R)0, dz = (R)0;
+        if (run && ok) {
             bool inb = true;
 #pragma unroll
             for (int i = 0; i < N; ++i) inb = inb && !(cur[i] < P.state_lo[i] || cur[i] > P.state_hi[i]);
             ok = inb;
+            if (!ok) box_end = s + 1;
             if (ok && n_obs > 0) {
-                R dx = cur[0] - prev0, dy = cur[1] - prev1, dz = cur[2] - prev2;
-                R dist = MathK<R>::sq(dx * dx + dy * dy + dz * dz);
-                // smallest power of two with steps * res >= dist (validity.py:26-31).  res * 2^k and 2^-k are
-                // exact, so doubling the threshold / halving the fraction reproduces steps * res and j / steps
-                // bit for bit without integer->float conversions.
-                int steps = 1;
-                R thr = P.check_res, inv_steps = (R)1;
-                while (thr < dist) { thr += thr; inv_steps *= (R)0.5; steps <<= 1; }
-                R t = (R)0;
-                for (int j = 1; j < steps; ++j) {
-                    t += inv_steps;
-                    ++points;
-                    if (point_hits_grid<R>(P, prev0 + t * dx, prev1 + t * dy, prev2 + t * dz, s_obs, s_occ, n_obs)) { ok = false; break; }
+                dx = cur[0] - q0; dy = cur[1] - q1; dz = cur[2] - q2;
+                const R d2 = dx * dx + dy * dy + dz * dz;
+                if (!grid) {
+                    const int r = walk_segment<R>(&P, q0, q1, q2, dx, dy, dz, cur[0], cur[1], cur[2], d2);
+                    points += r < 0 ? -r : r;
+                    if (r < 0) { ok = false; box_end = s + 1; }
+                } else {
+                    const int cx = occ_cell<R>(cur[0], P.occ_lo[0], P.occ_inv[0]);
+                    const int cy = occ_cell<R>(cur[1], P.occ_lo[1], P.occ_inv[1]);
+                    const int cz = occ_cell<R>(cur[2], P.occ_lo[2], P.occ_inv[2]);
+                    const int mx = min(cx, pcx), my = min(cy, pcy), mz = min(cz, pcz);
+                    const bool same = cx == pcx && cy == pcy && cz == pcz;
+                    const bool near = (cx + pcx - 2 * mx) <= 1 && (cy + pcy - 2 * my) <= 1 && (cz + pcz - 2 * mz) <= 1;
+                    const int flat = (mx * kOccGrid + my) * kOccGrid + mz;
+                    uint32_t m = same ? Scene<R>::occ()[flat] : Scene<R>::occ2()[flat];
+                    if (!near) m = 0xffffffffu >> (32 - n_obs);                    // long jump: every obstacle
+                    pcx = cx; pcy = cy; pcz = cz;
+                    if (m) {
+                        const R lx = fmin(q0, cur[0]), hx = fmax(q0, cur[0]);
+                        const R ly = fmin(q1, cur[1]), hy = fmax(q1, cur[1]);
+                        const R lz = fmin(q2, cur[2]), hz = fmax(q2, cur[2]);
+                        const R* bx = Scene<R>::boxes();
+                        do {
+                            const Box<R> b = load_box(bx, __ffs(m) - 1);
+                            m &= m - 1;
+                            cand = hx >= b.lx && lx <= b.hx && hy >= b.ly && ly <= b.hy && hz >= b.lz && lz <= b.hz;
+                        } while (m && !cand);
+                    }
+                    if (d2 > P.d2_thr[3]) {              // more than kCoopSteps points: walk it here
+                        int r;
+                        if (cand) {
+                            r = walk_segment<R>(&P, q0, q1, q2, dx, dy, dz, cur[0], cur[1], cur[2], d2);
+                        } else {
+                            const R dist = MathK<R>::sq(d2);
+                            R thr = P.check_res;
+                            r = 1;
+                            while (thr < dist) { thr += thr; r <<= 1; }
+                        }
+                        points += r < 0 ? -r : r;
+                        if (r < 0) { ok = false; box_end = s + 1; }
+                        cand = false;
+                    } else {
+                        steps = 1 + (d2 > P.d2_thr[0] ? 1 : 0) + (d2 > P.d2_thr[1] ? 2 : 0) + (d2 > P.d2_thr[2] ? 4 : 0);
+                        points += steps;                 // a staged segment counts as free until coop_walk says otherwise
+                    }
                 }
-                if (ok) { ++points; if (point_hits_grid<R>(P, cur[0], cur[1], cur[2], s_obs, s_occ, n_obs)) ok = false; }
             }
         }
-        prev0 = cur[0]; prev1 = cur[1]; prev2 = cur[2];
+        if (grid) {
+            const unsigned cm = __ballot_sync(FULL, cand);
+            if (cm) {
+                const unsigned pm = __ballot_sync(FULL, pend);
+                WarpCoop<R>& C = Scene<R>::coop();
+                const int lane = threadIdx.x & 31;
+                if (cm & pm) {                           // a lane needs its slot again: resolve what is staged
+                    const int hit = coop_walk<R>(&P, pend);
+                    if (hit != 0x7fffffff) {
+                        ok = false; cand = false; points = C.mark_pts[lane] + hit; box_end = C.mark_sub[lane] + 1;
+                    }
+                    pend = false;
+                }
+                if (cand) {
+                    C.seg[0][lane] = q0; C.seg[1][lane] = q1; C.seg[2][lane] = q2;
+                    C.seg[3][lane] = dx; C.seg[4][lane] = dy; C.seg[5][lane] = dz;
+                    C.seg[6][lane] = cur[0]; C.seg[7][lane] = cur[1]; C.seg[8][lane] = cur[2];
+                    C.seg[9][lane] = (R)1 / (R)steps;
+                    C.steps[lane] = steps;
+                    C.mark_pts[lane] = points - steps; C.mark_sub[lane] = s;
+                    pend = true;
+                }
+                if (__popc(__ballot_sync(FULL, pend)) >= KPX_FLUSH_AT) {
+                    const int hit = coop_walk<R>(&P, pend);
+                    if (hit != 0x7fffffff) { ok = false; points = C.mark_pts[lane] + hit; box_end = C.mark_sub[lane] + 1; }
+                    pend = false;
+                }
+            }
+        }
+    }
+    if (grid && __any_sync(FULL, pend)) {
+        WarpCoop<R>& C = Scene<R>::coop();
+        const int lane = threadIdx.x & 31;
+        const int hit = coop_walk<R>(&P, pend);
+        if (hit != 0x7fffffff) { ok = false; points = C.mark_pts[lane] + hit; box_end = C.mark_sub[lane] + 1; }
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) out.end[i] = cur[i];
-    out.substeps = done; out.points = points; out.boxsteps = boxsteps;
+    out.substeps = S; out.points = points; out.boxsteps = box_end >= 0 ? box_end : S;
     out.region = -1; out.sub = 0; out.valid = false;
     if (alive) {
         int reg = 0;

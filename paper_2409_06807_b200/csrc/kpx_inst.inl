@@ -37,7 +37,10 @@ cudaError_t do_launch_batch(const BatchLaunch& L, cudaStream_t st) {
     A.lam = L.lam; A.seed = L.seed; A.iteration = L.iteration; A.o_valid = L.o_valid; A.o_region = L.o_region;
     A.o_sub = L.o_sub; A.o_end = L.o_end; A.o_control = L.o_control; A.o_dt = L.o_dt; A.o_accept = L.o_accept;
     A.o_substeps = L.o_substeps; A.o_points = L.o_points;
-    batch_kernel<M, Real><<<L.grid, kBlock, L.smem, st>>>(A);
+    auto kern = batch_kernel<M, Real>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    if (e != cudaSuccess) return e;
+    kern<<<L.grid, kBlock, L.smem, st>>>(A);
     return cudaGetLastError();
 }
 

@@ -10,7 +10,7 @@ namespace kpx {
 
 struct PlanLaunch {
     const kpx_problem* prob;
-    const void* obs_dev;            // SoA [6][n_obs] in the launch precision
+    const void* obs_dev;            // boxes [n_obs][8] in the launch precision
     const uint32_t* occ_dev;        // occupancy masks [kOccGrid^3]
     Workspace* ws_dev;
     const QueryIn* queries_dev;

@@ -35,6 +35,15 @@
 #define KPX_MINB_F32_MID 2
 #endif
 
+// Everything on the propagation path is inlined into the kernel: measured on B200, any out-of-line call on
+// it (the S1 phase, the integrator, or even the rare cooperative walk) costs 30 % of the batch throughput.
+#ifndef KPX_S1_ATTR
+#define KPX_S1_ATTR __forceinline__
+#endif
+#ifndef KPX_RQ_ATTR
+#define KPX_RQ_ATTR __forceinline__
+#endif
+
 namespace kpx {
 
 struct Ctl {                      // one per workspace, global memory
@@ -108,7 +117,7 @@ struct QueryIn { unsigned long long seed; double start[KPX_MAX_DIM]; double goal
 template <class R>
 struct PlanArgs {
     Params<R> P;
-    const R* obs;                 // device SoA [6][n_obs]
+    const R* obs;                 // device boxes [n_obs][8]: min xyz, -, max xyz, -
     const uint32_t* occ;          // device occupancy masks [kOccGrid^3]
     Workspace* ws;                // [n_teams]
     const QueryIn* queries;       // [n_queries]
@@ -157,12 +166,6 @@ __device__ __forceinline__ void team_sync(const Team& T) {
 }
 
 // ---- block-level helpers (kBlock threads) ----------------------------------
-__device__ __forceinline__ int warp_incl_scan(int v) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) { int t = __shfl_up_sync(0xffffffffu, v, o); if (lane >= o) v += t; }
-    return v;
-}
 // exclusive prefix of one value per thread; *total = block sum.  s_w: >= kBlock/32 + 1 ints.
 __device__ __forceinline__ int block_excl_scan(int v, int* s_w, int* total) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -239,10 +242,92 @@ __device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __
     }
 }
 
+// S1 of one iteration, out of line so that the propagation loop gets the whole register budget (the
+// caller's run state is saved once around the call): propagate every (EXPAND slot x extension) item, count
+// outcomes per region, claim fresh (region, sub) pairs.  Warps take 32-item units -- from a shared cursor when
+// the items were length-sorted (S0), else one static unit each.
 template <class M, class R>
-__device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
-                          kpx_query_result* res_out, long long query_index, int* s_prefix, const R* s_obs,
-                          const uint32_t* s_occ, int* s_w, double* s_d, int* s_bin) {
+__device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, int team_rank,
+                                          int items, int lam, int n_sch_old, uint64_t h0, bool sorted, int par,
+                                          const int* s_prefix) {
+    constexpr int N = M::N, NU = M::NU;
+    const Params<R>& P = A.P;
+    const int lane = threadIdx.x & 31;
+    int static_unit = (team_rank * kBlock + (int)threadIdx.x) >> 5;     // unsorted: this warp's slice of one round
+#pragma unroll 1
+    for (;;) {
+        int unit = static_unit;
+        if (sorted) {
+            if (lane == 0) unit = (int)atomicAdd(&W.ctl->unit_next, 1u);
+            unit = __shfl_sync(0xffffffffu, unit, 0);
+        } else {
+            static_unit = 0x3fffffff;                   // one round only
+        }
+        if ((long long)unit * 32 >= items) break;
+        const int pos = unit * 32 + lane;
+        const bool active = pos < items;
+        int w = 0, S = 0;
+        R u[NU], dt = (R)0, x0[N];
+        if (active) {
+            int slot;
+            if (sorted) {
+                w = __ldcg(W.order + pos);
+                slot = __ldcg(W.it_parent + w);
+            } else {
+                w = pos;
+                const int i = w / lam;
+                int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
+                while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
+                slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
+                __stcg(W.it_parent + w, slot);
+            }
+            sample_control<M, R>(P, h0, slot, w % lam, u, &dt, &S, nullptr, nullptr);
+            const R* st = (const R*)W.states + slot;
+#pragma unroll
+            for (int d = 0; d < N; ++d) x0[d] = __ldcg(st + (size_t)d * A.stride);
+        } else {
+#pragma unroll
+            for (int d = 0; d < N; ++d) x0[d] = (R)0;
+#pragma unroll
+            for (int j = 0; j < NU; ++j) u[j] = (R)0;
+        }
+        ItemOut<R, N> o;
+        integrate_and_map<M, R>(P, active, x0, u, dt, S, o);     // warp-synchronous
+        int region = -1; bool valid = false;
+        if (active) {
+            region = o.region; valid = o.valid;
+            uint32_t code = kItemInvalid;
+            if (valid) {
+                const uint32_t pair = (uint32_t)region * (uint32_t)P.subs_per_region + (uint32_t)o.sub;
+                const R d0 = o.end[0] - (R)Q.goal[0], d1 = o.end[1] - (R)Q.goal[1], d2 = o.end[2] - (R)Q.goal[2];
+                const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= (R)Q.goal[3];
+                code = pair | (hit ? kItemGoalBit : 0u);
+                R* e = (R*)W.it_end + pos;
+#pragma unroll
+                for (int d = 0; d < N; ++d) __stcg(e + (size_t)d * A.stride, o.end[d]);
+                if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
+            }
+            __stcg(W.it_code + pos, code);
+        }
+        count_outcome(W.n_valid, W.n_invalid, region, valid, active, W.touched_bits);
+        // work counters: one reduction and one fire-and-forget atomic per unit
+        const int t_sub = __reduce_add_sync(0xffffffffu, active ? o.substeps : 0);
+        const int t_pts = __reduce_add_sync(0xffffffffu, active ? o.points : 0);
+        const int t_box = __reduce_add_sync(0xffffffffu, active ? o.boxsteps : 0);
+        const int t_val = __popc(__ballot_sync(0xffffffffu, valid));
+        if (lane == 0) {
+            atomicAdd(&W.ctl->sum_substeps, (unsigned long long)t_sub);
+            atomicAdd(&W.ctl->sum_points, (unsigned long long)t_pts);
+            atomicAdd(&W.ctl->sum_boxsteps, (unsigned long long)t_box);
+            if (t_val) atomicAdd(&W.ctl->cnt_valid[par], t_val);
+        }
+    }
+}
+
+template <class M, class R>
+__device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
+                          kpx_query_result* res_out, long long query_index, int* s_prefix, int* s_w, double* s_d,
+                          int* s_bin) {
     constexpr int N = M::N, NU = M::NU;
     const Params<R>& P = A.P;
     const int tid = threadIdx.x;
@@ -420,76 +505,7 @@ __device__ void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& 
         if (keeper) tp[1] = gtimer();
 
         // ================================================================= S1
-        {
-            int my_sub = 0, my_pts = 0, my_valid = 0, my_box = 0;
-            const int lane = tid & 31;
-            int static_unit = (T.rank * kBlock + tid) >> 5;     // unsorted: unit = this warp's slice of one round
-#pragma unroll 1
-            for (;;) {
-                int unit = static_unit;
-                if (sorted) {
-                    if (lane == 0) unit = (int)atomicAdd(&ctl->unit_next, 1u);
-                    unit = __shfl_sync(0xffffffffu, unit, 0);
-                } else {
-                    static_unit = 0x3fffffff;                   // one round only
-                }
-                if ((long long)unit * 32 >= items) break;
-                const int pos = unit * 32 + lane;
-                const bool active = pos < items;
-                int region = -1; bool valid = false;
-                if (active) {
-                    int w, slot;
-                    if (sorted) {
-                        w = __ldcg(W.order + pos);
-                        slot = __ldcg(W.it_parent + w);
-                    } else {
-                        w = pos;
-                        const int i = w / lam;
-                        int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
-                        while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
-                        slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
-                        __stcg(W.it_parent + w, slot);
-                    }
-                    const int ext = w % lam;
-                    R u[NU], dt, x0[N];
-                    int S;
-                    sample_control<M, R>(P, h0, slot, ext, u, &dt, &S, nullptr, nullptr);
-#pragma unroll
-                    for (int d = 0; d < N; ++d) x0[d] = __ldcg(states + (size_t)d * ld + slot);
-                    ItemOut<R, N> o;
-                    integrate_and_map<M, R>(P, s_obs, s_occ, x0, u, dt, S, o);
-                    my_sub += o.substeps; my_pts += o.points; my_box += o.boxsteps;
-                    region = o.region; valid = o.valid;
-                    uint32_t code = kItemInvalid;
-                    if (valid) {
-                        ++my_valid;
-                        const uint32_t pair = (uint32_t)region * (uint32_t)SUBS + (uint32_t)o.sub;
-                        R d0 = o.end[0] - goal[0], d1 = o.end[1] - goal[1], d2 = o.end[2] - goal[2];
-                        const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= goal[3];
-                        code = pair | (hit ? kItemGoalBit : 0u);
-#pragma unroll
-                        for (int d = 0; d < N; ++d) __stcg(it_end + (size_t)d * ld + pos, o.end[d]);
-                        if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
-                    }
-                    __stcg(W.it_code + pos, code);
-                }
-                count_outcome(W.n_valid, W.n_invalid, region, valid, active, W.touched_bits);
-            }
-            // work counters: one atomic per warp
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                my_sub += __shfl_xor_sync(0xffffffffu, my_sub, o);
-                my_pts += __shfl_xor_sync(0xffffffffu, my_pts, o);
-                my_valid += __shfl_xor_sync(0xffffffffu, my_valid, o);
-                my_box += __shfl_xor_sync(0xffffffffu, my_box, o);
-            }
-            if (lane == 0 && (my_sub | my_pts | my_valid)) {
-                atomicAdd(&ctl->sum_substeps, (unsigned long long)my_sub);
-                atomicAdd(&ctl->sum_points, (unsigned long long)my_pts);
-                atomicAdd(&ctl->sum_boxsteps, (unsigned long long)my_box);
-                atomicAdd(&ctl->cnt_valid[par], my_valid);
-            }
-        }
+        s1_propagate<M, R>(A, W, Q, T.rank, items, lam, n_sch_old, h0, sorted, par, s_prefix);
         team_sync(T);
         if (keeper) tp[2] = gtimer();
 
@@ -838,29 +854,26 @@ template <class M, class R> struct MinBlocks { static constexpr int value = size
 
 template <class M, class R>
 __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(const __grid_constant__ PlanArgs<R> A) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    int* s_prefix = (int*)smem_raw;                                       // [max_chunks + 1]
-    R* s_obs = (R*)(smem_raw + (((size_t)(A.max_chunks + 1) * sizeof(int) + 15) & ~(size_t)15));
-    uint32_t* s_occ = (uint32_t*)(s_obs + 6 * (A.P.n_obs > 0 ? A.P.n_obs : 1) + (6 * (A.P.n_obs > 0 ? A.P.n_obs : 1)) % 2);
+    int* s_prefix = (int*)(kpx_dyn_smem + Scene<R>::bytes(A.P.n_obs));    // [max_chunks + 1], after the scene
     __shared__ int s_w[kBlock / 32 + 1];
     __shared__ double s_d[kBlock / 32];
     __shared__ int s_q;
     __shared__ int s_bin[4 * kBins];      // S0: local histogram | CTA base | local fill | global bin start
-
-    for (int i = threadIdx.x; i < 6 * A.P.n_obs; i += kBlock) s_obs[i] = A.obs[i];
-    if (A.P.occ_g) for (int i = threadIdx.x; i < kOccGrid * kOccGrid * kOccGrid; i += kBlock) s_occ[i] = A.occ[i];
-    __syncthreads();
+    Scene<R>::stage(A.P, A.obs, A.occ);
 
     Team T;
     T.ctas = A.team_ctas;
     const int team_id = blockIdx.x / A.team_ctas;
     T.rank = blockIdx.x - team_id * A.team_ctas;
     if (team_id >= A.n_teams) return;
-    const Workspace W = A.ws[team_id];
+    __shared__ Workspace s_ws;            // CTA-uniform: one copy in shared memory instead of ~60 registers per thread
+    if (threadIdx.x == 0) s_ws = A.ws[team_id];
+    __syncthreads();
+    const Workspace& W = s_ws;
     T.bar = W.bar;
 
     if (A.queue == nullptr) {       // single query bound to team 0 (plan handle: stepped / resumable)
-        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_obs, s_occ, s_w, s_d, s_bin);
+        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_w, s_d, s_bin);
         return;
     }
     for (;;) {                      // batch: teams pull queries until the queue is drained
@@ -877,7 +890,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
         const int q = s_q;
         __syncthreads();
         if (q >= A.n_queries) return;
-        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_obs, s_occ, s_w, s_d, s_bin);
+        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_w, s_d, s_bin);
         team_sync(T);
     }
 }
@@ -886,7 +899,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
 template <class R>
 struct BatchArgs {
     Params<R> P;
-    const R* obs;              // device SoA [6][n_obs]
+    const R* obs;              // device boxes [n_obs][8]
     const uint32_t* occ;       // device occupancy masks
     const double* states;      // (rows, n) f64 row-major, as the reference passes it
     const long long* e_slots;  // (m)
@@ -899,24 +912,30 @@ struct BatchArgs {
 template <class M, class R>
 __global__ void __launch_bounds__(kBlock) batch_kernel(const __grid_constant__ BatchArgs<R> A) {
     constexpr int N = M::N, NU = M::NU;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    R* s_obs = (R*)smem_raw;
-    uint32_t* s_occ = (uint32_t*)(s_obs + 6 * (A.P.n_obs > 0 ? A.P.n_obs : 1) + (6 * (A.P.n_obs > 0 ? A.P.n_obs : 1)) % 2);
-    for (int i = threadIdx.x; i < 6 * A.P.n_obs; i += kBlock) s_obs[i] = A.obs[i];
-    if (A.P.occ_g) for (int i = threadIdx.x; i < kOccGrid * kOccGrid * kOccGrid; i += kBlock) s_occ[i] = A.occ[i];
-    __syncthreads();
+    Scene<R>::stage(A.P, A.obs, A.occ);
     const uint64_t h0 = iter_hash(A.seed, A.iteration);
-    for (long long w = (long long)blockIdx.x * kBlock + threadIdx.x; w < A.items; w += (long long)gridDim.x * kBlock) {
-        const long long i = w / A.lam;
-        const int ext = (int)(w - i * A.lam);
-        const long long slot = A.e_slots[i];
-        R u[NU], dt, x0[N]; int S; double u64v[NU], dt64;
-        // the reference hashes the 64-bit slot; planner slots always fit 31 bits
-        sample_control<M, R>(A.P, h0, (int)slot, ext, u, &dt, &S, u64v, &dt64);
+    // whole warps iterate together (integrate_and_map is warp-synchronous); lanes past the end idle
+    for (long long base = (long long)blockIdx.x * kBlock; base < A.items; base += (long long)gridDim.x * kBlock) {
+        const long long w = base + threadIdx.x;
+        const bool active = w < A.items;
+        long long slot = 0; int ext = 0, S = 0;
+        R u[NU], dt = (R)0, x0[N]; double u64v[NU], dt64 = 0.0;
 #pragma unroll
-        for (int d = 0; d < N; ++d) x0[d] = (R)A.states[slot * N + d];
+        for (int d = 0; d < N; ++d) x0[d] = (R)0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) { u[j] = (R)0; u64v[j] = 0.0; }
+        if (active) {
+            const long long i = w / A.lam;
+            ext = (int)(w - i * A.lam);
+            slot = A.e_slots[i];
+            // the reference hashes the 64-bit slot; planner slots always fit 31 bits
+            sample_control<M, R>(A.P, h0, (int)slot, ext, u, &dt, &S, u64v, &dt64);
+#pragma unroll
+            for (int d = 0; d < N; ++d) x0[d] = (R)A.states[slot * N + d];
+        }
         ItemOut<R, N> o;
-        integrate_and_map<M, R>(A.P, s_obs, s_occ, x0, u, dt, S, o);
+        integrate_and_map<M, R>(A.P, active, x0, u, dt, S, o);
+        if (!active) continue;
 #pragma unroll
         for (int d = 0; d < N; ++d) A.o_end[w * N + d] = (double)o.end[d];
 #pragma unroll
