@@ -84,6 +84,16 @@ struct ResultPacket {             // everything the host needs after a run, one 
     double seg_start[kPacketSegs][KPX_MAX_DIM];
 };
 
+struct RunState {                 // CTA-uniform state of the running query, shared memory (one copy per CTA)
+    int size, it, status, solution_slot, ve, iters;
+    double total_prev;
+    unsigned long long t_start;   // keeper only
+    // header of the current iteration
+    int lam, items, n_sch_old, par, sorted;
+    unsigned long long h0;
+    unsigned long long tp[7];     // keeper only: phase boundary timestamps
+};
+
 struct Workspace {                // device pointers of one team's state
     void *states, *control, *dt;  // R[n][cap], R[nu][cap], R[cap]          (tree arena, SoA)
     int *parent, *region;         // [cap]
@@ -247,15 +257,18 @@ __device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __
 // outcomes per region, claim fresh (region, sub) pairs.  Warps take 32-item units -- from a shared cursor when
 // the items were length-sorted (S0), else one static unit each.
 template <class M, class R>
-__device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, int team_rank,
-                                          int items, int lam, int n_sch_old, uint64_t h0, bool sorted, int par,
-                                          const int* s_prefix) {
+__device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, const RunState& RS,
+                                         int team_rank, const int* s_prefix) {
     constexpr int N = M::N, NU = M::NU;
     const Params<R>& P = A.P;
     const int lane = threadIdx.x & 31;
     int static_unit = (team_rank * kBlock + (int)threadIdx.x) >> 5;     // unsorted: this warp's slice of one round
 #pragma unroll 1
     for (;;) {
+        // the iteration header is re-read from shared memory per unit: nothing of it stays in registers
+        const int items = RS.items, lam = RS.lam, n_sch_old = RS.n_sch_old, par = RS.par;
+        const bool sorted = RS.sorted != 0;
+        const uint64_t h0 = RS.h0;
         int unit = static_unit;
         if (sorted) {
             if (lane == 0) unit = (int)atomicAdd(&W.ctl->unit_next, 1u);
@@ -324,29 +337,29 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
     }
 }
 
-template <class M, class R>
-__device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
-                          kpx_query_result* res_out, long long query_index, int* s_prefix, int* s_w, double* s_d,
-                          int* s_bin) {
-    constexpr int N = M::N, NU = M::NU;
-    const Params<R>& P = A.P;
-    const int tid = threadIdx.x;
-    const int cap = (int)P.t_e;
-    const size_t ld = (size_t)A.stride;    // SoA row stride
-    const int RG = P.n_regions, SUBS = P.subs_per_region;
-    const bool keeper = (T.rank == 0 && tid == 0);
-    const long long tthreads = (long long)T.ctas * kBlock;
-    const long long ttid = (long long)T.rank * kBlock + tid;
-    R* const states = (R*)W.states; R* const control = (R*)W.control; R* const dts = (R*)W.dt;
-    R* const it_end = (R*)W.it_end;
-    Ctl* const ctl = W.ctl;
-    const uint64_t seed = Q.seed;
-    R goal[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) goal[i] = (R)Q.goal[i];
+// Thread / problem constants every phase re-derives for itself (nothing here is carried between phases).
+#define KPX_PHASE_LOCALS                                                                                     \
+    constexpr int N = M::N, NU = M::NU;                                                                      \
+    const Params<R>& P = A.P;                                                                                \
+    const int tid = threadIdx.x;                                                                             \
+    const int cap = (int)P.t_e;                                                                              \
+    const size_t ld = (size_t)A.stride; /* SoA row stride */                                                 \
+    const int RG = P.n_regions, SUBS = P.subs_per_region;                                                    \
+    const bool keeper = (T.rank == 0 && tid == 0);                                                           \
+    const long long tthreads = (long long)T.ctas * kBlock;                                                   \
+    const long long ttid = (long long)T.rank * kBlock + tid;                                                 \
+    R* const states = (R*)W.states; R* const control = (R*)W.control; R* const dts = (R*)W.dt;               \
+    R* const it_end = (R*)W.it_end;                                                                          \
+    Ctl* const ctl = W.ctl;                                                                                  \
+    (void)N; (void)NU; (void)cap; (void)ld; (void)RG; (void)SUBS; (void)keeper; (void)tthreads; (void)ttid;  \
+    (void)states; (void)control; (void)dts; (void)it_end; (void)ctl; (void)P;
 
+// ---- reset of a team's workspace for a new query ---------------------------------------------------------
+template <class M, class R>
+__device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q) {
+    KPX_PHASE_LOCALS
     // ------------------------------------------------------------------ reset
-    if (!A.resume) {
+    {
         if (keeper) ctl->t_begin = gtimer();
         const int n_words = (RG + 31) >> 5;
         if (__ldcg(&ctl->dirty_ok)) {
@@ -417,36 +430,44 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
         team_sync(T);
     }
 
-    // ------------------------------------------------ uniform run state (registers)
-    int size = __ldcg(&ctl->size), it = __ldcg(&ctl->iteration), status = __ldcg(&ctl->status);
-    int solution_slot = __ldcg(&ctl->solution_slot);
-    double total_prev = __ldcg(&ctl->total_prev);
-    unsigned long long t_start = 0;         // run clock origin; only the keeper thread uses it
-    if (keeper) {
-        t_start = __ldcg(&ctl->t_reset_done);
-        if (t_start == 0) { t_start = gtimer(); ctl->t_reset_done = t_start; ctl->t_begin = t_start; }  // loaded state
-    }
-    int iters_this_launch = 0;
-    int ve = scan_counts(W.cnt_expand, (size + kChunk - 1) / kChunk, s_prefix, s_w);
+}
 
-    while (status == KPX_RUNNING) {
-        if (A.max_iters > 0 && iters_this_launch >= A.max_iters) break;
-        { const int st = __ldcg(&ctl->stop); if (st) { status = st; break; } }
-        ++iters_this_launch;
+// ---- head of an iteration: termination tests, branching factor, S0.  Returns false when the run is over. ---
+template <class M, class R>
+__device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
+                                               RunState& RS, int* s_prefix, int* s_bin) {
+    KPX_PHASE_LOCALS
+    const int size = RS.size, ve = RS.ve, iters = RS.iters;
+    int it = RS.it, status = RS.status;
+    __syncthreads();                            // every thread holds the state before thread 0 rewrites it
+    bool go = status == KPX_RUNNING;
+    if (go && A.max_iters > 0 && iters >= A.max_iters) go = false;
+    if (go) { const int st = __ldcg(&ctl->stop); if (st) { status = st; go = false; } }
+    int lam = 1;
+    long long items_ll = 0;
+    if (go) {
         ++it;
-        const int par = it & 1;
-        int lam = (cap - size) / ve;                                   // planner.py:48
+        lam = (cap - size) / ve;                                       // planner.py:48
         lam = lam > P.lambda_max ? P.lambda_max : lam;
         lam = lam < 1 ? 1 : lam;
         if (A.lam_override > 0) lam = A.lam_override;
-        const long long items_ll = (long long)ve * lam;
-        if (items_ll > cap) { status = KPX_ERROR; break; }
-        const int items = (int)items_ll;
-        const int n_ich = (items + kChunk - 1) / kChunk;
-        const int n_sch_old = (size + kChunk - 1) / kChunk;
-        const uint64_t h0 = iter_hash(seed, (uint64_t)it);
-        unsigned long long tp[7];               // keeper: phase boundary timestamps
-        if (keeper) tp[0] = gtimer();
+        items_ll = (long long)ve * lam;
+        if (items_ll > cap) { status = KPX_ERROR; go = false; }
+    }
+    if (!go) {
+        if (tid == 0) { RS.status = status; RS.it = it; }
+        __syncthreads();
+        return false;
+    }
+    const int items = (int)items_ll;
+    const int n_sch_old = (size + kChunk - 1) / kChunk;
+    const uint64_t h0 = iter_hash(Q.seed, (uint64_t)it);
+    const bool sorted = items > tthreads;
+    if (tid == 0) {
+        RS.it = it; RS.iters = iters + 1; RS.lam = lam; RS.items = items; RS.n_sch_old = n_sch_old; RS.par = it & 1;
+        RS.sorted = sorted ? 1 : 0; RS.h0 = h0;
+    }
+    if (keeper) RS.tp[0] = gtimer();
 
         // ================================================================= S0: order items by length
         // The substep count S = max(4, ceil(dt/0.02)) of an item follows from its RNG draw alone.  A counting
@@ -454,7 +475,6 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
         // 32-item units from a shared cursor, so neither lanes nor warps idle behind one long extension.
         // Results stay indexed by the item number w, so nothing downstream sees the processing order.
         // An iteration that fits in one round (items <= team threads) gains nothing from it and skips S0.
-        const bool sorted = items > tthreads;
         if (sorted) {
             for (int b = tid; b < kBins; b += kBlock) { s_bin[b] = 0; s_bin[2 * kBins + b] = 0; }
             __syncthreads();
@@ -502,13 +522,23 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
             }
         }
         if (sorted) team_sync(T);
-        if (keeper) tp[1] = gtimer();
+        if (keeper) RS.tp[1] = gtimer();
 
-        // ================================================================= S1
-        s1_propagate<M, R>(A, W, Q, T.rank, items, lam, n_sch_old, h0, sorted, par, s_prefix);
-        team_sync(T);
-        if (keeper) tp[2] = gtimer();
+    __syncthreads();                            // the iteration header is visible to the whole CTA
+    return true;
+}
 
+// ---- S2..S4 and the epilogue of an iteration -------------------------------------------------------------
+template <class M, class R>
+__device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
+                                               RunState& RS, int* s_prefix, int* s_w, double* s_d) {
+    KPX_PHASE_LOCALS
+    const int size = RS.size, it = RS.it, lam = RS.lam, items = RS.items, par = RS.par;
+    const bool sorted = RS.sorted != 0;
+    const uint64_t h0 = RS.h0;
+    const double total_prev = RS.total_prev;
+    const int n_ich = (items + kChunk - 1) / kChunk;
+    {
         // ================================================================= S2
         for (int c = T.rank; c < n_ich; c += T.ctas) {
             const int base = c * kChunk + tid * 4;
@@ -585,7 +615,7 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
             if (tid == 0) __stcg(W.cnt_keep + c, tot);
         }
         team_sync(T);
-        if (keeper) tp[3] = gtimer();
+        if (keeper) RS.tp[3] = gtimer();
 
         // ================================================================= S3
         const int k_keep = scan_counts(W.cnt_keep, n_ich, s_prefix, s_w);
@@ -664,7 +694,7 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
         }
         const int new_size = size + n_app;
         team_sync(T);
-        if (keeper) tp[4] = gtimer();
+        if (keeper) RS.tp[4] = gtimer();
 
         // ================================================================= S4
         double total;
@@ -734,17 +764,17 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
             __stcg(&ctl->unit_next, 0u);
             for (int b = 0; b < kBins; ++b) __stcg(W.bin_cursor + b, 0u);
             atomicAdd(&ctl->sum_items, (unsigned long long)items);
-            const double el = (double)(gtimer() - t_start) * 1e-9;
+            const double el = (double)(gtimer() - RS.t_start) * 1e-9;
             int stop = 0;
             if (!(el < A.t_max_s)) stop = KPX_TIMEOUT;                               // planner.py:282
             if (A.stop_flag && *((volatile const uint32_t*)A.stop_flag)) stop = KPX_STOPPED;
             if (stop) ctl->stop = stop;
         }
         team_sync(T);
-        if (keeper) tp[5] = gtimer();
+        if (keeper) RS.tp[5] = gtimer();
 
         // ================================================= epilogue of the iteration
-        ve = scan_counts(W.cnt_expand, (new_size + kChunk - 1) / kChunk, s_prefix, s_w);
+        int ve = scan_counts(W.cnt_expand, (new_size + kChunk - 1) / kChunk, s_prefix, s_w);
         if (ve == 0) {
             // rescue rule (planner.py:259-265): OPEN slot with max p_accept, lowest slot on ties
             unsigned long long best = 0ull;
@@ -778,25 +808,35 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
                 kpx_trace tr;
                 tr.iteration = it; tr.branching = lam; tr.ve_size = items / lam; tr.vo_size = __ldcg(&ctl->cnt_open[par]);
                 tr.attempted = items; tr.valid = __ldcg(&ctl->cnt_valid[par]); tr.staged = k_keep; tr.appended = n_app;
-                tp[6] = gtimer();
-                tr.tree_size = new_size; tr.elapsed_ms = (double)(tp[6] - t_start) * 1e-6;
-                for (int ph = 0; ph < 6; ++ph) tr.phase_ms[ph] = (double)(tp[ph + 1] - tp[ph]) * 1e-6;
+                RS.tp[6] = gtimer();
+                tr.tree_size = new_size; tr.elapsed_ms = (double)(RS.tp[6] - RS.t_start) * 1e-6;
+                for (int ph = 0; ph < 6; ++ph) tr.phase_ms[ph] = (double)(RS.tp[ph + 1] - RS.tp[ph]) * 1e-6;
                 W.trace[nt] = tr;
                 ctl->n_trace = nt + 1;
             }
             ctl->cnt_open[par] = 0; ctl->cnt_valid[par] = 0;
             ctl->n_items_last = items; ctl->n_keep_last = k_keep; ctl->lam_last = lam; ctl->last_sorted = sorted ? 1 : 0;
         }
-        size = new_size;
-        total_prev = total;
-        if (found) { status = KPX_SOLVED; solution_slot = size - 1; }              // planner.py:297-303
-        else if (exhausted) status = KPX_CAPACITY_EXHAUSTED;
+        __syncthreads();                        // every thread is done with this iteration's state
+        if (tid == 0) {
+            RS.size = new_size; RS.total_prev = total; RS.ve = ve;
+            if (found) { RS.status = KPX_SOLVED; RS.solution_slot = new_size - 1; }              // planner.py:297-303
+            else if (exhausted) RS.status = KPX_CAPACITY_EXHAUSTED;
+        }
+        __syncthreads();
     }
+}
 
+// ---- results of a run: chain walk, packet, per-query record (keeper thread) -------------------------------
+template <class M, class R>
+__device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const RunState& RS,
+                                             kpx_query_result* res_out, long long query_index) {
+    KPX_PHASE_LOCALS
     // ------------------------------------------------------------------ results
     if (keeper) {
+        const int size = RS.size, it = RS.it, status = RS.status, solution_slot = RS.solution_slot;
         ctl->size = size; ctl->iteration = it; ctl->status = status; ctl->solution_slot = solution_slot;
-        ctl->total_prev = total_prev; ctl->ve = ve;
+        ctl->total_prev = RS.total_prev; ctl->ve = RS.ve;
         int len = 0;
         if (status == KPX_SOLVED) {
             // parent chain (planner.py:325-336), written root-first
@@ -848,6 +888,39 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
     }
 }
 
+// One query on one team.  The CTA-uniform run state lives in shared memory (RunState), each phase re-derives
+// its locals from it, and nothing but the propagation loop's own registers is live across S1.
+template <class M, class R>
+__device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
+                                      kpx_query_result* res_out, long long query_index, RunState& RS, int* s_prefix,
+                                      int* s_w, double* s_d, int* s_bin) {
+    if (!A.resume) reset_query<M, R>(A, W, T, Q);
+    {   // run state out of Ctl (valid between launches: stepped runs, resume)
+        Ctl* const ctl = W.ctl;
+        const int size = __ldcg(&ctl->size);
+        const int ve = scan_counts(W.cnt_expand, (size + kChunk - 1) / kChunk, s_prefix, s_w);
+        if (threadIdx.x == 0) {
+            RS.size = size; RS.it = __ldcg(&ctl->iteration); RS.status = __ldcg(&ctl->status);
+            RS.solution_slot = __ldcg(&ctl->solution_slot); RS.total_prev = __ldcg(&ctl->total_prev);
+            RS.ve = ve; RS.iters = 0;
+            unsigned long long t_start = 0;     // run clock origin; only the keeper thread uses it
+            if (T.rank == 0) {
+                t_start = __ldcg(&ctl->t_reset_done);
+                if (t_start == 0) { t_start = gtimer(); ctl->t_reset_done = t_start; ctl->t_begin = t_start; }  // loaded state
+            }
+            RS.t_start = t_start;
+        }
+        __syncthreads();
+    }
+    while (iteration_head<M, R>(A, W, T, Q, RS, s_prefix, s_bin)) {
+        s1_propagate<M, R>(A, W, Q, RS, T.rank, s_prefix);
+        team_sync(T);
+        if (T.rank == 0 && threadIdx.x == 0) RS.tp[2] = gtimer();
+        iteration_tail<M, R>(A, W, T, Q, RS, s_prefix, s_w, s_d);
+    }
+    finish_query<M, R>(A, W, T, RS, res_out, query_index);
+}
+
 // Resident CTAs per SM each instantiation is compiled for (register budget = 65536 / (kBlock * n)).
 // The propagation loop is latency-bound, so the small float32 models trade registers for warps.
 template <class M, class R> struct MinBlocks { static constexpr int value = sizeof(R) == 4 ? (M::N <= 6 ? KPX_MINB_F32_SMALL : (M::N <= 12 ? KPX_MINB_F32_MID : 1)) : (M::N <= 6 ? 2 : 1); };
@@ -866,6 +939,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
     const int team_id = blockIdx.x / A.team_ctas;
     T.rank = blockIdx.x - team_id * A.team_ctas;
     if (team_id >= A.n_teams) return;
+    __shared__ RunState s_rs;
     __shared__ Workspace s_ws;            // CTA-uniform: one copy in shared memory instead of ~60 registers per thread
     if (threadIdx.x == 0) s_ws = A.ws[team_id];
     __syncthreads();
@@ -873,7 +947,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
     T.bar = W.bar;
 
     if (A.queue == nullptr) {       // single query bound to team 0 (plan handle: stepped / resumable)
-        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_prefix, s_w, s_d, s_bin);
+        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_rs, s_prefix, s_w, s_d, s_bin);
         return;
     }
     for (;;) {                      // batch: teams pull queries until the queue is drained
@@ -890,7 +964,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(co
         const int q = s_q;
         __syncthreads();
         if (q >= A.n_queries) return;
-        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_prefix, s_w, s_d, s_bin);
+        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_rs, s_prefix, s_w, s_d, s_bin);
         team_sync(T);
     }
 }
