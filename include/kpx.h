@@ -192,6 +192,8 @@ typedef struct kpx_query_result {
     int64_t tree_size, solution_slot, chain_len;
     double device_ms;
     uint64_t items, substeps, points, boxsteps;
+    int32_t checked;     /* kpx_batch_validate: 1 = solution re-validated in float64, -1 = rejected, 0 = not checked */
+    int32_t check_code;  /* 0 ok, 3 a state or interpolant is invalid, 4 goal missed, 5 chain longer than max_chain */
 } kpx_query_result;
 
 int kpx_batch_create(const kpx_problem *prob, int32_t precision, int32_t n_teams, int32_t team_ctas,
@@ -207,6 +209,16 @@ int kpx_batch_run(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const 
 int kpx_batch_upload(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const double *starts,
                      const double *goals, int32_t want_chains, void *stream);
 int kpx_batch_launch(kpx_batch *b, double t_max, void *stream);
+/*
+ * Re-validate every solved query of the last kpx_batch_launch on the device, in float64, with the reference
+ * checker's rules (ValidityChecker.trajectory_valid, validity.py:108-125, on the trajectory that
+ * propagate_ode, dynamics.py:242-283, rebuilds from the query's start state): fills `checked` / `check_code`
+ * of the per-query records that kpx_batch_download returns.  Needs want_chains = 1 at upload.  `res` <= 0
+ * selects the problem's check_res.  Asynchronous on `stream`.  Replaces a host loop over
+ * extract_trajectory (planner.py:325-341) + trajectory_valid per query.
+ */
+int kpx_batch_validate(kpx_batch *b, double res, void *stream);
+
 int kpx_batch_download(kpx_batch *b, kpx_query_result *results, double *chain_start, double *chain_control,
                        double *chain_dt, void *stream);
 

@@ -59,13 +59,14 @@ class QueryResult(C.Structure):
         ("status", C.c_int32), ("iterations", C.c_int32), ("tree_size", C.c_int64), ("solution_slot", C.c_int64),
         ("chain_len", C.c_int64), ("device_ms", C.c_double),
         ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("boxsteps", C.c_uint64),
+        ("checked", C.c_int32), ("check_code", C.c_int32),
     ]
 
 
 QUERY_RESULT_DTYPE = np.dtype([
     ("status", np.int32), ("iterations", np.int32), ("tree_size", np.int64), ("solution_slot", np.int64),
     ("chain_len", np.int64), ("device_ms", np.float64), ("items", np.uint64), ("substeps", np.uint64),
-    ("points", np.uint64), ("boxsteps", np.uint64)], align=True)
+    ("points", np.uint64), ("boxsteps", np.uint64), ("checked", np.int32), ("check_code", np.int32)], align=True)
 
 _SIGNATURES = {
     "kpx_last_error": (C.c_char_p, []),
@@ -96,6 +97,7 @@ _SIGNATURES = {
     "kpx_batch_destroy": (None, [_vp]),
     "kpx_batch_upload": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_int32, _vp]),
     "kpx_batch_launch": (C.c_int, [_vp, C.c_double, _vp]),
+    "kpx_batch_validate": (C.c_int, [_vp, C.c_double, _vp]),
     "kpx_batch_download": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "kpx_batch_run": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, _vp,
                                 C.POINTER(C.c_double), _vp]),

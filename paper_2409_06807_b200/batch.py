@@ -61,6 +61,16 @@ class BatchResult:
     def success_rate(self) -> float:
         return float(self.solved.mean()) if len(self.records) else 0.0
 
+    @property
+    def validated(self) -> np.ndarray:
+        """Per query: the solution passed the device's float64 re-validation (reference checker rules)."""
+        return self.records["checked"] == 1
+
+    @property
+    def rejected(self) -> np.ndarray:
+        """Per query: solved by the planner but refused by the float64 re-validation."""
+        return self.records["checked"] == -1
+
 
 class BatchPlanner:
     """Persistent multi-query planner bound to one GPU."""
@@ -102,7 +112,9 @@ class BatchPlanner:
 
     def run(self, seeds: Sequence[int], starts=None, goals=None, t_max: Optional[float] = None,
             want_chains: bool = True, stream=None) -> BatchResult:
-        """Plan ``len(seeds)`` queries; ``starts`` (Q, n) / ``goals`` (Q, 4) default to the environment's."""
+        """Plan ``len(seeds)`` queries; ``starts`` (Q, n) / ``goals`` (Q, 4) default to the environment's.
+        With ``want_chains`` every solution is also re-validated on the device in float64
+        (``BatchResult.validated`` / ``rejected``)."""
         q = len(seeds)
         if q < 1:
             raise ConfigError("need at least one query")
@@ -145,6 +157,12 @@ class BatchPlanner:
         _lib.check(self._lib.kpx_batch_launch(self._handle, float(self.cfg.t_max if t_max is None else t_max), stream),
                    "kpx_batch_launch")
 
+    def validate(self, resolution: Optional[float] = None, stream=None) -> None:
+        """Re-validate every solved query of the last launch on the device in float64 (asynchronous): the
+        batched form of ``extract_trajectory`` + ``ValidityChecker.trajectory_valid`` (``planner.py:325-341``,
+        ``validity.py:108-125``).  Needs ``upload(..., want_chains=True)``; ``run`` does it by itself."""
+        _lib.check(self._lib.kpx_batch_validate(self._handle, float(resolution or 0.0), stream), "kpx_batch_validate")
+
     def download(self, stream=None) -> BatchResult:
         q, starts, goals, want = self._uploaded
         n, nu = self.model.n, self.model.control_dim
@@ -157,8 +175,10 @@ class BatchPlanner:
         return BatchResult(rec, cs, cc, cd, 0.0, 0.0, starts, goals)
 
     # -- host-side rebuild / re-validation of one solution ------------------------------------------
-    def trajectory(self, result: BatchResult, q: int) -> tuple:
-        """(segments, ok): float64 rebuild of query q's solution from its chain; ok = collision-free and in goal."""
+    def trajectory(self, result: BatchResult, q: int, resolution: Optional[float] = None) -> tuple:
+        """(segments, ok): float64 rebuild of query q's solution from its chain on the host; ok = collision-free
+        (checked at ``resolution``, default the planner's) and in goal.  ``BatchResult.validated`` holds the
+        same verdict for every query, computed on the device."""
         L = int(result.records["chain_len"][q])
         if result.status(q) is not PlanStatus.SOLVED or L <= 0 or result.chain_dt is None:
             return [], result.status(q) is PlanStatus.SOLVED and L == 0
@@ -177,7 +197,7 @@ class BatchPlanner:
         okc, code = C.c_int32(0), C.c_int32(0)
         goal = np.ascontiguousarray(result.goals[q])
         _lib.check(self._lib.kpx_trajectory_valid(C.byref(self._prob_struct), L, _lib.ptr(sampled), _lib.ptr(off),
-                                                  _lib.ptr(goal), self.problem.check_resolution, C.byref(okc),
+                                                  _lib.ptr(goal), float(resolution or self.problem.check_resolution), C.byref(okc),
                                                   C.byref(code)), "kpx_trajectory_valid")
         segs = [TrajectorySegment(control=ctrl[i].copy(), dt=float(dts[i]), end_state=sampled[off[i + 1] - 1].copy(),
                                   sampled_states=sampled[off[i]:off[i + 1]]) for i in range(L)]

@@ -104,6 +104,7 @@ struct kpx_batch {
     std::vector<Workspace> ws_host;
     Workspace* ws_dev = nullptr;
     void* obs_dev = nullptr;
+    double* boxes64_dev = nullptr;     // float64 boxes for kpx_batch_validate (whatever the tree precision)
     uint32_t* occ_dev = nullptr;
     unsigned int* queue_dev = nullptr;
     QueryIn* q_dev = nullptr;
@@ -131,7 +132,7 @@ namespace {
 
 void destroy_batch(kpx_batch& b) {
     cudaSetDevice(b.device);
-    cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.occ_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
+    cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.boxes64_dev); cudaFree(b.occ_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
     cudaFree(b.r_dev); cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt); cudaFree(b.peers_dev);
     cudaFreeHost(b.pk_host); cudaFreeHost(b.q_pinned);
 }
@@ -492,6 +493,7 @@ int kpx_plan_set_obstacles(kpx_plan* p, int32_t n_obs, const double* omin, const
     b.prob.n_obs = n_obs;
     std::copy(omin, omin + 3 * (size_t)n_obs, b.obs_min.begin());
     std::copy(omax, omax + 3 * (size_t)n_obs, b.obs_max.begin());
+    cudaFree(b.boxes64_dev); b.boxes64_dev = nullptr;      // rebuilt on the next validation
     return upload_obstacles(b.prob, b.precision, n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
 }
 
@@ -926,6 +928,30 @@ int kpx_batch_launch(kpx_batch* bp, double t_max, void* stream) {
     return launch(b, L, st);
 }
 
+int kpx_batch_validate(kpx_batch* bp, double res, void* stream) {
+    if (!bp) return fail(KPX_E_ARG, "null batch");
+    kpx_batch& b = *bp;
+    if (b.n_uploaded < 1) return fail(KPX_E_STATE, "kpx_batch_upload first");
+    if (!b.want_chains || !b.bc_ctrl || !b.bc_dt) return fail(KPX_E_STATE, "validation needs want_chains = 1 at upload");
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaSetDevice(b.device));
+    if (!b.boxes64_dev) {
+        const int k = std::max(b.prob.n_obs, 1);
+        std::vector<double> h(8 * (size_t)k, 0.0);
+        for (int j = 0; j < b.prob.n_obs; ++j)
+            for (int a = 0; a < 3; ++a) { h[8 * j + a] = b.obs_min[3 * j + a]; h[8 * j + 4 + a] = b.obs_max[3 * j + a]; }
+        CU(cudaMalloc(&b.boxes64_dev, h.size() * 8));
+        CU(cudaMemcpy(b.boxes64_dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    }
+    ValidateLaunch L{};
+    L.prob = &b.prob; L.boxes_dev = b.boxes64_dev; L.queries_dev = b.q_dev; L.results_dev = b.r_dev;
+    L.chain_control = b.bc_ctrl; L.chain_dt = b.bc_dt; L.n_queries = (int)b.n_uploaded; L.max_chain = b.max_chain;
+    L.res = res > 0.0 ? res : b.prob.check_res;
+    cudaError_t e = launch_validate_f64(L, st);
+    if (e != cudaSuccess) return fail(KPX_E_CUDA, "validate kernel launch: %s", cudaGetErrorString(e));
+    return KPX_OK;
+}
+
 int kpx_batch_download(kpx_batch* bp, kpx_query_result* results, double* chain_start, double* chain_control,
                        double* chain_dt, void* stream) {
     if (!bp || !results) return fail(KPX_E_ARG, "null argument");
@@ -957,6 +983,7 @@ int kpx_batch_run(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const
     CU(cudaEventRecord(e0, st));
     rc = kpx_batch_launch(bp, t_max, stream);
     if (rc) return rc;
+    if (want) { rc = kpx_batch_validate(bp, 0.0, stream); if (rc) return rc; }    // every solution is re-checked in float64
     CU(cudaEventRecord(e1, st));
     rc = kpx_batch_download(bp, results, chain_start, chain_control, chain_dt, stream);
     if (rc) return rc;

@@ -587,9 +587,10 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
         int steps = 1;
         R dx = (R)0, dy = (R)0, dz = (R)0;
         if (run && ok) {
+            // closed state box; the state is finite here, so !(x < lo || x > hi) == (x >= lo) & (x <= hi)
             bool inb = true;
 #pragma unroll
-            for (int i = 0; i < N; ++i) inb = inb && !(cur[i] < P.state_lo[i] || cur[i] > P.state_hi[i]);
+            for (int i = 0; i < N; ++i) inb = inb & (cur[i] >= P.state_lo[i]) & (cur[i] <= P.state_hi[i]);
             ok = inb;
             if (!ok) box_end = s + 1;
             if (ok && n_obs > 0) {
@@ -603,12 +604,17 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
                     const int cx = occ_cell<R>(cur[0], P.occ_lo[0], P.occ_inv[0]);
                     const int cy = occ_cell<R>(cur[1], P.occ_lo[1], P.occ_inv[1]);
                     const int cz = occ_cell<R>(cur[2], P.occ_lo[2], P.occ_inv[2]);
-                    const int mx = min(cx, pcx), my = min(cy, pcy), mz = min(cz, pcz);
-                    const bool same = cx == pcx && cy == pcy && cz == pcz;
-                    const bool near = (cx + pcx - 2 * mx) <= 1 && (cy + pcy - 2 * my) <= 1 && (cz + pcz - 2 * mz) <= 1;
-                    const int flat = (mx * kOccGrid + my) * kOccGrid + mz;
-                    uint32_t m = same ? Scene<R>::occ()[flat] : Scene<R>::occ2()[flat];
-                    if (!near) m = 0xffffffffu >> (32 - n_obs);                    // long jump: every obstacle
+                    // cells of the two ends: equal or one step apart along one axis (L1 distance <= 1) -> the
+                    // walk's points can only lie in those two cells; otherwise the dilated table of the lower
+                    // corner (<= 1 apart on every axis) or, for a long jump, every obstacle
+                    const int l1 = abs(cx - pcx) + abs(cy - pcy) + abs(cz - pcz);
+                    uint32_t m = Scene<R>::occ()[(cx * kOccGrid + cy) * kOccGrid + cz] |
+                                 Scene<R>::occ()[(pcx * kOccGrid + pcy) * kOccGrid + pcz];
+                    if (l1 > 1) {
+                        const int mx = min(cx, pcx), my = min(cy, pcy), mz = min(cz, pcz);
+                        const bool near = (cx + pcx - 2 * mx) <= 1 && (cy + pcy - 2 * my) <= 1 && (cz + pcz - 2 * mz) <= 1;
+                        m = near ? Scene<R>::occ2()[(mx * kOccGrid + my) * kOccGrid + mz] : 0xffffffffu >> (32 - n_obs);
+                    }
                     pcx = cx; pcy = cy; pcz = cz;
                     if (m) {
                         const R lx = fmin(q0, cur[0]), hx = fmax(q0, cur[0]);
@@ -618,7 +624,7 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
                         do {
                             const Box<R> b = load_box(bx, __ffs(m) - 1);
                             m &= m - 1;
-                            cand = hx >= b.lx && lx <= b.hx && hy >= b.ly && ly <= b.hy && hz >= b.lz && lz <= b.hz;
+                            cand = (hx >= b.lx) & (lx <= b.hx) & (hy >= b.ly) & (ly <= b.hy) & (hz >= b.lz) & (lz <= b.hz);
                         } while (m && !cand);
                     }
                     if (d2 > P.d2_thr[3]) {              // more than kCoopSteps points: walk it here
@@ -635,7 +641,9 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
                         if (r < 0) { ok = false; box_end = s + 1; }
                         cand = false;
                     } else {
-                        steps = 1 + (d2 > P.d2_thr[0] ? 1 : 0) + (d2 > P.d2_thr[1] ? 2 : 0) + (d2 > P.d2_thr[2] ? 4 : 0);
+                        if (d2 > P.d2_thr[0]) steps = 2;
+                        if (d2 > P.d2_thr[1]) steps = 4;
+                        if (d2 > P.d2_thr[2]) steps = 8;
                         points += steps;                 // a staged segment counts as free until coop_walk says otherwise
                     }
                 }

@@ -44,7 +44,18 @@ struct BatchLaunch {
     size_t smem;
 };
 
+struct ValidateLaunch {
+    const kpx_problem* prob;
+    const double* boxes_dev;        // float64 boxes [n_obs][8]
+    const QueryIn* queries_dev;
+    kpx_query_result* results_dev;
+    const double *chain_control, *chain_dt;
+    int n_queries, max_chain;
+    double res;
+};
+
 // each returns cudaErrorInvalidValue for an unsupported (model_id, n)
+cudaError_t launch_validate_f64(const ValidateLaunch& L, cudaStream_t st);
 cudaError_t launch_plan_f64(const PlanLaunch& L, cudaStream_t st);
 cudaError_t launch_plan_f32(const PlanLaunch& L, cudaStream_t st);
 cudaError_t launch_batch_f64(const BatchLaunch& L, cudaStream_t st);

@@ -882,6 +882,7 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
             kpx_query_result r;
             r.status = status; r.iterations = it; r.tree_size = size; r.solution_slot = solution_slot;
             r.chain_len = len; r.device_ms = (double)(ctl->t_end - __ldcg(&ctl->t_begin)) * 1e-6;
+            r.checked = 0; r.check_code = 0;        // filled by kpx_batch_validate
             r.items = __ldcg(&ctl->sum_items); r.substeps = __ldcg(&ctl->sum_substeps); r.points = __ldcg(&ctl->sum_points); r.boxsteps = __ldcg(&ctl->sum_boxsteps);
             *res_out = r;
         }

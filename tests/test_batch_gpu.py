@@ -62,6 +62,46 @@ def test_batch_with_per_query_goals(kp):
             assert np.linalg.norm(end - goals[i, :3]) <= goals[i, 3] + 1e-9
 
 
+@pytest.mark.parametrize("model_name,scene,backend,t_e", [("di6", "forest", "cuda-f32", 20000), ("di6", "forest", "cuda", 8000),
+                                                          ("dubins6", "building", "cuda-f32", 30000),
+                                                          ("quad12", "forest", "cuda-f32", 60000)])
+def test_device_revalidation_matches_host_checker(kp, model_name, scene, backend, t_e):
+    """kpx_batch_validate (float64, one thread per query) gives every query the verdict of the host twin of
+    the reference checker (kpx_trajectory + kpx_trajectory_valid, themselves pinned to propagate_ode and
+    ValidityChecker in test_host.py) -- at the planner's resolution, at a 25x finer one, and for a goal the
+    trajectory does not reach."""
+    model = kp.get_model(model_name)
+    env = kp.gen_environment(scene, model, seed=0)
+    cfg = small_cfg(kp, model, t_e=t_e, seed=0)
+    seeds = np.arange(24)
+    with kp.BatchPlanner(cfg, env, model, backend=backend, n_teams=12, team_ctas=1) as bp:
+        res = bp.run(seeds)
+        assert res.solved.sum() >= 12
+        for q in range(len(seeds)):
+            if res.status(q) is kp.PlanStatus.SOLVED:
+                _, ok = bp.trajectory(res, q)
+                assert (res.records["checked"][q] == 1) == ok, (q, res.records["checked"][q], res.records["check_code"][q])
+                assert res.records["checked"][q] in (1, -1)
+            else:
+                assert res.records["checked"][q] == 0
+        assert res.validated.sum() >= 0.9 * res.solved.sum()        # the planner's own resolution: (nearly) all pass
+        # resident path at a much finer resolution: verdicts still agree query by query
+        bp.upload(seeds, want_chains=True)
+        bp.launch()
+        bp.validate(resolution=0.002)
+        fine = bp.download()
+        for q in np.flatnonzero(fine.solved):
+            _, ok = bp.trajectory(fine, int(q), resolution=0.002)
+            assert (fine.records["checked"][q] == 1) == ok, q
+        # the queries are re-read at validation time: against a goal nobody was planning for, all are refused
+        far = np.tile(np.array([env.start[0], env.start[1], env.start[2], 1e-3]), (len(seeds), 1))
+        bp.upload(seeds, goals=far, want_chains=True)
+        bp.validate()
+        missed = bp.download()
+        sel = fine.solved & (fine.records["chain_len"] > 0)
+        assert np.all(missed.records["checked"][sel] == -1) and np.all(missed.records["check_code"][sel] == 4)
+
+
 def test_race_flag_stops_a_run(kp):
     """OR-parallel race plumbing on one GPU: a pre-set stop word ends the run at the first iteration
     boundary with TIMEOUT-like status; a solving run raises the peers' words."""
