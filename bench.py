@@ -29,13 +29,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (model, scene, flops per RK4 substep [SURVEY 8d], queries per GPU per step).  A step holds several
-    # queries per resident team (592 / 296 teams on a B200) so that teams keep pulling work while the slowest
-    # queries finish: with one query per team the tail of the launch idles ~17 % of the GPU.
-    "di6_forest": ("di6", "forest", 78, 4736),
-    "dubins6_building": ("dubins6", "building", 118, 2368),
-    "quad12_narrow": ("quad12", "narrow", 336, 1184),
-    "quad12_forest": ("quad12", "forest", 336, 1184),
+    # name: (model, scene, flops per RK4 substep [SURVEY 8d], queries per resident team per step).  A step holds
+    # several queries per team (592 / 444 teams of one CTA on a B200) so that teams keep pulling work while the
+    # slowest queries finish: with one query per team the tail of the launch idles ~17 % of the GPU.
+    "di6_forest": ("di6", "forest", 78, 8),
+    "dubins6_building": ("dubins6", "building", 118, 4),
+    "quad12_narrow": ("quad12", "narrow", 336, 4),
+    "quad12_forest": ("quad12", "forest", 336, 4),
 }
 
 
@@ -166,8 +166,7 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    model_name, scene, f_step, q_default = WORKLOADS[args.workload]
-    q_per_gpu = args.queries or q_default
+    model_name, scene, f_step, q_per_team = WORKLOADS[args.workload]
 
     # CPU baseline first (rank 0, N=1 only), before this process touches CUDA: bounded sample, one plan per core
     cpu = None
@@ -235,6 +234,7 @@ def run_gpu(args):
 
     # ---- throughput leg
     bp = kp.BatchPlanner(cfg, env, model, backend=args.backend, team_ctas=args.team_ctas, device=local)
+    q_per_gpu = args.queries or q_per_team * bp.n_teams
     seeds = np.arange(q_per_gpu, dtype=np.int64) + rank * q_per_gpu
     bp.upload(seeds, want_chains=True, stream=sptr)
     for _ in range(args.warmup):

@@ -94,6 +94,7 @@ _SIGNATURES = {
     "kpx_plan_load": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int32, C.c_int64] + [_vp] * 13),
     "kpx_batch_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                    C.POINTER(_vp)]),
+    "kpx_batch_info": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kpx_batch_destroy": (None, [_vp]),
     "kpx_batch_upload": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_int32, _vp]),
     "kpx_batch_launch": (C.c_int, [_vp, C.c_double, _vp]),

@@ -83,15 +83,15 @@ class BatchPlanner:
         self.precision = get_backend(backend, model).precision
         self._lib = _lib.load()
         self._prob_struct, self._keep = _lib.problem_from(self.problem)
-        if n_teams <= 0:
-            sm, f32b, f64b = C.c_int32(0), C.c_int32(0), C.c_int32(0)
-            _lib.check(self._lib.kpx_device_info(device, C.byref(sm), C.byref(f32b), C.byref(f64b)), "kpx_device_info")
-            resident = f32b.value if self.precision == _lib.F32 else f64b.value
-            n_teams = max(1, resident // max(1, team_ctas))
-        self.n_teams, self.team_ctas, self.max_chain, self.device = int(n_teams), int(team_ctas), int(max_chain), device
+        self.max_chain, self.device = int(max_chain), device
         self._handle = _lib._vp()
-        _lib.check(self._lib.kpx_batch_create(C.byref(self._prob_struct), self.precision, self.n_teams, self.team_ctas,
-                                              self.max_chain, int(device), C.byref(self._handle)), "kpx_batch_create")
+        # n_teams <= 0: as many teams as are co-resident on the device for this model and precision
+        _lib.check(self._lib.kpx_batch_create(C.byref(self._prob_struct), self.precision, int(max(n_teams, 0)),
+                                              int(team_ctas), self.max_chain, int(device), C.byref(self._handle)),
+                   "kpx_batch_create")
+        nt, tc = C.c_int32(0), C.c_int32(0)
+        _lib.check(self._lib.kpx_batch_info(self._handle, C.byref(nt), C.byref(tc)), "kpx_batch_info")
+        self.n_teams, self.team_ctas = int(nt.value), int(tc.value)
 
     def close(self) -> None:
         if getattr(self, "_handle", None):

@@ -96,7 +96,7 @@ struct kpx_batch {
     std::vector<double> obs_min, obs_max;
     int precision = KPX_F64, n_teams = 1, team_ctas = 1, device = 0;
     int max_chunks = 0, max_trace = 4096, max_chain = KPX_MAX_CHAIN;
-    bool cooperative = false;
+    bool cooperative = false, latency = false;
     size_t rs = 8, smem = 0;
     int cap = 0, cap_pad = 0, regions = 0, subs = 0, dirty_pairs_cap = 0;
     char* slab = nullptr;
@@ -138,8 +138,8 @@ void destroy_batch(kpx_batch& b) {
 }
 
 int blocks_per_sm(const kpx_batch& b) {
-    return b.precision == KPX_F64 ? plan_blocks_per_sm_f64(b.prob.model_id, b.prob.n, b.smem)
-                                  : plan_blocks_per_sm_f32(b.prob.model_id, b.prob.n, b.smem);
+    return b.precision == KPX_F64 ? plan_blocks_per_sm_f64(b.prob.model_id, b.prob.n, b.smem, b.latency)
+                                  : plan_blocks_per_sm_f32(b.prob.model_id, b.prob.n, b.smem, b.latency);
 }
 
 // allocate everything a batch of n_teams workspaces needs
@@ -168,13 +168,15 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
 
     cudaDeviceProp dp;
     CU(cudaGetDeviceProperties(&dp, device));
+    b.latency = team_ctas <= 0;     // whole GPU on one query
     const int bps = blocks_per_sm(b);
     if (bps < 1) return fail(KPX_E_ARG, "no kernel for model_id=%d n=%d", prob->model_id, prob->n);
     const int max_resident = bps * dp.multiProcessorCount;
-    if (team_ctas <= 0) {           // whole GPU on one query
+    if (team_ctas <= 0) {
         n_teams = 1;
         team_ctas = max_resident;
     }
+    if (n_teams <= 0) n_teams = std::max(1, max_resident / team_ctas);     // as many teams as fit the device
     if (n_teams < 1) return fail(KPX_E_ARG, "n_teams must be >= 1");
     b.cooperative = team_ctas > 1;
     if (b.cooperative && (long long)n_teams * team_ctas > max_resident)
@@ -270,7 +272,7 @@ PlanLaunch base_launch(kpx_batch& b) {
     PlanLaunch L{};
     L.prob = &b.prob; L.obs_dev = b.obs_dev; L.occ_dev = b.occ_dev; L.ws_dev = b.ws_dev; L.n_teams = b.n_teams; L.team_ctas = b.team_ctas;
     L.max_chunks = b.max_chunks; L.stride = b.cap_pad; L.dirty_pairs_cap = b.dirty_pairs_cap; L.max_trace = b.max_trace; L.max_chain = b.max_chain; L.smem = b.smem;
-    L.cooperative = b.cooperative;
+    L.cooperative = b.cooperative; L.latency = b.latency;
     return L;
 }
 
@@ -386,8 +388,8 @@ int kpx_device_info(int device, int32_t* sm_count, int32_t* f32_blocks, int32_t*
     CU(cudaGetDeviceProperties(&dp, device));
     CU(cudaSetDevice(device));
     if (sm_count) *sm_count = dp.multiProcessorCount;
-    if (f32_blocks) *f32_blocks = plan_blocks_per_sm_f32(KPX_MODEL_DI6, 6, 4096) * dp.multiProcessorCount;
-    if (f64_blocks) *f64_blocks = plan_blocks_per_sm_f64(KPX_MODEL_DI6, 6, 4096) * dp.multiProcessorCount;
+    if (f32_blocks) *f32_blocks = plan_blocks_per_sm_f32(KPX_MODEL_DI6, 6, 4096, false) * dp.multiProcessorCount;
+    if (f64_blocks) *f64_blocks = plan_blocks_per_sm_f64(KPX_MODEL_DI6, 6, 4096, false) * dp.multiProcessorCount;
     return KPX_OK;
 }
 
@@ -872,6 +874,13 @@ int kpx_batch_create(const kpx_problem* prob, int32_t precision, int32_t n_teams
     int rc = init_batch(*b, prob, precision, n_teams, team_ctas, max_chain > 0 ? max_chain : 64, device);
     if (rc) { destroy_batch(*b); delete b; return rc; }
     *out = b;
+    return KPX_OK;
+}
+
+int kpx_batch_info(const kpx_batch* b, int32_t* n_teams, int32_t* team_ctas) {
+    if (!b) return fail(KPX_E_ARG, "null batch");
+    if (n_teams) *n_teams = b->n_teams;
+    if (team_ctas) *team_ctas = b->team_ctas;
     return KPX_OK;
 }
 

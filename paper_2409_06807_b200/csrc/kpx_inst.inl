@@ -17,7 +17,9 @@ cudaError_t do_launch_plan(const PlanLaunch& L, cudaStream_t st) {
     A.max_iters = L.max_iters; A.lam_override = L.lam_override; A.t_max_s = L.t_max_s;
     A.stop_flag = L.stop_flag; A.peer_flags = L.peer_flags; A.n_peers = L.n_peers;
     A.b_chain_start = L.b_chain_start; A.b_chain_control = L.b_chain_control; A.b_chain_dt = L.b_chain_dt;
-    auto kern = plan_kernel<M, Real>;
+    // float64 has one build; float32 has a throughput and a latency build (MinBlocks)
+    constexpr int kLat = sizeof(Real) == 4 ? KPX_LATENCY : KPX_THROUGHPUT;
+    auto kern = L.latency ? plan_kernel<M, Real, kLat> : plan_kernel<M, Real, KPX_THROUGHPUT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
     const dim3 grid((unsigned)(L.n_teams * L.team_ctas)), block(kBlock);
@@ -45,8 +47,9 @@ cudaError_t do_launch_batch(const BatchLaunch& L, cudaStream_t st) {
 }
 
 template <class M>
-int do_occupancy(size_t smem) {
-    auto kern = plan_kernel<M, Real>;
+int do_occupancy(size_t smem, bool latency) {
+    constexpr int kLat = sizeof(Real) == 4 ? KPX_LATENCY : KPX_THROUGHPUT;
+    auto kern = latency ? plan_kernel<M, Real, kLat> : plan_kernel<M, Real, KPX_THROUGHPUT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, smem) != cudaSuccess) return 0;
@@ -95,8 +98,8 @@ void KPX_CAT(occupancy_masks_, KPX_SUFFIX)(const kpx_problem& pr, int n_obs, con
     build_occupancy_masks<Real>(P, n_obs, omin, omax, masks);
 }
 
-int KPX_CAT(plan_blocks_per_sm_, KPX_SUFFIX)(int model_id, int n, size_t smem) {
-#define CALL(M) return do_occupancy<M>(smem)
+int KPX_CAT(plan_blocks_per_sm_, KPX_SUFFIX)(int model_id, int n, size_t smem, bool latency) {
+#define CALL(M) return do_occupancy<M>(smem, latency)
     KPX_DISPATCH(CALL)
 #undef CALL
     return 0;

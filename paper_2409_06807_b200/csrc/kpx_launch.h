@@ -25,6 +25,7 @@ struct PlanLaunch {
     double *b_chain_start, *b_chain_control, *b_chain_dt;
     size_t smem;
     bool cooperative;
+    bool latency;                   // one query on the whole GPU: the latency build of the float32 kernels
 };
 
 struct BatchLaunch {
@@ -64,7 +65,7 @@ cudaError_t launch_batch_f32(const BatchLaunch& L, cudaStream_t st);
 void occupancy_masks_f64(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);
 void occupancy_masks_f32(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);
 // co-resident CTAs per SM of the plan kernel for this model (0 if unsupported)
-int plan_blocks_per_sm_f64(int model_id, int n, size_t smem);
-int plan_blocks_per_sm_f32(int model_id, int n, size_t smem);
+int plan_blocks_per_sm_f64(int model_id, int n, size_t smem, bool latency);
+int plan_blocks_per_sm_f32(int model_id, int n, size_t smem, bool latency);
 
 }  // namespace kpx

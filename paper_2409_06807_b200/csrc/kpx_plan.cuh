@@ -28,11 +28,26 @@
 #pragma once
 #include "kpx_device.cuh"
 
-#ifndef KPX_MINB_F32_SMALL
-#define KPX_MINB_F32_SMALL 4
+// Resident CTAs per SM the float32 kernels are compiled for (register budget = 65536 / (256 * n)), per use:
+// THROUGHPUT (many queries, one CTA each) wants warps to hide latency; LATENCY (one query on the whole GPU)
+// wants fewer, fatter CTAs: fewer barrier participants and no spills.  Measured on B200.
+#ifndef KPX_MINB_F32_DI
+#define KPX_MINB_F32_DI 4        // double integrators (6-D blocks), throughput
+#endif
+#ifndef KPX_MINS_F32_DI
+#define KPX_MINS_F32_DI 2        // ... latency
+#endif
+#ifndef KPX_MINB_F32_TRIG6
+#define KPX_MINB_F32_TRIG6 3     // Dubins airplane, throughput
+#endif
+#ifndef KPX_MINS_F32_TRIG6
+#define KPX_MINS_F32_TRIG6 3
 #endif
 #ifndef KPX_MINB_F32_MID
-#define KPX_MINB_F32_MID 2
+#define KPX_MINB_F32_MID 3       // 12-D models (quadcopter, 2 stacked integrators), throughput
+#endif
+#ifndef KPX_MINS_F32_MID
+#define KPX_MINS_F32_MID 2
 #endif
 
 // Everything on the propagation path is inlined into the kernel: measured on B200, any out-of-line call on
@@ -922,12 +937,17 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
     finish_query<M, R>(A, W, T, RS, res_out, query_index);
 }
 
-// Resident CTAs per SM each instantiation is compiled for (register budget = 65536 / (kBlock * n)).
-// The propagation loop is latency-bound, so the small float32 models trade registers for warps.
-template <class M, class R> struct MinBlocks { static constexpr int value = sizeof(R) == 4 ? (M::N <= 6 ? KPX_MINB_F32_SMALL : (M::N <= 12 ? KPX_MINB_F32_MID : 1)) : (M::N <= 6 ? 2 : 1); };
+enum { KPX_THROUGHPUT = 0, KPX_LATENCY = 1 };
+template <class M, class R, int V> struct MinBlocks {
+    static constexpr bool kDI = M::ID == KPX_MODEL_DI6 || M::ID == KPX_MODEL_STACKED_DI;
+    static constexpr int f32 = M::N <= 6 ? (kDI ? (V == KPX_LATENCY ? KPX_MINS_F32_DI : KPX_MINB_F32_DI)
+                                               : (V == KPX_LATENCY ? KPX_MINS_F32_TRIG6 : KPX_MINB_F32_TRIG6))
+                                         : (M::N <= 12 ? (V == KPX_LATENCY ? KPX_MINS_F32_MID : KPX_MINB_F32_MID) : 1);
+    static constexpr int value = sizeof(R) == 4 ? f32 : (M::N <= 6 ? 2 : 1);
+};
 
-template <class M, class R>
-__global__ void __launch_bounds__(kBlock, MinBlocks<M, R>::value) plan_kernel(const __grid_constant__ PlanArgs<R> A) {
+template <class M, class R, int V>
+__global__ void __launch_bounds__(kBlock, MinBlocks<M, R, V>::value) plan_kernel(const __grid_constant__ PlanArgs<R> A) {
     int* s_prefix = (int*)(kpx_dyn_smem + Scene<R>::bytes(A.P.n_obs));    // [max_chunks + 1], after the scene
     __shared__ int s_w[kBlock / 32 + 1];
     __shared__ double s_d[kBlock / 32];
