@@ -113,6 +113,96 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+
+# ------------------------------------------------------------ kernel seam (reference kernel vs CUDA)
+
+def _load_reference_kernel():
+    """The reference's own compiled propagation kernel (oracle/_ref, built from /root/reference's _kernel.pyx by
+    oracle/build_ref.sh; the checker side of the repository -- never used by the product path)."""
+    import glob
+    import importlib.machinery
+    import importlib.util
+    hits = sorted(glob.glob(os.path.join(ROOT, "oracle", "_ref", "_kernel*.so")))
+    if not hits:
+        return None
+    loader = importlib.machinery.ExtensionFileLoader("_kernel", hits[0])
+    spec = importlib.util.spec_from_file_location("_kernel", hits[0], loader=loader)
+    mod = importlib.util.module_from_spec(spec)
+    loader.exec_module(mod)
+    return mod
+
+
+def kernel_seam(kp, cfg, env, model, device, target_items=1_000_000):
+    """The drop-in boundary itself (`_kernel.propagate_batch`, _kernel.pyx:299-379): one identical batch of
+    ~1 M extensions through (i) the reference's compiled kernel on every host thread and (ii)
+    `CudaBackend.propagate_batch` with HOST arrays in and out (H2D + kernel + D2H inside the timing).
+    Returns items/s for both and the parity of the outputs."""
+    import numpy as np
+    from paper_2409_06807_b200.backend import PlanContext
+    ref = _load_reference_kernel()
+    if ref is None:
+        return {"unavailable": "oracle/_ref/_kernel*.so not built (oracle/build_ref.sh needs /root/reference)"}
+    prob = kp.build_problem(cfg, env, model)
+    with kp.KinoPax(cfg.with_seed(3), env, model, backend="cuda", device=device) as eng:   # a real tree to expand
+        snap = eng.solve(capture_tree=True).tree_snapshot
+    size = int(snap["size"])
+    states = np.ascontiguousarray(snap["states"][:size], dtype=np.float64)
+    lam = 8
+    m = min(size, max(1, target_items // lam))
+    e_slots = np.sort(np.random.default_rng(0).choice(size, size=m, replace=False)).astype(np.int64)
+    g, ck = prob.grid, prob.checker
+    ctx = PlanContext(model=model, seed=11, t_prop=cfg.t_prop, state_lo=ck.state_lo, state_hi=ck.state_hi,
+                      obs_min=env.obstacles_min, obs_max=env.obstacles_max, check_res=prob.check_resolution,
+                      grid_lo=g.lo, grid_width=g.widths, grid_cells=g.cells, grid_strides=g.strides,
+                      subcells=cfg.subcells_per_dim)
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)
+    f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+
+    def run_ref(slots, nthreads):
+        return ref.propagate_batch(states, slots, lam, 11, 5, model.kernel_id, f64(model.control_lo),
+                                   f64(model.control_hi), float(cfg.t_prop), f64(ck.state_lo), f64(ck.state_hi),
+                                   f64(env.obstacles_min).reshape(-1, 3), f64(env.obstacles_max).reshape(-1, 3),
+                                   float(prob.check_resolution), f64(g.lo), f64(g.widths), i64(g.cells), i64(g.strides),
+                                   int(cfg.subcells_per_dim), nthreads)
+
+    def best(fn, reps=3):
+        out, t = None, float("inf")
+        for _ in range(reps):
+            t0 = time.perf_counter(); out = fn(); t = min(t, time.perf_counter() - t0)
+        return out, t
+
+    # whole batch single-threaded (also the parity reference); a bounded sample on every host thread -- the
+    # reference's helpers re-check the GIL on each call, so more OpenMP threads make it slower (SURVEY 6.2)
+    r, t_ref = best(lambda: run_ref(e_slots, 1), reps=1)
+    sample = e_slots[:max(1, 16384 // lam)]
+    _, t_mt = best(lambda: run_ref(sample, threads), reps=1)
+    r_valid, r_region, r_sub, r_end = (np.asarray(r[k]) for k in ("valid", "region", "sub", "end"))
+    items = m * lam
+    ips_1, ips_mt = items / t_ref, len(sample) * lam / t_mt
+    res = {"items": items, "lam": lam, "parents": m, "reference_items_per_s": max(ips_1, ips_mt),
+           "reference_items_per_s_1_thread": ips_1, f"reference_items_per_s_{threads}_threads": ips_mt,
+           "reference_threads": 1 if ips_1 >= ips_mt else threads,
+           "reference": "oracle/_ref: the reference's own _kernel.pyx compiled with its flags (-O3 -fopenmp "
+                        "-ffp-contract=off); whole batch on 1 thread, 16 k-item sample on all threads, best reported"}
+    for name in ("cuda", "cuda-f32"):
+        be = kp.get_backend(name)
+        be.propagate_batch(ctx, states, e_slots[:64], lam, 5)          # context / module warm-up
+        b, t = best(lambda: be.propagate_batch(ctx, states, e_slots, lam, 5))
+        key = "cuda_f64" if name == "cuda" else "cuda_f32"
+        res[key + "_items_per_s"] = items / t
+        res[key + "_kernel_only_items_per_s"] = items / (b.kernel_ms * 1e-3) if b.kernel_ms else None
+        same = bool(np.array_equal(b.valid, r_valid) and np.array_equal(b.region, r_region)
+                    and np.array_equal(b.sub[b.valid == 1], r_sub[r_valid == 1]))
+        if name == "cuda":
+            err = float(np.max(np.abs(b.end - r_end))) if items else 0.0
+            res["parity_f64"] = {"valid_region_sub_identical": same, "max_abs_end_diff": err}
+        else:
+            keep = (b.valid == 1) & (r_valid == 1)
+            rel = float(np.max(np.abs(b.end[keep] - r_end[keep]) / np.maximum(np.abs(r_end[keep]), 1.0))) if keep.any() else 0.0
+            res["parity_f32"] = {"verdicts_agree_frac": float(np.mean(b.valid == r_valid)), "max_rel_end_diff_valid": rel}
+    return res
+
 # --------------------------------------------------------------------------------------- GPU arm
 
 class ClockSampler:
@@ -232,6 +322,14 @@ def run_gpu(args):
                "median_tree_size": statistics.median(trees) if trees else None,
                "revalidated_at_check_resolution": reval, "revalidated_at_fine_resolution": reval_fine}
 
+    # ---- kernel seam leg (rank 0, N = 1): the reference's compiled kernel beside the CUDA backend
+    seam = None
+    if rank == 0 and world == 1 and not args.no_kernel_seam:
+        try:
+            seam = kernel_seam(kp, cfg, env, model, local)
+        except Exception as exc:                     # the seam leg must never take the headline down with it
+            seam = {"error": f"{type(exc).__name__}: {exc}"}
+
     # ---- throughput leg
     bp = kp.BatchPlanner(cfg, env, model, backend=args.backend, team_ctas=args.team_ctas, device=local)
     q_per_gpu = args.queries or q_per_team * bp.n_teams
@@ -343,6 +441,8 @@ def run_gpu(args):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if seam is not None:
+        line["kernel_seam"] = seam
     print(json.dumps(line), flush=True)
 
 
@@ -366,6 +466,7 @@ def main():
     ap.add_argument("--latency-seeds", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-kernel-seam", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
