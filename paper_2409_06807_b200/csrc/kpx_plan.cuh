@@ -267,88 +267,169 @@ __device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __
     }
 }
 
-// S1 of one iteration, out of line so that the propagation loop gets the whole register budget (the
-// caller's run state is saved once around the call): propagate every (EXPAND slot x extension) item, count
-// outcomes per region, claim fresh (region, sub) pairs.  Warps take 32-item units -- from a shared cursor when
-// the items were length-sorted (S0), else one static unit each.
+// ---- S1: propagation ---------------------------------------------------------------------------------
+#ifndef KPX_TILE_CHUNKS
+#define KPX_TILE_CHUNKS 4
+#endif
+constexpr int kTile = KPX_TILE_CHUNKS * kChunk;     // items per tile of the tile-local length sort (one-CTA teams)
+
+// i-th EXPAND slot: chunk by binary search over the chunk prefix, then the chunk-local compacted list
+__device__ __forceinline__ int expand_slot(const Workspace& W, const int* s_prefix, int n_sch_old, int i) {
+    int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
+    while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
+    return __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
+}
+
+// One 32-item unit (warp-synchronous): lane `lane` handles the item stored at position `pos`.
+// sorted: the item number comes from `order` (results stay addressed by item number w through pos_of);
+// unsorted: position == item number.
 template <class M, class R>
-__device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, const RunState& RS,
-                                         int team_rank, const int* s_prefix) {
+__device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q,
+                                               const RunState& RS, const int* s_prefix, int pos, bool sorted) {
     constexpr int N = M::N, NU = M::NU;
     const Params<R>& P = A.P;
-    const int lane = threadIdx.x & 31;
-    int static_unit = (team_rank * kBlock + (int)threadIdx.x) >> 5;     // unsorted: this warp's slice of one round
+    // the iteration header is re-read from shared memory per unit: nothing of it stays in registers
+    const int items = RS.items, lam = RS.lam;
+    const uint64_t h0 = RS.h0;
+    const bool active = pos < items;
+    int w = 0, S = 0;
+    R u[NU], dt = (R)0, x0[N];
+    if (active) {
+        int slot;
+        if (sorted) {
+            w = __ldcg(W.order + pos);
+            slot = __ldcg(W.it_parent + w);
+        } else {
+            w = pos;
+            slot = expand_slot(W, s_prefix, RS.n_sch_old, w / lam);
+            __stcg(W.it_parent + w, slot);
+        }
+        sample_control<M, R>(P, h0, slot, w % lam, u, &dt, &S, nullptr, nullptr);
+        const R* st = (const R*)W.states + slot;
+#pragma unroll
+        for (int d = 0; d < N; ++d) x0[d] = __ldcg(st + (size_t)d * A.stride);
+    } else {
+#pragma unroll
+        for (int d = 0; d < N; ++d) x0[d] = (R)0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) u[j] = (R)0;
+    }
+    ItemOut<R, N> o;
+    integrate_and_map<M, R>(P, active, x0, u, dt, S, o);     // warp-synchronous
+    int region = -1; bool valid = false;
+    if (active) {
+        region = o.region; valid = o.valid;
+        uint32_t code = kItemInvalid;
+        if (valid) {
+            const uint32_t pair = (uint32_t)region * (uint32_t)P.subs_per_region + (uint32_t)o.sub;
+            const R d0 = o.end[0] - (R)Q.goal[0], d1 = o.end[1] - (R)Q.goal[1], d2 = o.end[2] - (R)Q.goal[2];
+            const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= (R)Q.goal[3];
+            code = pair | (hit ? kItemGoalBit : 0u);
+            R* e = (R*)W.it_end + pos;
+#pragma unroll
+            for (int d = 0; d < N; ++d) __stcg(e + (size_t)d * A.stride, o.end[d]);
+            if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
+        }
+        __stcg(W.it_code + pos, code);
+    }
+    count_outcome(W.n_valid, W.n_invalid, region, valid, active, W.touched_bits);
+    // work counters: one reduction and one fire-and-forget atomic per unit
+    const int t_sub = __reduce_add_sync(0xffffffffu, active ? o.substeps : 0);
+    const int t_pts = __reduce_add_sync(0xffffffffu, active ? o.points : 0);
+    const int t_box = __reduce_add_sync(0xffffffffu, active ? o.boxsteps : 0);
+    const int t_val = __popc(__ballot_sync(0xffffffffu, valid));
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&W.ctl->sum_substeps, (unsigned long long)t_sub);
+        atomicAdd(&W.ctl->sum_points, (unsigned long long)t_pts);
+        atomicAdd(&W.ctl->sum_boxsteps, (unsigned long long)t_box);
+        if (t_val) atomicAdd(&W.ctl->cnt_valid[RS.par], t_val);
+    }
+}
+
+// S1 of one iteration: propagate every (EXPAND slot x extension) item, count outcomes per region, claim fresh
+// (region, sub) pairs.  Three schedules, identical results (everything downstream is addressed by item number):
+//   * few items (one round of the team's threads): position == item number, one static unit per warp;
+//   * a team of many CTAs: the items were sorted by length over the whole iteration (S0 in iteration_head),
+//     warps pull units from a shared cursor, longest first;
+//   * a team of ONE CTA (many queries per GPU): tiles of kTile consecutive items are sorted by length in shared
+//     memory and propagated right away.  A warp's 32 items then have nearly equal length AND parents that lie
+//     within a few KB of each other in every SoA row (a tile spans kTile / lambda consecutive EXPAND slots), so
+//     the parent-state gather stays in a handful of sectors instead of 32 per row, and S0 needs neither global
+//     atomics nor team barriers.
+template <class M, class R>
+__device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, const RunState& RS,
+                                         int team_rank, int team_ctas, const int* s_prefix, int* s_bin) {
+    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    const bool sorted = RS.sorted != 0;
+    const bool tiled = sorted && team_ctas == 1;
+    uint8_t* const s_len = (uint8_t*)(kpx_dyn_smem + Scene<R>::kCoop);   // [kTile]; the staging area is idle while sorting
+    static_assert(sizeof(WarpCoop<R>) * kWarps >= kTile, "tile lengths must fit the staging area");
+    int tile = -kTile, n_units = 0;
+    int unit = sorted ? 0x3fffffff : (team_rank * kBlock + tid) >> 5;    // unsorted: this warp's slice of the one round
+    // one loop, one copy of the integrator: the three schedules only differ in how the next unit is found
 #pragma unroll 1
     for (;;) {
-        // the iteration header is re-read from shared memory per unit: nothing of it stays in registers
-        const int items = RS.items, lam = RS.lam, n_sch_old = RS.n_sch_old, par = RS.par;
-        const bool sorted = RS.sorted != 0;
-        const uint64_t h0 = RS.h0;
-        int unit = static_unit;
-        if (sorted) {
+        int pos;
+        if (tiled) {
+            if (unit >= n_units) {
+                // this warp is through with the tile: every warp of the CTA meets here once per tile.
+                // Counting sort of the next tile by substep count, longest first.
+                tile += kTile;
+                const int items = RS.items;
+                if (tile >= items) break;
+                const int lam = RS.lam, n_sch_old = RS.n_sch_old;
+                const uint64_t h0 = RS.h0;
+                const int n_t = items - tile < kTile ? items - tile : kTile;
+                __syncthreads();                        // the previous tile's walks are done with the staging area
+                for (int b = tid; b < 2 * kBins; b += kBlock) s_bin[b] = 0;          // histogram | fill
+                if (tid == 0) s_bin[3 * kBins] = 0;                                  // unit cursor of the tile
+                __syncthreads();
+#pragma unroll 1
+                for (int j = tid; j < n_t; j += kBlock) {
+                    const int w = tile + j;
+                    const int i = w / lam;
+                    const int slot = expand_slot(W, s_prefix, n_sch_old, i);
+                    int S = substeps_of<M, R>(A.P, h0, slot, w - i * lam);
+                    S = S < kBins - 1 ? S : kBins - 1;
+                    __stcg(W.it_parent + w, slot);
+                    s_len[j] = (uint8_t)S;
+                    atomicAdd(&s_bin[S], 1);
+                }
+                __syncthreads();
+                if (tid < 32) {                         // start of every bin, longest first (2 bins per lane)
+                    const int b1 = kBins - 1 - 2 * lane, b0 = b1 - 1;
+                    const int h1 = s_bin[b1], h0c = s_bin[b0];
+                    const int incl = warp_incl_scan(h1 + h0c);
+                    s_bin[2 * kBins + b1] = incl - h1 - h0c;
+                    s_bin[2 * kBins + b0] = incl - h0c;
+                }
+                __syncthreads();
+#pragma unroll 1
+                for (int j = tid; j < n_t; j += kBlock) {
+                    const int b = s_len[j];
+                    const int p = tile + s_bin[2 * kBins + b] + atomicAdd(&s_bin[kBins + b], 1);
+                    __stcg(W.order + p, tile + j);
+                    __stcg(W.pos_of + tile + j, p);     // results of item w are stored at its sorted position
+                }
+                __syncthreads();
+                n_units = (n_t + 31) >> 5;
+            }
+            // warps pull the tile's units from a shared-memory cursor, longest first
+            if (lane == 0) unit = atomicAdd(&s_bin[3 * kBins], 1);
+            unit = __shfl_sync(0xffffffffu, unit, 0);
+            if (unit >= n_units) continue;              // tile exhausted: on to the next one
+            pos = tile + unit * 32 + lane;
+        } else if (sorted) {
             if (lane == 0) unit = (int)atomicAdd(&W.ctl->unit_next, 1u);
             unit = __shfl_sync(0xffffffffu, unit, 0);
+            if ((long long)unit * 32 >= RS.items) break;
+            pos = unit * 32 + lane;
         } else {
-            static_unit = 0x3fffffff;                   // one round only
+            if ((long long)unit * 32 >= RS.items) break;
+            pos = unit * 32 + lane;
+            unit = 0x3fffffff;                          // one round only
         }
-        if ((long long)unit * 32 >= items) break;
-        const int pos = unit * 32 + lane;
-        const bool active = pos < items;
-        int w = 0, S = 0;
-        R u[NU], dt = (R)0, x0[N];
-        if (active) {
-            int slot;
-            if (sorted) {
-                w = __ldcg(W.order + pos);
-                slot = __ldcg(W.it_parent + w);
-            } else {
-                w = pos;
-                const int i = w / lam;
-                int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
-                while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
-                slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
-                __stcg(W.it_parent + w, slot);
-            }
-            sample_control<M, R>(P, h0, slot, w % lam, u, &dt, &S, nullptr, nullptr);
-            const R* st = (const R*)W.states + slot;
-#pragma unroll
-            for (int d = 0; d < N; ++d) x0[d] = __ldcg(st + (size_t)d * A.stride);
-        } else {
-#pragma unroll
-            for (int d = 0; d < N; ++d) x0[d] = (R)0;
-#pragma unroll
-            for (int j = 0; j < NU; ++j) u[j] = (R)0;
-        }
-        ItemOut<R, N> o;
-        integrate_and_map<M, R>(P, active, x0, u, dt, S, o);     // warp-synchronous
-        int region = -1; bool valid = false;
-        if (active) {
-            region = o.region; valid = o.valid;
-            uint32_t code = kItemInvalid;
-            if (valid) {
-                const uint32_t pair = (uint32_t)region * (uint32_t)P.subs_per_region + (uint32_t)o.sub;
-                const R d0 = o.end[0] - (R)Q.goal[0], d1 = o.end[1] - (R)Q.goal[1], d2 = o.end[2] - (R)Q.goal[2];
-                const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= (R)Q.goal[3];
-                code = pair | (hit ? kItemGoalBit : 0u);
-                R* e = (R*)W.it_end + pos;
-#pragma unroll
-                for (int d = 0; d < N; ++d) __stcg(e + (size_t)d * A.stride, o.end[d]);
-                if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
-            }
-            __stcg(W.it_code + pos, code);
-        }
-        count_outcome(W.n_valid, W.n_invalid, region, valid, active, W.touched_bits);
-        // work counters: one reduction and one fire-and-forget atomic per unit
-        const int t_sub = __reduce_add_sync(0xffffffffu, active ? o.substeps : 0);
-        const int t_pts = __reduce_add_sync(0xffffffffu, active ? o.points : 0);
-        const int t_box = __reduce_add_sync(0xffffffffu, active ? o.boxsteps : 0);
-        const int t_val = __popc(__ballot_sync(0xffffffffu, valid));
-        if (lane == 0) {
-            atomicAdd(&W.ctl->sum_substeps, (unsigned long long)t_sub);
-            atomicAdd(&W.ctl->sum_points, (unsigned long long)t_pts);
-            atomicAdd(&W.ctl->sum_boxsteps, (unsigned long long)t_box);
-            if (t_val) atomicAdd(&W.ctl->cnt_valid[par], t_val);
-        }
+        propagate_unit<M, R>(A, W, Q, RS, s_prefix, pos, sorted);
     }
 }
 
@@ -490,7 +571,8 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
         // 32-item units from a shared cursor, so neither lanes nor warps idle behind one long extension.
         // Results stay indexed by the item number w, so nothing downstream sees the processing order.
         // An iteration that fits in one round (items <= team threads) gains nothing from it and skips S0.
-        if (sorted) {
+        const bool global_sort = sorted && T.ctas > 1;    // one-CTA teams sort tile by tile inside S1
+        if (global_sort) {
             for (int b = tid; b < kBins; b += kBlock) { s_bin[b] = 0; s_bin[2 * kBins + b] = 0; }
             __syncthreads();
 #pragma unroll 1
@@ -516,8 +598,8 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
                 s_bin[kBins + b] = h ? (int)atomicAdd(W.bin_cursor + b, (unsigned)h) : 0;
             }
         }
-        if (sorted) team_sync(T);
-        if (sorted) {
+        if (global_sort) team_sync(T);
+        if (global_sort) {
             if (tid < kBins) s_bin[3 * kBins + tid] = (int)__ldcg(W.bin_cursor + tid);
             __syncthreads();
             if (tid == 0) {
@@ -536,7 +618,7 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
                 }
             }
         }
-        if (sorted) team_sync(T);
+        if (global_sort) team_sync(T);
         if (keeper) RS.tp[1] = gtimer();
 
     __syncthreads();                            // the iteration header is visible to the whole CTA
@@ -929,7 +1011,7 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
         __syncthreads();
     }
     while (iteration_head<M, R>(A, W, T, Q, RS, s_prefix, s_bin)) {
-        s1_propagate<M, R>(A, W, Q, RS, T.rank, s_prefix);
+        s1_propagate<M, R>(A, W, Q, RS, T.rank, T.ctas, s_prefix, s_bin);
         team_sync(T);
         if (T.rank == 0 && threadIdx.x == 0) RS.tp[2] = gtimer();
         iteration_tail<M, R>(A, W, T, Q, RS, s_prefix, s_w, s_d);
