@@ -441,6 +441,7 @@ __device__ __forceinline__ bool point_hits(const Params<R>& P, R px, R py, R pz)
     const R* bx = Scene<R>::boxes();
     bool h = false;
     if (P.occ_g == 0) {
+#pragma unroll 1
         for (int k = 0; k < P.n_obs; ++k) {
             const Box<R> b = load_box(bx, k);
             h = h || (px >= b.lx && px <= b.hx && py >= b.ly && py <= b.hy && pz >= b.lz && pz <= b.hz);
@@ -451,6 +452,7 @@ __device__ __forceinline__ bool point_hits(const Params<R>& P, R px, R py, R pz)
     const int iy = occ_cell<R>(py, P.occ_lo[1], P.occ_inv[1]);
     const int iz = occ_cell<R>(pz, P.occ_lo[2], P.occ_inv[2]);
     uint32_t m = Scene<R>::occ()[(ix * kOccGrid + iy) * kOccGrid + iz];
+#pragma unroll 1
     while (m) {
         const Box<R> b = load_box(bx, __ffs(m) - 1);
         m &= m - 1;
@@ -473,6 +475,7 @@ __device__ KPX_WALK_ATTR int walk_segment(const Params<R>* Pp, R p0, R p1, R p2,
     R thr = P.check_res, inv_steps = (R)1;
     while (thr < dist) { thr += thr; inv_steps *= (R)0.5; steps <<= 1; }
     R t = (R)0;
+#pragma unroll 1
     for (int j = 1; j < steps; ++j) {
         t += inv_steps;
         if (point_hits<R>(P, p0 + t * dx, p1 + t * dy, p2 + t * dz)) return -j;
@@ -596,7 +599,7 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
             if (ok && n_obs > 0) {
                 dx = cur[0] - q0; dy = cur[1] - q1; dz = cur[2] - q2;
                 const R d2 = dx * dx + dy * dy + dz * dz;
-                if (!grid) {
+                if (__builtin_expect(!grid, 0)) {
                     const int r = walk_segment<R>(&P, q0, q1, q2, dx, dy, dz, cur[0], cur[1], cur[2], d2);
                     points += r < 0 ? -r : r;
                     if (r < 0) { ok = false; box_end = s + 1; }
@@ -627,7 +630,7 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
                             cand = (hx >= b.lx) & (lx <= b.hx) & (hy >= b.ly) & (ly <= b.hy) & (hz >= b.lz) & (lz <= b.hz);
                         } while (m && !cand);
                     }
-                    if (d2 > P.d2_thr[3]) {              // more than kCoopSteps points: walk it here
+                    if (__builtin_expect(d2 > P.d2_thr[3], 0)) {   // more than kCoopSteps points: walk it here
                         int r;
                         if (cand) {
                             r = walk_segment<R>(&P, q0, q1, q2, dx, dy, dz, cur[0], cur[1], cur[2], d2);
@@ -650,40 +653,41 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
             }
         }
         if (grid) {
-            const unsigned cm = __ballot_sync(FULL, cand);
-            if (cm) {
-                const unsigned pm = __ballot_sync(FULL, pend);
+            const bool last = s + 1 >= Smax;             // the item ends: whatever is staged is resolved now
+            unsigned cm = __ballot_sync(FULL, cand);
+            if (cm || last) {
                 WarpCoop<R>& C = Scene<R>::coop();
                 const int lane = threadIdx.x & 31;
-                if (cm & pm) {                           // a lane needs its slot again: resolve what is staged
-                    const int hit = coop_walk<R>(&P, pend);
-                    if (hit != 0x7fffffff) {
-                        ok = false; cand = false; points = C.mark_pts[lane] + hit; box_end = C.mark_sub[lane] + 1;
+                // One static call site of the cooperative walk, run at most twice: a lane that needs its slot
+                // again forces a walk of what is staged before the new segments are stored.
+#pragma unroll 1
+                for (;;) {
+                    unsigned pm = __ballot_sync(FULL, pend);
+                    const bool conflict = (cm & pm) != 0u;
+                    if (!conflict) {
+                        if (cand) {
+                            C.seg[0][lane] = q0; C.seg[1][lane] = q1; C.seg[2][lane] = q2;
+                            C.seg[3][lane] = dx; C.seg[4][lane] = dy; C.seg[5][lane] = dz;
+                            C.seg[6][lane] = cur[0]; C.seg[7][lane] = cur[1]; C.seg[8][lane] = cur[2];
+                            C.seg[9][lane] = (R)1 / (R)steps;
+                            C.steps[lane] = steps;
+                            C.mark_pts[lane] = points - steps; C.mark_sub[lane] = s;
+                            pend = true; cand = false;
+                        }
+                        pm |= cm; cm = 0u;
                     }
-                    pend = false;
-                }
-                if (cand) {
-                    C.seg[0][lane] = q0; C.seg[1][lane] = q1; C.seg[2][lane] = q2;
-                    C.seg[3][lane] = dx; C.seg[4][lane] = dy; C.seg[5][lane] = dz;
-                    C.seg[6][lane] = cur[0]; C.seg[7][lane] = cur[1]; C.seg[8][lane] = cur[2];
-                    C.seg[9][lane] = (R)1 / (R)steps;
-                    C.steps[lane] = steps;
-                    C.mark_pts[lane] = points - steps; C.mark_sub[lane] = s;
-                    pend = true;
-                }
-                if (__popc(__ballot_sync(FULL, pend)) >= KPX_FLUSH_AT) {
-                    const int hit = coop_walk<R>(&P, pend);
-                    if (hit != 0x7fffffff) { ok = false; points = C.mark_pts[lane] + hit; box_end = C.mark_sub[lane] + 1; }
-                    pend = false;
+                    if (conflict || __popc(pm) >= KPX_FLUSH_AT || (last && pm != 0u)) {
+                        const int hit = coop_walk<R>(&P, pend);
+                        if (hit != 0x7fffffff) {         // the staged segment hits: rewind, and drop a newer one
+                            ok = false; cand = false; points = C.mark_pts[lane] + hit; box_end = C.mark_sub[lane] + 1;
+                        }
+                        pend = false;
+                        if (conflict) cm = __ballot_sync(FULL, cand);
+                    }
+                    if (cm == 0u) break;
                 }
             }
         }
-    }
-    if (grid && __any_sync(FULL, pend)) {
-        WarpCoop<R>& C = Scene<R>::coop();
-        const int lane = threadIdx.x & 31;
-        const int hit = coop_walk<R>(&P, pend);
-        if (hit != 0x7fffffff) { ok = false; points = C.mark_pts[lane] + hit; box_end = C.mark_sub[lane] + 1; }
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) out.end[i] = cur[i];
