@@ -207,7 +207,9 @@ template <> struct MathK<float> {
         if ((q + 1) & 2) co = -co;
         *s = so; *c = co;
     }
-    __device__ static __forceinline__ float mod(float a, float b) { return fmodf(a, b); }
+    // only reached by angles that left [0, 2 pi) by more than a wrap, i.e. diverged states: one floor instead
+    // of fmodf's exact (looping) reduction in the substep loop
+    __device__ static __forceinline__ float mod(float a, float b) { return a - b * floorf(a * (1.0f / b)); }
     __device__ static __forceinline__ float sq(float x) { return sqrtf(x); }
     __device__ static __forceinline__ float fl(float x) { return floorf(x); }
 };
