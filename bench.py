@@ -36,7 +36,36 @@ WORKLOADS = {
     "dubins6_building": ("dubins6", "building", 118, 4),
     "quad12_narrow": ("quad12", "narrow", 336, 4),
     "quad12_forest": ("quad12", "forest", 336, 4),
+    # BASELINE.json config 4: k stacked 3-D double integrators (only block 1 is workspace position).
+    # 12D uses the full-state grid (cells=3).  A full-state grid is not representable for 24D/48D (cells=1 is a
+    # single region: no guidance, the planner fills its tree without reaching the goal), so those two run the
+    # separately labelled variant whose grid spans block 1 only (position + velocity, cells=4, like di6).
+    "di12_forest": ("di12", "forest", 156, 4),
+    "di24_forest": ("di24g6", "forest", 312, 4),
+    "di48_forest": ("di48g6", "forest", 624, 4),
 }
+
+
+def get_workload_model(dynamics, name):
+    """Model of a workload; 'diNNg6' = stacked integrators with the grid on block 1 (6 dims, 4 cells each)."""
+    if name.endswith("g6"):
+        import dataclasses
+        m = dynamics.stacked_double_integrator(int(name[2:-2]) // 6, grid_dims=6)
+        return dataclasses.replace(m, default_cells_per_dim=4)
+    return dynamics.get_model(name)
+
+
+def make_env(kp_envgen, kp_core, model, scene):
+    """Scene of a workload.  Stacked integrators (config 4) reuse the di6 Trees scene: block 1 starts at the
+    scene's start, the other blocks at the centre of their box, at rest."""
+    import numpy as np
+    if model.name.startswith("di") and model.n > 6:
+        base = kp_envgen.gen_environment(scene, "di6", seed=0)
+        start = np.tile(np.array([5.0, 5.0, 5.0, 0.0, 0.0, 0.0]), model.n // 6)
+        start[:3] = base.start[:3]
+        return kp_core.Environment(f"{scene}-{model.name}", base.workspace_lo, base.workspace_hi, base.obstacles_min,
+                                   base.obstacles_max, start, base.goal)
+    return kp_envgen.gen_environment(scene, model, seed=0)
 
 
 def _cfg(kp, model, seed=0, t_max=60.0):
@@ -56,8 +85,8 @@ def _cpu_solve(args):
     import paper_2409_06807_b200.core as core
     from paper_2409_06807_b200 import dynamics, envgen, problem
     model_name, scene, _, _ = WORKLOADS[workload]
-    model = dynamics.get_model(model_name)
-    env = envgen.gen_environment(scene, model, seed=0)
+    model = get_workload_model(dynamics, model_name)
+    env = make_env(envgen, core, model, scene)
     cfg = core.PlannerConfig(t_e=model.default_t_e, t_prop=model.default_t_prop,
                              cells_per_dim=model.default_cells_per_dim, seed=seed, t_max=120.0)
     op = oracle.plan_from_problem(problem.build_problem(cfg, env, model))
@@ -276,8 +305,9 @@ def run_gpu(args):
     from paper_2409_06807_b200 import _lib
 
     L = _lib.load()
-    model = kp.get_model(model_name)
-    env = kp.gen_environment(scene, model, seed=0)
+    from paper_2409_06807_b200 import core as kp_core, dynamics as kp_dynamics, envgen as kp_envgen
+    model = get_workload_model(kp_dynamics, model_name)
+    env = make_env(kp_envgen, kp_core, model, scene)
     cfg = _cfg(kp, model)
     stream = torch.cuda.current_stream().cuda_stream
     sptr = _lib.C.c_void_p(stream)
@@ -422,6 +452,9 @@ def run_gpu(args):
         "batch": {"solved": int((rec["status"] == 0).sum()), "queries": int(len(rec)),
                   "revalidated_f64_on_device": int((rec["checked"] == 1).sum()),
                   "rejected_by_revalidation": int((rec["checked"] == -1).sum()),
+                  "query_device_ms": {"median": float(np.median(rec["device_ms"])),
+                                      "p90": float(np.percentile(rec["device_ms"], 90)),
+                                      "max": float(rec["device_ms"].max())},
                   "median_iterations": float(np.median(rec["iterations"])),
                   "median_tree_size": float(np.median(rec["tree_size"])), "host_checker_sample": f"{okc}/{checked}",
                   "host_and_device_verdicts_agree": f"{agree}/{checked}"},

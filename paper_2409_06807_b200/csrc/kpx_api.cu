@@ -283,27 +283,35 @@ int d2h(std::vector<T>& dst, const void* src, size_t count) {
     return KPX_OK;
 }
 
-// SoA device array of `rows` x `dims` reals -> AoS f64 host
+// chunked-SoA device array (soa_base, kpx_device.cuh) of `rows` x `dims` reals -> AoS f64 host
 int soa_to_aos(const kpx_batch& b, const void* dev, int dims, long long rows, double* out) {
     if (rows == 0) return KPX_OK;
-    std::vector<char> h((size_t)rows * b.rs);
-    for (int d = 0; d < dims; ++d) {
-        CU(cudaMemcpy(h.data(), (const char*)dev + (size_t)d * b.cap_pad * b.rs, (size_t)rows * b.rs,
-                      cudaMemcpyDeviceToHost));
-        if (b.rs == 8) { const double* s = (const double*)h.data(); for (long long i = 0; i < rows; ++i) out[i * dims + d] = s[i]; }
-        else { const float* s = (const float*)h.data(); for (long long i = 0; i < rows; ++i) out[i * dims + d] = (double)s[i]; }
+    const size_t elems = (size_t)((rows + kChunk - 1) / kChunk) * kChunk * dims;      // whole chunks
+    std::vector<char> h(elems * b.rs);
+    CU(cudaMemcpy(h.data(), dev, h.size(), cudaMemcpyDeviceToHost));
+    for (long long i = 0; i < rows; ++i) {
+        const size_t base = soa_base(i, dims);
+        for (int d = 0; d < dims; ++d) {
+            const size_t k = base + (size_t)d * kChunk;
+            out[i * dims + d] = b.rs == 8 ? ((const double*)h.data())[k] : (double)((const float*)h.data())[k];
+        }
     }
     return KPX_OK;
 }
 
 int aos_to_soa(const kpx_batch& b, void* dev, int dims, long long rows, const double* in) {
     if (rows == 0) return KPX_OK;
-    std::vector<char> h((size_t)rows * b.rs);
-    for (int d = 0; d < dims; ++d) {
-        if (b.rs == 8) { double* s = (double*)h.data(); for (long long i = 0; i < rows; ++i) s[i] = in[i * dims + d]; }
-        else { float* s = (float*)h.data(); for (long long i = 0; i < rows; ++i) s[i] = (float)in[i * dims + d]; }
-        CU(cudaMemcpy((char*)dev + (size_t)d * b.cap_pad * b.rs, h.data(), (size_t)rows * b.rs, cudaMemcpyHostToDevice));
+    const size_t elems = (size_t)((rows + kChunk - 1) / kChunk) * kChunk * dims;
+    std::vector<char> h(elems * b.rs, 0);
+    for (long long i = 0; i < rows; ++i) {
+        const size_t base = soa_base(i, dims);
+        for (int d = 0; d < dims; ++d) {
+            const size_t k = base + (size_t)d * kChunk;
+            if (b.rs == 8) ((double*)h.data())[k] = in[i * dims + d];
+            else ((float*)h.data())[k] = (float)in[i * dims + d];
+        }
     }
+    CU(cudaMemcpy(dev, h.data(), h.size(), cudaMemcpyHostToDevice));
     return KPX_OK;
 }
 

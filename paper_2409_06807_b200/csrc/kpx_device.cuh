@@ -44,6 +44,15 @@ constexpr uint32_t kItemGoalBit = 0x80000000u;
 
 enum : int { PH_SAMPLE = 1, PH_ACCEPT = 2, PH_DEMOTE = 3, PH_PROMOTE = 4 };
 
+// Chunked structure-of-arrays for per-node vectors (states, controls, end states): rows of kChunk consecutive
+// slots, the n rows of a chunk adjacent --  element (slot, d) lives at soa_base(slot, n) + d * kChunk.
+// A warp still touches 32 consecutive reals of one dimension (coalesced, vectorisable), but all dimensions of
+// a node lie within n * 4 KB instead of n row strides of ~1 MB apart: one or two pages per node instead of n
+// (page locality for the high-dimensional models when hundreds of workspaces are live).
+__host__ __device__ __forceinline__ size_t soa_base(long long slot, int n) {
+    return ((size_t)(slot / kChunk) * (size_t)n) * kChunk + (size_t)(slot % kChunk);
+}
+
 // ------------------------------------------------------------------ RNG ----
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z += 0x9E3779B97F4A7C15ULL;

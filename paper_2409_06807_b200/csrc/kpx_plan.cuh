@@ -110,7 +110,7 @@ struct RunState {                 // CTA-uniform state of the running query, sha
 };
 
 struct Workspace {                // device pointers of one team's state
-    void *states, *control, *dt;  // R[n][cap], R[nu][cap], R[cap]          (tree arena, SoA)
+    void *states, *control, *dt;  // R[cap/1024][n][1024], R[cap/1024][nu][1024], R[cap]   (tree arena, chunked SoA)
     int *parent, *region;         // [cap]
     uint8_t* tag;                 // [cap]
     int *n_valid, *n_invalid, *cov, *avail_it;   // [R]
@@ -119,7 +119,7 @@ struct Workspace {                // device pointers of one team's state
     uint32_t* touched_bits;       // [ceil(R/32)] regions whose counters the current query has touched (lazy reset)
     int* dirty_pairs;             // log of the (region,sub) pairs marked visited (lazy reset of the claim table)
     uint32_t* claim;              // [R * subs]: kUnclaimed | kVisited | lowest claiming item
-    void* it_end;                 // R[n][cap]  end states of this iteration's valid items
+    void* it_end;                 // chunked SoA like `states`: end states of this iteration's valid items
     uint32_t* it_code;            // [cap] kItemInvalid | (goal bit | pair)
     int *it_rank, *it_parent;     // [cap]
     uint8_t* it_bin;              // [cap] substep-count bin of each item
@@ -305,9 +305,9 @@ __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Works
             __stcg(W.it_parent + w, slot);
         }
         sample_control<M, R>(P, h0, slot, w % lam, u, &dt, &S, nullptr, nullptr);
-        const R* st = (const R*)W.states + slot;
+        const R* st = (const R*)W.states + soa_base(slot, N);
 #pragma unroll
-        for (int d = 0; d < N; ++d) x0[d] = __ldcg(st + (size_t)d * A.stride);
+        for (int d = 0; d < N; ++d) x0[d] = __ldcg(st + d * kChunk);
     } else {
 #pragma unroll
         for (int d = 0; d < N; ++d) x0[d] = (R)0;
@@ -325,9 +325,9 @@ __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Works
             const R d0 = o.end[0] - (R)Q.goal[0], d1 = o.end[1] - (R)Q.goal[1], d2 = o.end[2] - (R)Q.goal[2];
             const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= (R)Q.goal[3];
             code = pair | (hit ? kItemGoalBit : 0u);
-            R* e = (R*)W.it_end + pos;
+            R* e = (R*)W.it_end + soa_base(pos, N);
 #pragma unroll
-            for (int d = 0; d < N; ++d) __stcg(e + (size_t)d * A.stride, o.end[d]);
+            for (int d = 0; d < N; ++d) __stcg(e + d * kChunk, o.end[d]);
             if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
         }
         __stcg(W.it_code + pos, code);
@@ -439,7 +439,6 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
     const Params<R>& P = A.P;                                                                                \
     const int tid = threadIdx.x;                                                                             \
     const int cap = (int)P.t_e;                                                                              \
-    const size_t ld = (size_t)A.stride; /* SoA row stride */                                                 \
     const int RG = P.n_regions, SUBS = P.subs_per_region;                                                    \
     const bool keeper = (T.rank == 0 && tid == 0);                                                           \
     const long long tthreads = (long long)T.ctas * kBlock;                                                   \
@@ -447,7 +446,7 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
     R* const states = (R*)W.states; R* const control = (R*)W.control; R* const dts = (R*)W.dt;               \
     R* const it_end = (R*)W.it_end;                                                                          \
     Ctl* const ctl = W.ctl;                                                                                  \
-    (void)N; (void)NU; (void)cap; (void)ld; (void)RG; (void)SUBS; (void)keeper; (void)tthreads; (void)ttid;  \
+    (void)N; (void)NU; (void)cap; (void)RG; (void)SUBS; (void)keeper; (void)tthreads; (void)ttid;  \
     (void)states; (void)control; (void)dts; (void)it_end; (void)ctl; (void)P;
 
 // ---- reset of a team's workspace for a new query ---------------------------------------------------------
@@ -489,7 +488,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             bool in_goal0;
             for (int d = 0; d < N; ++d) {
                 R x = (R)Q.start[d];
-                states[(size_t)d * ld] = x;
+                states[d * kChunk] = x;                                  // slot 0 (chunked SoA)
                 if (d < P.grid_n) {
                     R rel = (x - P.grid_lo[d]) / P.grid_width[d];
                     R cl = rel < (R)0 ? (R)0 : (rel > P.grid_cmax[d] ? P.grid_cmax[d] : rel);
@@ -500,7 +499,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
                 double d0 = Q.start[0] - Q.goal[0], d1 = Q.start[1] - Q.goal[1], d2 = Q.start[2] - Q.goal[2];
                 in_goal0 = sqrt(d0 * d0 + d1 * d1 + d2 * d2) <= Q.goal[3];
             }
-            for (int j = 0; j < NU; ++j) control[(size_t)j * ld] = (R)0;
+            for (int j = 0; j < NU; ++j) control[j * kChunk] = (R)0;
             dts[0] = (R)0;
             W.parent[0] = -1; W.region[0] = reg; W.tag[0] = KPX_TAG_EXPAND;
             W.cnt_expand[0] = 1; W.e_local[0] = 0;
@@ -745,9 +744,9 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                 R u[NU], dt; int S;
                 sample_control<M, R>(P, h0, par_slot, w % lam, u, &dt, &S, nullptr, nullptr);
 #pragma unroll
-                for (int d = 0; d < N; ++d) states[(size_t)d * ld + slot] = __ldcg(it_end + (size_t)d * ld + ipos);
+                for (int d = 0; d < N; ++d) states[soa_base(slot, N) + d * kChunk] = __ldcg(it_end + soa_base(ipos, N) + d * kChunk);
 #pragma unroll
-                for (int q = 0; q < NU; ++q) control[(size_t)q * ld + slot] = u[q];
+                for (int q = 0; q < NU; ++q) control[soa_base(slot, NU) + q * kChunk] = u[q];
                 dts[slot] = dt;
                 W.parent[slot] = par_slot; W.region[slot] = region; W.tag[slot] = KPX_TAG_EXPAND;
                 if (__ldcg(W.avail_it + region) == 0) {                                      // planner.py:246
@@ -950,14 +949,14 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
                 s = solution_slot;
                 for (int i = len - 1; i >= 0; --i) {
                     const int par_s = __ldcg(W.parent + s);
-                    for (int d = 0; d < N; ++d) c_start[(size_t)i * N + d] = (double)__ldcg(states + (size_t)d * ld + par_s);
-                    for (int q = 0; q < NU; ++q) c_ctrl[(size_t)i * NU + q] = (double)__ldcg(control + (size_t)q * ld + s);
+                    for (int d = 0; d < N; ++d) c_start[(size_t)i * N + d] = (double)__ldcg(states + soa_base(par_s, N) + d * kChunk);
+                    for (int q = 0; q < NU; ++q) c_ctrl[(size_t)i * NU + q] = (double)__ldcg(control + soa_base(s, NU) + q * kChunk);
                     c_dt[i] = (double)__ldcg(dts + s);
                     if (!res_out && W.chain_slot) W.chain_slot[i] = s;
                     s = par_s;
                 }
                 if (!res_out && W.chain_end)
-                    for (int d = 0; d < N; ++d) W.chain_end[d] = (double)__ldcg(states + (size_t)d * ld + solution_slot);
+                    for (int d = 0; d < N; ++d) W.chain_end[d] = (double)__ldcg(states + soa_base(solution_slot, N) + d * kChunk);
             }
             for (int i = 0; i < A.n_peers; ++i) { *((volatile uint32_t*)A.peer_flags[i]) = 1u; }
             if (A.n_peers) __threadfence_system();

@@ -127,7 +127,8 @@ def test_batch_edge_cases(kp, orc):
 
 
 def _step_compare(kp, orc, model_name, scene, t_e, seed, backend, max_iters=60, env=None):
-    model = kp.get_model(model_name)
+    model = kp.get_model(model_name) if isinstance(model_name, str) else model_name
+    model_name = model.name
     env = kp.gen_environment(scene, model, seed=0) if env is None else env
     cfg = small_cfg(kp, model, t_e=t_e, seed=seed)
     op = orc.plan_from_problem(kp.build_problem(cfg, env, model))
@@ -296,3 +297,16 @@ def test_high_dimensional_stacked_integrators(kp, orc):
         env = kp.Environment(f"forest-{model.name}", base.workspace_lo, base.workspace_hi, base.obstacles_min,
                              base.obstacles_max, start, base.goal)
         _step_compare(kp, orc, model.name, "forest", t_e, 3, "cuda", max_iters=12, env=env)
+
+
+def test_stacked_integrators_with_block1_grid(kp, orc):
+    """Config 4 variant for 24D/48D: the grid spans block 1 only (6 of n dims); device vs oracle, every iteration."""
+    import dataclasses
+    for blocks, t_e in ((4, 3000), (8, 2500)):
+        model = dataclasses.replace(kp.stacked_double_integrator(blocks, grid_dims=6), default_cells_per_dim=4)
+        base = kp.gen_environment("forest", "di6", seed=0)
+        start = np.tile(np.array([5.0, 5, 5, 0, 0, 0]), blocks)
+        start[:3] = base.start[:3]
+        env = kp.Environment(f"forest-{model.name}-g6", base.workspace_lo, base.workspace_hi, base.obstacles_min,
+                             base.obstacles_max, start, base.goal)
+        _step_compare(kp, orc, model, "forest", t_e, 5, "cuda", max_iters=12, env=env)
