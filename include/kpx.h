@@ -109,6 +109,17 @@ int kpx_struct_size(int which);
 /* FP32 FMA micro-benchmark on `device` (the non-tensor roofline denominator): dense fused multiply-adds
  * on every SM for roughly `ms_target` milliseconds; *tflops counts 2 flops per FMA. */
 int kpx_fma_peak(int device, double ms_target, double *tflops, double *tflops_f64);
+/*
+ * Host-only views of what the collision cull is built from (no CUDA call; used by the CPU test-suite):
+ *  - kpx_cull_thresholds: out[k] = largest squared length d2 with fl(sqrt(d2)) <= check_res * 2^k, k = 0..3, in
+ *    the arithmetic of `precision` (returned as double) -- the compare-only form of densify_steps
+ *    (validity.py:26-31);
+ *  - kpx_cull_tables: the 16^3 occupancy-mask table followed by its 2x2x2 dilation (2 * 4096 words), and the
+ *    cell lookup's origin / scale per axis (lo[3], inv[3]) so a test can recompute cells.
+ */
+int kpx_cull_thresholds(const kpx_problem *prob, int32_t precision, double *out4);
+int kpx_cull_tables(const kpx_problem *prob, int32_t precision, uint32_t *masks8192, double *lo3, double *inv3);
+
 int kpx_device_info(int device, int32_t *sm_count, int32_t *max_coop_blocks_f32, int32_t *max_coop_blocks_f64);
 
 /*

@@ -391,6 +391,30 @@ int kpx_struct_size(int which) {
     }
 }
 
+int kpx_cull_thresholds(const kpx_problem* prob, int32_t precision, double* out4) {
+    int rc = check_problem(prob);
+    if (rc) return rc;
+    if (!out4) return fail(KPX_E_ARG, "null output");
+    double lo[3], inv[3];
+    if (precision == KPX_F64) cull_constants_f64(*prob, out4, lo, inv); else cull_constants_f32(*prob, out4, lo, inv);
+    return KPX_OK;
+}
+
+int kpx_cull_tables(const kpx_problem* prob, int32_t precision, uint32_t* masks, double* lo3, double* inv3) {
+    int rc = check_problem(prob);
+    if (rc) return rc;
+    if (!masks || !lo3 || !inv3) return fail(KPX_E_ARG, "null output");
+    double thr[4];
+    if (precision == KPX_F64) {
+        cull_constants_f64(*prob, thr, lo3, inv3);
+        occupancy_masks_f64(*prob, std::min(prob->n_obs, 32), prob->obs_min, prob->obs_max, masks);
+    } else {
+        cull_constants_f32(*prob, thr, lo3, inv3);
+        occupancy_masks_f32(*prob, std::min(prob->n_obs, 32), prob->obs_min, prob->obs_max, masks);
+    }
+    return KPX_OK;
+}
+
 int kpx_device_info(int device, int32_t* sm_count, int32_t* f32_blocks, int32_t* f64_blocks) {
     cudaDeviceProp dp;
     CU(cudaGetDeviceProperties(&dp, device));

@@ -98,6 +98,13 @@ void KPX_CAT(occupancy_masks_, KPX_SUFFIX)(const kpx_problem& pr, int n_obs, con
     build_occupancy_masks<Real>(P, n_obs, omin, omax, masks);
 }
 
+void KPX_CAT(cull_constants_, KPX_SUFFIX)(const kpx_problem& pr, double* thr4, double* lo3, double* inv3) {
+    Params<Real> P;
+    fill_params<Real>(P, pr);
+    for (int k = 0; k < 4; ++k) thr4[k] = (double)P.d2_thr[k];
+    for (int a = 0; a < 3; ++a) { lo3[a] = (double)P.occ_lo[a]; inv3[a] = (double)P.occ_inv[a]; }
+}
+
 int KPX_CAT(plan_blocks_per_sm_, KPX_SUFFIX)(int model_id, int n, size_t smem, bool latency) {
 #define CALL(M) return do_occupancy<M>(smem, latency)
     KPX_DISPATCH(CALL)

@@ -64,6 +64,9 @@ cudaError_t launch_batch_f32(const BatchLaunch& L, cudaStream_t st);
 // host: occupancy masks (kOccGrid^3 words) computed with the launch precision's own cell arithmetic
 void occupancy_masks_f64(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);
 void occupancy_masks_f32(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);
+// host: Params<R>::d2_thr and the occupancy lookup constants, as doubles
+void cull_constants_f64(const kpx_problem& pr, double* thr4, double* lo3, double* inv3);
+void cull_constants_f32(const kpx_problem& pr, double* thr4, double* lo3, double* inv3);
 // co-resident CTAs per SM of the plan kernel for this model (0 if unsupported)
 int plan_blocks_per_sm_f64(int model_id, int n, size_t smem, bool latency);
 int plan_blocks_per_sm_f32(int model_id, int n, size_t smem, bool latency);

@@ -197,3 +197,81 @@ def test_native_trajectory_rebuild_and_check(kp):
         L.kpx_trajectory_valid(C.byref(ps), n_seg, _lib.ptr(sampled), _lib.ptr(off), _lib.ptr(far), 0.05,
                                C.byref(ok), C.byref(code))
         assert ok.value == 0 and code.value == 4
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_cull_thresholds_are_exact(kp, precision):
+    """The compare-only densification (kpx_device.cuh, Params::d2_thr) against validity.py:26-31: for squared
+    lengths at and next to every threshold, `steps` from the compares equals the reference's sqrt + doubling loop
+    evaluated in the same arithmetic."""
+    from paper_2409_06807_b200 import _lib
+    L = _lib.load()
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    ft = np.float64 if precision == "f64" else np.float32
+    for res in (0.05, 0.013, 0.2):
+        prob, keep = _lib.problem_from(kp.build_problem(kp.PlannerConfig(t_e=1000, seed=0), env, model, res))
+        thr = np.zeros(4)
+        _lib.check(L.kpx_cull_thresholds(ctypes.byref(prob), _lib.F64 if precision == "f64" else _lib.F32,
+                                         _lib.ptr(thr)), "kpx_cull_thresholds")
+        thr = thr.astype(ft)
+        assert np.all(np.diff(thr) > 0)
+
+        def steps_ref(d2):                      # densify_steps in the arithmetic of `ft`
+            dist, t, m = np.sqrt(ft(d2)), ft(res), 1
+            while t < dist:
+                t, m = ft(t + t), m * 2
+            return m
+
+        def steps_cmp(d2):
+            return 1 + (d2 > thr[0]) + 2 * (d2 > thr[1]) + 4 * (d2 > thr[2])
+
+        rng = np.random.default_rng(0)
+        probes = [ft(x) for x in rng.uniform(0, float(thr[3]), 2000)]
+        for k in range(4):
+            t = thr[k]
+            probes += [t, np.nextafter(t, ft(0)), np.nextafter(t, ft(np.inf)), np.nextafter(np.nextafter(t, ft(np.inf)), ft(np.inf))]
+        for d2 in probes:
+            if d2 <= thr[3]:
+                assert steps_cmp(d2) == steps_ref(d2), (res, float(d2))
+            else:
+                assert steps_ref(d2) > 8, (res, float(d2))
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_cull_tables_are_conservative(kp, precision):
+    """Occupancy tables of the segment cull: a point inside a closed obstacle box always finds that obstacle's
+    bit in its cell's mask; the dilated table is the OR of the 2x2x2 block starting at the cell."""
+    from paper_2409_06807_b200 import _lib
+    L = _lib.load()
+    ft = np.float64 if precision == "f64" else np.float32
+    G = 16
+    for scene, name in (("forest", "di6"), ("building", "dubins6"), ("narrow", "quad12")):
+        model = kp.get_model(name)
+        env = kp.gen_environment(scene, model, seed=0)
+        prob, keep = _lib.problem_from(kp.build_problem(kp.PlannerConfig(t_e=1000, seed=0,
+                                                                         cells_per_dim=model.default_cells_per_dim),
+                                                        env, model))
+        masks, lo, inv = np.zeros(2 * G ** 3, np.uint32), np.zeros(3), np.zeros(3)
+        _lib.check(L.kpx_cull_tables(ctypes.byref(prob), _lib.F64 if precision == "f64" else _lib.F32,
+                                     _lib.ptr(masks), _lib.ptr(lo), _lib.ptr(inv)), "kpx_cull_tables")
+        occ, occ2 = masks[:G ** 3].reshape(G, G, G), masks[G ** 3:].reshape(G, G, G)
+        pad = np.zeros((G + 1, G + 1, G + 1), np.uint32)
+        pad[:G, :G, :G] = occ
+        dil = np.zeros_like(occ)
+        for dx in (0, 1):
+            for dy in (0, 1):
+                for dz in (0, 1):
+                    dil |= pad[dx:dx + G, dy:dy + G, dz:dz + G]
+        assert np.array_equal(dil, occ2)
+        omin, omax = env.obstacles_min.astype(ft), env.obstacles_max.astype(ft)
+        rng = np.random.default_rng(1)
+        pts = rng.uniform(env.workspace_lo, env.workspace_hi, size=(20000, 3)).astype(ft)
+        # add points on obstacle faces / corners: the boxes are closed
+        pts = np.vstack([pts, omin, omax, (omin + omax) / ft(2)])
+        cell = ((pts - lo.astype(ft)) * inv.astype(ft)).astype(np.int64).clip(0, G - 1)      # the kernel's occ_cell
+        m = occ[cell[:, 0], cell[:, 1], cell[:, 2]]
+        inside = np.all((pts[:, None, :] >= omin[None]) & (pts[:, None, :] <= omax[None]), axis=2)   # (P, K)
+        for k in range(len(omin)):
+            assert np.all((m[inside[:, k]] >> np.uint32(k)) & 1), (scene, k)
+        assert inside.any()
