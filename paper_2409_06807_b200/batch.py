@@ -46,6 +46,7 @@ class BatchResult:
     wall_ms: float
     starts: np.ndarray
     goals: np.ndarray
+    replanned: Optional[np.ndarray] = None   # indices re-planned in float64 after the re-validation refused them
 
     def __len__(self) -> int:
         return len(self.records)
@@ -92,8 +93,12 @@ class BatchPlanner:
         nt, tc = C.c_int32(0), C.c_int32(0)
         _lib.check(self._lib.kpx_batch_info(self._handle, C.byref(nt), C.byref(tc)), "kpx_batch_info")
         self.n_teams, self.team_ctas = int(nt.value), int(tc.value)
+        self._f64 = None              # float64 twin, created when a refused float32 solution needs re-planning
 
     def close(self) -> None:
+        if getattr(self, "_f64", None) is not None:
+            self._f64.close()
+            self._f64 = None
         if getattr(self, "_handle", None):
             self._lib.kpx_batch_destroy(self._handle)
             self._handle = None
@@ -111,10 +116,16 @@ class BatchPlanner:
         self.close()
 
     def run(self, seeds: Sequence[int], starts=None, goals=None, t_max: Optional[float] = None,
-            want_chains: bool = True, stream=None) -> BatchResult:
+            want_chains: bool = True, stream=None, replan_rejected: bool = True,
+            validate_resolution: Optional[float] = None) -> BatchResult:
         """Plan ``len(seeds)`` queries; ``starts`` (Q, n) / ``goals`` (Q, 4) default to the environment's.
-        With ``want_chains`` every solution is also re-validated on the device in float64
-        (``BatchResult.validated`` / ``rejected``)."""
+
+        With ``want_chains`` every solution is re-validated on the device in float64
+        (``BatchResult.validated`` / ``rejected``; ``validate_resolution`` overrides the planner's check
+        resolution).  A float32 tree is integrated in float32, so once in a few thousand queries its solution
+        grazes an obstacle or the goal rim in float64: with ``replan_rejected`` those queries are planned again
+        by the float64 kernels (same seeds, still on the GPU) and their records and chains replace the refused
+        ones -- what ``KinoPax.solve`` does for a single query."""
         q = len(seeds)
         if q < 1:
             raise ConfigError("need at least one query")
@@ -124,20 +135,39 @@ class BatchPlanner:
         goals = np.ascontiguousarray(np.tile(self.problem.goal4, (q, 1)) if goals is None else goals, dtype=np.float64)
         if starts.shape != (q, n) or goals.shape != (q, 4):
             raise ConfigError("starts must be (Q, n) and goals (Q, 4)")
-        rec = np.zeros(q, dtype=_lib.QUERY_RESULT_DTYPE)
-        cs = cc = cd = None
-        if want_chains:
-            cs = np.zeros((q, self.max_chain, n))
-            cc = np.zeros((q, self.max_chain, nu))
-            cd = np.zeros((q, self.max_chain))
-        ms = C.c_double(0.0)
+        tm = float(self.cfg.t_max if t_max is None else t_max)
         t0 = time.perf_counter()
-        _lib.check(self._lib.kpx_batch_run(self._handle, q, _lib.ptr(seeds), _lib.ptr(starts), _lib.ptr(goals),
-                                           float(self.cfg.t_max if t_max is None else t_max), _lib.ptr(rec),
-                                           _lib.ptr(cs), _lib.ptr(cc), _lib.ptr(cd), C.byref(ms), stream),
-                   "kpx_batch_run")
-        wall = (time.perf_counter() - t0) * 1e3
-        return BatchResult(rec, cs, cc, cd, ms.value, wall, starts, goals)
+        if validate_resolution is None or not want_chains:
+            rec = np.zeros(q, dtype=_lib.QUERY_RESULT_DTYPE)
+            cs = cc = cd = None
+            if want_chains:
+                cs = np.zeros((q, self.max_chain, n))
+                cc = np.zeros((q, self.max_chain, nu))
+                cd = np.zeros((q, self.max_chain))
+            ms = C.c_double(0.0)
+            _lib.check(self._lib.kpx_batch_run(self._handle, q, _lib.ptr(seeds), _lib.ptr(starts), _lib.ptr(goals), tm,
+                                               _lib.ptr(rec), _lib.ptr(cs), _lib.ptr(cc), _lib.ptr(cd), C.byref(ms),
+                                               stream), "kpx_batch_run")
+            res = BatchResult(rec, cs, cc, cd, ms.value, 0.0, starts, goals)
+        else:
+            self.upload(seeds.astype(np.int64), starts, goals, want_chains=True, stream=stream)
+            self.launch(tm, stream=stream)
+            self.validate(validate_resolution, stream=stream)
+            res = self.download(stream=stream)
+        if want_chains and replan_rejected and self.precision != _lib.F64:
+            bad = np.flatnonzero(res.rejected)
+            if len(bad):
+                if self._f64 is None:
+                    self._f64 = BatchPlanner(self.cfg, self.env, self.model, self.problem.check_resolution, "cuda",
+                                             n_teams=int(min(len(bad), 8)), team_ctas=1, max_chain=self.max_chain,
+                                             device=self.device)
+                r64 = self._f64.run(seeds[bad].astype(np.int64), starts[bad], goals[bad], tm, True, stream, False,
+                                    validate_resolution)
+                res.records[bad] = r64.records
+                res.chain_start[bad], res.chain_control[bad], res.chain_dt[bad] = r64.chain_start, r64.chain_control, r64.chain_dt
+                res.replanned = bad
+        res.wall_ms = (time.perf_counter() - t0) * 1e3
+        return res
 
     # -- resident-input form: upload once, launch many times (what bench.py times with CUDA events) ---
     def upload(self, seeds, starts=None, goals=None, want_chains: bool = False, stream=None) -> int:

@@ -102,6 +102,39 @@ def test_device_revalidation_matches_host_checker(kp, model_name, scene, backend
         assert np.all(missed.records["checked"][sel] == -1) and np.all(missed.records["check_code"][sel] == 4)
 
 
+def test_refused_float32_solutions_are_replanned_in_float64(kp):
+    """BatchPlanner.run: queries whose float32 solution the float64 re-validation refuses are planned again by
+    the float64 kernels and their records / chains replace the refused ones (what KinoPax.solve does for one
+    query).  Refusals are provoked with a validation resolution far finer than the planner's."""
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=20000, seed=0)
+    seeds = np.arange(64)
+    with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", n_teams=16, team_ctas=1) as bp:
+        for res_v in (0.004, 0.001, 0.00025):
+            plain = bp.run(seeds, replan_rejected=False, validate_resolution=res_v)
+            bad = np.flatnonzero(plain.rejected)
+            if len(bad):
+                break
+        else:
+            pytest.skip("no float32 solution was refused even at 200x the planner's resolution")
+        assert plain.replanned is None
+        res = bp.run(seeds, validate_resolution=res_v)
+        assert np.array_equal(res.replanned, bad)
+        good = np.setdiff1d(np.arange(len(seeds)), bad)
+        for k in ("status", "iterations", "tree_size", "chain_len", "checked"):
+            assert np.array_equal(res.records[k][good], plain.records[k][good]), k
+        with kp.BatchPlanner(cfg, env, model, backend="cuda", n_teams=4, team_ctas=1) as b64:
+            r64 = b64.run(seeds[bad], replan_rejected=False, validate_resolution=res_v)
+        for k in ("status", "iterations", "tree_size", "chain_len", "checked", "check_code"):
+            assert np.array_equal(res.records[k][bad], r64.records[k]), k
+        assert np.array_equal(res.chain_dt[bad], r64.chain_dt) and np.array_equal(res.chain_control[bad], r64.chain_control)
+        for q in bad:                                   # the replaced chains are what the host checker sees too
+            if res.status(int(q)) is kp.PlanStatus.SOLVED:
+                _, ok = bp.trajectory(res, int(q), resolution=res_v)
+                assert ok == bool(res.records["checked"][q] == 1)
+
+
 def test_race_flag_stops_a_run(kp):
     """OR-parallel race plumbing on one GPU: a pre-set stop word ends the run at the first iteration
     boundary with TIMEOUT-like status; a solving run raises the peers' words."""
