@@ -122,10 +122,16 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     procs = max(1, min(cores, 64))
     model_name, scene, _, _ = WORKLOADS[args.workload]
-    steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
-    for _ in range(warmup):
+    # honour --steps / --warmup as long as the whole run stays within ~2.5 minutes of CPU wall time
+    t0 = time.perf_counter()
+    first = cpu_throughput(args.workload, procs, procs)
+    t_step = max(time.perf_counter() - t0, 1e-3)
+    warmup = max(1, min(args.warmup, int(30.0 / t_step) + 1))
+    steps = max(1, min(args.steps, int(120.0 / t_step)))
+    for _ in range(warmup - 1):
         cpu_throughput(args.workload, procs, procs)
     res = [cpu_throughput(args.workload, procs, procs) for _ in range(steps)]
+    del first
     plans = sum(r["plans"] for r in res)
     wall = sum(r["wall_s"] for r in res)
     value = plans / wall
@@ -139,8 +145,8 @@ def run_reference(args):
         "success_rate": sum(r["solved"] for r in res) / plans,
         "cpu_baseline": {"value": value, "unit": "plans/s", "cores": procs, "kind": "port",
                          "sample": f"{plans} plans (seeds 0..{procs - 1} per step), {procs} single-thread processes "
-                                   f"of the C oracle (bit-exact restatement of the reference planner; steps capped "
-                                   f"at 3 to bound the run)"},
+                                   f"of the C oracle (bit-exact restatement of the reference planner; steps / warm-up "
+                                   f"are cut only if the run would exceed ~2.5 min)"},
         "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
