@@ -295,6 +295,12 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks (a one-GPU box cannot host two NCCL ranks): KPX_BENCH_DIST_BACKEND=gloo KPX_BENCH_DEVICE=0 run the
+    # multi-rank code path with every rank on one device
+    dist_backend = os.environ.get("KPX_BENCH_DIST_BACKEND", "nccl")
+    if "KPX_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["KPX_BENCH_DEVICE"])
+    red_dev = "cuda" if dist_backend == "nccl" else "cpu"
     model_name, scene, f_step, q_per_team = WORKLOADS[args.workload]
 
     # CPU baseline first (rank 0, N=1 only), before this process touches CUDA: bounded sample, one plan per core
@@ -310,7 +316,10 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(dist_backend)
     import paper_2409_06807_b200 as kp
     from paper_2409_06807_b200 import _lib
 
@@ -413,7 +422,7 @@ def run_gpu(args):
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
     if world > 1:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     res = bp.download(stream=sptr)
@@ -430,7 +439,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     n, nu = model.n, model.control_dim
