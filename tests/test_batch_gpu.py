@@ -155,3 +155,48 @@ def test_race_flag_stops_a_run(kp):
         assert st.status == 0
         torch.cuda.synchronize()
         assert int(peer[0].item()) == 1 and not flags.fired()
+
+
+@pytest.mark.parametrize("name,model_name,scene,exact", [("di6_forest", "di6", "forest", True),
+                                                          ("dubins6_building", "dubins6", "building", False),
+                                                          ("quad12_narrow", "quad12", "narrow", False)])
+def test_full_size_outcomes_match_reference_golden(kp, name, model_name, scene, exact):
+    """BASELINE.json's full-size configurations, seeds 0..99, against what the UNMODIFIED reference produced for
+    them (tests/golden/outcomes_*.json, written by oracle/make_golden.py): the float64 kernels must reproduce
+    status, iteration count, tree size, solution length and duration seed by seed -- all 100 for the double
+    integrator (bit-exact arithmetic), and all but a few for the trig models (CUDA libm vs glibc differ in the
+    last ulp, which can flip a cell decision once in a while).  The float32 kernels must solve a statistically
+    equal share of the seeds."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"outcomes_{name}.json")))
+    recs = sorted(gold["records"], key=lambda r: r["seed"])
+    seeds = np.array([r["seed"] for r in recs])
+    model = kp.get_model(model_name)
+    env = kp.gen_environment(scene, model, seed=0)
+    cfg = kp.PlannerConfig(t_e=model.default_t_e, lambda_max=32, t_prop=model.default_t_prop, epsilon=0.005, delta=1.0,
+                           cells_per_dim=model.default_cells_per_dim, subcells_per_dim=4, t_max=60.0, seed=0)
+    ref_solved = np.array([r["status"] == "solved" for r in recs])
+    with kp.BatchPlanner(cfg, env, model, backend="cuda", team_ctas=1) as bp:
+        res = bp.run(seeds)
+    same = np.zeros(len(seeds), bool)
+    for i, r in enumerate(recs):
+        ok = (res.status(i).value == r["status"] and int(res.records["iterations"][i]) == r["iterations"]
+              and int(res.records["tree_size"][i]) == r["tree_size"])
+        if ok and r["status"] == "solved":
+            L = int(res.records["chain_len"][i])
+            ok = L == r["segments"] and abs(float(res.chain_dt[i, :L].sum()) - r["solution_duration_s"]) < 1e-9
+        same[i] = ok
+    if exact:
+        assert same.all(), np.flatnonzero(~same)
+    else:
+        assert same.mean() >= 0.9, (same.mean(), np.flatnonzero(~same))
+    assert int(res.solved.sum()) == int(ref_solved.sum()) or not exact
+    assert res.validated.sum() == res.solved.sum()            # float64 trees always pass their own re-validation
+    with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", team_ctas=1) as bp32:
+        r32 = bp32.run(seeds)
+    # binomial 3-sigma band around the reference's success count
+    p = ref_solved.mean()
+    band = 3.0 * np.sqrt(max(p * (1 - p), 0.01) * len(seeds)) + 1
+    assert abs(int(r32.solved.sum()) - int(ref_solved.sum())) <= band, (int(r32.solved.sum()), int(ref_solved.sum()))
+    assert not r32.rejected.any()                             # refused solutions were re-planned in float64
