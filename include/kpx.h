@@ -149,6 +149,9 @@ void kpx_plan_destroy(kpx_plan *p);
 /* new query on the same problem: seed, start state (n), goal (cx,cy,cz,r) */
 int kpx_plan_reset(kpx_plan *p, uint64_t seed, const double *start, const double *goal4);
 /* replace the obstacle set / goal without reallocating (same n_obs capacity or fewer) */
+/* Test hook: overwrite the claim-table epoch the next reset starts from (the table is epoch-tagged and only
+ * refilled when the epochs run out, once in 2^(32-bits(t_e)) queries; this lets a test cross that boundary). */
+int kpx_plan_set_epoch(kpx_plan *p, uint32_t epoch_used);
 int kpx_plan_set_obstacles(kpx_plan *p, int32_t n_obs, const double *obs_min, const double *obs_max);
 /*
  * Run the device-resident loop.  t_max seconds (device clock), max_iters <= 0

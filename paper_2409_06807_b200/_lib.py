@@ -82,6 +82,7 @@ _SIGNATURES = {
     "kpx_plan_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.c_int32, C.c_int32, C.POINTER(_vp)]),
     "kpx_plan_destroy": (None, [_vp]),
     "kpx_plan_reset": (C.c_int, [_vp, C.c_uint64, _vp, _vp]),
+    "kpx_plan_set_epoch": (C.c_int, [_vp, C.c_uint32]),
     "kpx_plan_set_obstacles": (C.c_int, [_vp, C.c_int32, _vp, _vp]),
     "kpx_plan_run": (C.c_int, [_vp, C.c_double, C.c_int32, C.c_int32, _vp, _vp, C.c_int32, C.POINTER(Stats), _vp]),
     "kpx_plan_snapshot": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),

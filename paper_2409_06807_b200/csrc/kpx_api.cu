@@ -98,7 +98,7 @@ struct kpx_batch {
     int max_chunks = 0, max_trace = 4096, max_chain = KPX_MAX_CHAIN;
     bool cooperative = false, latency = false;
     size_t rs = 8, smem = 0;
-    int cap = 0, cap_pad = 0, regions = 0, subs = 0, dirty_pairs_cap = 0;
+    int cap = 0, cap_pad = 0, regions = 0, subs = 0, claim_shift = 30;
     char* slab = nullptr;
     size_t ws_bytes = 0;
     std::vector<Workspace> ws_host;
@@ -187,15 +187,16 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     const int n = prob->n, nu = prob->nu;
     const size_t cp = (size_t)b.cap_pad, R = (size_t)b.regions, pairs = R * (size_t)b.subs;
     Carver c;
-    struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, bits, dpairs, dregions, it_end,
+    struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, bits, dregions, it_end,
                         it_code, it_rank, it_parent, it_bin, order, pos_of, bin_cursor, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
                         ch_dt, ch_slot, ch_end, packet; } o;
     o.states = c.take(b.rs * n * cp); o.control = c.take(b.rs * nu * cp); o.dt = c.take(b.rs * cp);
     o.parent = c.take(4 * cp); o.region = c.take(4 * cp); o.tag = c.take(cp);
     o.n_valid = c.take(4 * R); o.n_invalid = c.take(4 * R); o.cov = c.take(4 * R); o.avail = c.take(4 * R);
     o.score = c.take(8 * R); o.claim = c.take(4 * (pairs + 4));
-    b.dirty_pairs_cap = (int)std::min<size_t>(pairs, 4 * cp);
-    o.bits = c.take(4 * ((R + 31) / 32 + 1)); o.dpairs = c.take(4 * (size_t)b.dirty_pairs_cap);
+    b.claim_shift = 1;
+    while ((1ll << b.claim_shift) <= (long long)b.cap) ++b.claim_shift;      // 2^shift > t_e >= item index + 1
+    o.bits = c.take(4 * ((R + 31) / 32 + 1));
     o.dregions = c.take(4 * ((R + 31) / 32 + 1));
     o.it_end = c.take(b.rs * n * cp); o.it_code = c.take(4 * cp); o.it_rank = c.take(4 * cp); o.it_parent = c.take(4 * cp);
     o.it_bin = c.take(cp); o.order = c.take(4 * cp); o.pos_of = c.take(4 * cp); o.bin_cursor = c.take(4 * (size_t)kBins);
@@ -220,7 +221,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         w.parent = (int*)(s + o.parent); w.region = (int*)(s + o.region); w.tag = (uint8_t*)(s + o.tag);
         w.n_valid = (int*)(s + o.n_valid); w.n_invalid = (int*)(s + o.n_invalid); w.cov = (int*)(s + o.cov);
         w.avail_it = (int*)(s + o.avail); w.score = (double*)(s + o.score); w.claim = (uint32_t*)(s + o.claim);
-        w.avail_bits = (uint32_t*)(s + o.bits); w.dirty_pairs = (int*)(s + o.dpairs); w.touched_bits = (uint32_t*)(s + o.dregions);
+        w.avail_bits = (uint32_t*)(s + o.bits); w.touched_bits = (uint32_t*)(s + o.dregions);
         w.it_end = s + o.it_end; w.it_code = (uint32_t*)(s + o.it_code); w.it_rank = (int*)(s + o.it_rank);
         w.it_parent = (int*)(s + o.it_parent); w.e_local = (int*)(s + o.e_local);
         w.it_bin = (uint8_t*)(s + o.it_bin); w.order = (int*)(s + o.order); w.pos_of = (int*)(s + o.pos_of); w.bin_cursor = (unsigned int*)(s + o.bin_cursor);
@@ -231,11 +232,12 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         w.chain_end = (double*)(s + o.ch_end);
         w.packet = (ResultPacket*)(s + o.packet);
     }
-    for (int t = 0; t < n_teams; ++t) {      // a fresh workspace is clean: claim all UNCLAIMED, nothing dirty
+    for (int t = 0; t < n_teams; ++t) {      // a fresh workspace is clean: no pair ever claimed, every epoch left
         CU(cudaMemset(b.ws_host[t].claim, 0xFF, 4 * pairs));
         Ctl c0;
         memset(&c0, 0, sizeof c0);
-        c0.dirty_ok = 1;
+        c0.epoch_valid = 1;
+        c0.epoch_used = (1u << (32 - b.claim_shift)) - 1u;                   // the first query takes e_max
         CU(cudaMemcpy(b.ws_host[t].ctl, &c0, sizeof c0, cudaMemcpyHostToDevice));
     }
     CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
@@ -271,7 +273,7 @@ int launch(kpx_batch& b, const PlanLaunch& L, cudaStream_t st) {
 PlanLaunch base_launch(kpx_batch& b) {
     PlanLaunch L{};
     L.prob = &b.prob; L.obs_dev = b.obs_dev; L.occ_dev = b.occ_dev; L.ws_dev = b.ws_dev; L.n_teams = b.n_teams; L.team_ctas = b.team_ctas;
-    L.max_chunks = b.max_chunks; L.stride = b.cap_pad; L.dirty_pairs_cap = b.dirty_pairs_cap; L.max_trace = b.max_trace; L.max_chain = b.max_chain; L.smem = b.smem;
+    L.max_chunks = b.max_chunks; L.stride = b.cap_pad; L.claim_shift = b.claim_shift; L.max_trace = b.max_trace; L.max_chain = b.max_chain; L.smem = b.smem;
     L.cooperative = b.cooperative; L.latency = b.latency;
     return L;
 }
@@ -518,6 +520,18 @@ int kpx_plan_reset(kpx_plan* p, uint64_t seed, const double* start, const double
     return KPX_OK;
 }
 
+int kpx_plan_set_epoch(kpx_plan* p, uint32_t epoch_used) {
+    if (!p) return fail(KPX_E_ARG, "null plan");
+    kpx_batch& b = p->b;
+    CU(cudaSetDevice(b.device));
+    Ctl c;
+    int rc = read_ctl(b, &c);
+    if (rc) return rc;
+    c.epoch_used = epoch_used;
+    CU(cudaMemcpy(b.ws_host[0].ctl, &c, sizeof c, cudaMemcpyHostToDevice));
+    return KPX_OK;
+}
+
 int kpx_plan_set_obstacles(kpx_plan* p, int32_t n_obs, const double* omin, const double* omax) {
     if (!p) return fail(KPX_E_ARG, "null plan");
     kpx_batch& b = p->b;
@@ -627,7 +641,10 @@ int kpx_plan_regions(kpx_plan* p, int64_t* n_valid, int64_t* n_invalid, int64_t*
     if (visited) {
         std::vector<uint32_t> cl;
         if ((rc = d2h(cl, w.claim, R * (size_t)b.subs))) return rc;
-        for (size_t i = 0; i < cl.size(); ++i) visited[i] = cl[i] == kVisited;
+        Ctl c;
+        if ((rc = read_ctl(b, &c))) return rc;
+        const uint32_t tag = c.epoch_used << b.claim_shift;                   // "visited" of the current query's epoch
+        for (size_t i = 0; i < cl.size(); ++i) visited[i] = cl[i] == tag;
     }
     return KPX_OK;
 }
@@ -756,7 +773,8 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     CU(cudaMemcpy(w.cov, x.data(), 4 * R, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(w.score, score, 8 * R, cudaMemcpyHostToDevice));
     std::vector<uint32_t> cl(R * (size_t)b.subs);
-    for (size_t i = 0; i < cl.size(); ++i) cl[i] = visited[i] ? kVisited : kUnclaimed;
+    const uint32_t load_epoch = (1u << (32 - b.claim_shift)) - 2u;           // e_max
+    for (size_t i = 0; i < cl.size(); ++i) cl[i] = visited[i] ? load_epoch << b.claim_shift : kUnclaimed;
     CU(cudaMemcpy(w.claim, cl.data(), 4 * cl.size(), cudaMemcpyHostToDevice));
     // EXPAND lists per chunk
     std::vector<int> e_local((size_t)b.cap_pad, 0), cnt((size_t)b.max_chunks, 0);
@@ -769,6 +787,7 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     memset(&c, 0, sizeof c);
     c.size = (int)rows; c.iteration = iteration; c.status = KPX_RUNNING; c.solution_slot = -1; c.total_prev = total;
     c.ve = ve; c.first_hit_w = 0x7fffffff; c.rescue_slot = 0x7fffffff;
+    c.epoch_used = load_epoch; c.epoch_valid = 0;      // resumed with this epoch; the next reset is dense
     CU(cudaMemcpy(w.ctl, &c, sizeof c, cudaMemcpyHostToDevice));
     // t_reset_done stays 0: the first resumed launch stamps the start of the run clock itself
     memset(&b.q_host, 0, sizeof b.q_host);

@@ -38,7 +38,7 @@ constexpr int kCoopSteps = 8;        // segments densified into more points than
 #define KPX_FLUSH_AT 12              // deferred segment walks per warp that trigger a cooperative pass
 #endif
 constexpr uint32_t kUnclaimed = 0xFFFFFFFFu;
-constexpr uint32_t kVisited = 0xFFFFFFFEu;
+
 constexpr uint32_t kItemInvalid = 0xFFFFFFFFu;
 constexpr uint32_t kItemGoalBit = 0x80000000u;
 

@@ -13,7 +13,7 @@ cudaError_t do_launch_plan(const PlanLaunch& L, cudaStream_t st) {
     A.obs = (const Real*)L.obs_dev; A.occ = L.occ_dev; A.ws = L.ws_dev; A.queries = L.queries_dev; A.results = L.results_dev;
     A.queue = L.queue_dev; A.n_queries = L.n_queries; A.n_teams = L.n_teams; A.team_ctas = L.team_ctas;
     A.max_chunks = L.max_chunks; A.stride = L.stride;
-    A.dirty_pairs_cap = L.dirty_pairs_cap; A.max_trace = L.max_trace; A.max_chain = L.max_chain; A.resume = L.resume;
+    A.claim_shift = L.claim_shift; A.max_trace = L.max_trace; A.max_chain = L.max_chain; A.resume = L.resume;
     A.max_iters = L.max_iters; A.lam_override = L.lam_override; A.t_max_s = L.t_max_s;
     A.stop_flag = L.stop_flag; A.peer_flags = L.peer_flags; A.n_peers = L.n_peers;
     A.b_chain_start = L.b_chain_start; A.b_chain_control = L.b_chain_control; A.b_chain_dt = L.b_chain_dt;

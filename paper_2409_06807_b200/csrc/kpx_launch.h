@@ -16,7 +16,7 @@ struct PlanLaunch {
     const QueryIn* queries_dev;
     kpx_query_result* results_dev;
     unsigned int* queue_dev;        // null: single bound query
-    int n_queries, n_teams, team_ctas, max_chunks, max_trace, max_chain, stride, dirty_pairs_cap;
+    int n_queries, n_teams, team_ctas, max_chunks, max_trace, max_chain, stride, claim_shift;
     int resume, max_iters, lam_override;
     double t_max_s;
     const uint32_t* stop_flag;

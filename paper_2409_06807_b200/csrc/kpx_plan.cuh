@@ -83,9 +83,10 @@ struct Ctl {                      // one per workspace, global memory
     int cur_query;                // batch mode: query index broadcast to the team
     unsigned int unit_next;       // S1: next 32-item unit of the length-sorted order
     int last_sorted;              // 1 if the last iteration's it_* arrays are in sorted-position order
-    // lazy reset: what the finished query dirtied (valid while dirty_ok; otherwise the next reset is dense)
-    int dirty_ok;
-    unsigned int n_dirty_pairs;
+    // claim-table epoch (see Workspace::claim): the epoch the last query used; epoch_valid = 0 forces a dense
+    // reset of the claim table and the region arrays (fresh state loaded from the host)
+    int epoch_valid;
+    unsigned int epoch_used;
 };
 
 constexpr int kBins = 64;          // substep-count bins of the S0 counting sort (S >= 63 share the last bin)
@@ -105,6 +106,7 @@ struct RunState {                 // CTA-uniform state of the running query, sha
     unsigned long long t_start;   // keeper only
     // header of the current iteration
     int lam, items, n_sch_old, par, sorted;
+    uint32_t claim_tag;           // epoch of this query << claim_shift
     unsigned long long h0;
     unsigned long long tp[7];     // keeper only: phase boundary timestamps
 };
@@ -117,8 +119,13 @@ struct Workspace {                // device pointers of one team's state
     double* score;                // [R]
     uint32_t* avail_bits;         // [ceil(R/32)] bit r set once region r has been made available
     uint32_t* touched_bits;       // [ceil(R/32)] regions whose counters the current query has touched (lazy reset)
-    int* dirty_pairs;             // log of the (region,sub) pairs marked visited (lazy reset of the claim table)
-    uint32_t* claim;              // [R * subs]: kUnclaimed | kVisited | lowest claiming item
+    // [R * subs] first-visit claims, epoch-tagged so that a new query needs no reset: with E the query's epoch
+    // (counting DOWN from query to query) and s = PlanArgs::claim_shift, a word is  E << s        visited,
+    //                                                                              E << s | w+1  claimed by item w
+    // and any word whose upper bits differ from E (older epochs are LARGER, 0xFFFFFFFF = never) is free, which is
+    // exactly the order atomicMin needs: a fresh claim beats stale words, the lowest item beats other items, and
+    // nothing beats "visited".  The table is refilled with 0xFF only when the epochs run out (2^(32-s) - 1 queries).
+    uint32_t* claim;
     void* it_end;                 // chunked SoA like `states`: end states of this iteration's valid items
     uint32_t* it_code;            // [cap] kItemInvalid | (goal bit | pair)
     int *it_rank, *it_parent;     // [cap]
@@ -149,7 +156,7 @@ struct PlanArgs {
     kpx_query_result* results;    // [n_queries] (may be null)
     unsigned int* queue;          // next query index (batch mode)
     int n_queries, n_teams, team_ctas, max_chunks, max_trace, max_chain;
-    int dirty_pairs_cap;
+    int claim_shift;              // bits of a claim word that hold the item index + 1 (2^shift > t_e)
     int stride;                   // row stride (elements) of every SoA array: capacity padded to a chunk multiple
     int resume;                   // 1: continue from Ctl (no reset), single query
     int max_iters, lam_override;
@@ -328,7 +335,8 @@ __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Works
             R* e = (R*)W.it_end + soa_base(pos, N);
 #pragma unroll
             for (int d = 0; d < N; ++d) __stcg(e + d * kChunk, o.end[d]);
-            if (__ldcg(W.claim + pair) != kVisited) atomicMin(W.claim + pair, (uint32_t)w);
+            const uint32_t tag = RS.claim_tag;
+            if (__ldcg(W.claim + pair) != tag) atomicMin(W.claim + pair, tag | (uint32_t)(w + 1));
         }
         __stcg(W.it_code + pos, code);
     }
@@ -457,11 +465,14 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
     {
         if (keeper) ctl->t_begin = gtimer();
         const int n_words = (RG + 31) >> 5;
-        if (__ldcg(&ctl->dirty_ok)) {
-            // lazy reset: the previous query logged every pair it visited and every region it touched
-            const unsigned int np = __ldcg(&ctl->n_dirty_pairs);
-            for (long long i = ttid; i < np; i += tthreads) W.claim[__ldcg(W.dirty_pairs + i)] = kUnclaimed;
-            // one warp per bitmap word, one lane per region
+        // epochs left?  (usable epochs: 2^(32-shift) - 2 down to 0; the all-ones field means "never claimed")
+        const unsigned int e_max = (1u << (32 - A.claim_shift)) - 2u;
+        const unsigned int e_old = __ldcg(&ctl->epoch_used);
+        const bool lazy = __ldcg(&ctl->epoch_valid) != 0 && e_old != 0u && e_old <= e_max + 1u;
+        const unsigned int e_new = lazy ? e_old - 1u : e_max;
+        if (lazy) {
+            // the claim table needs nothing (new epoch); the region arrays are cleared where the previous query
+            // touched them: one warp per bitmap word, one lane per region
             const int lane = tid & 31;
             for (long long wi = ttid >> 5; wi < n_words; wi += tthreads >> 5) {
                 const uint32_t bits = __ldcg(W.touched_bits + wi);
@@ -519,7 +530,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             W.avail_it[reg0] = 1;
             W.avail_bits[reg0 >> 5] = 1u << (reg0 & 31);
             W.touched_bits[reg0 >> 5] = 1u << (reg0 & 31);   // the root's region is dirty from the start
-            ctl->n_dirty_pairs = 0u; ctl->dirty_ok = 1;
+            ctl->epoch_used = e_new; ctl->epoch_valid = 1;
             ctl->t_reset_done = gtimer();
         }
         team_sync(T);
@@ -632,6 +643,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
     const int size = RS.size, it = RS.it, lam = RS.lam, items = RS.items, par = RS.par;
     const bool sorted = RS.sorted != 0;
     const uint64_t h0 = RS.h0;
+    const uint32_t claim_tag = RS.claim_tag;
     const double total_prev = RS.total_prev;
     const int n_ich = (items + kChunk - 1) / kChunk;
     {
@@ -659,7 +671,6 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
             }
             bool keep[4];
             int cnt = 0;
-            int win_pair[4], nwin = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 keep[j] = false;
@@ -667,11 +678,10 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                     const int w = base + j;
                     const uint32_t pair = code[j] & ~kItemGoalBit;
                     const int region = (int)(pair / (uint32_t)SUBS);
-                    const bool first = __ldcg(W.claim + pair) == (uint32_t)w;    // lowest item index wins
+                    const bool first = __ldcg(W.claim + pair) == (claim_tag | (uint32_t)(w + 1));   // lowest item index wins
                     if (first) {
-                        __stcg(W.claim + pair, kVisited);
+                        __stcg(W.claim + pair, claim_tag);                                           // visited
                         atomicAdd(W.cov + region, 1);
-                        win_pair[nwin++] = (int)pair;                                   // logged below, per warp
                     }
                     bool kp = first;
                     if (!kp) {
@@ -683,20 +693,6 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                     if (kp) {
                         ++cnt;
                         if (code[j] & kItemGoalBit) atomicMin(&ctl->first_hit_w, w);
-                    }
-                }
-            }
-            {   // lazy-reset log of the pairs this warp just marked visited: one reservation per warp
-                const int inc = warp_incl_scan(nwin);
-                const int wtot = __shfl_sync(0xffffffffu, inc, 31);
-                if (wtot) {
-                    unsigned int wbase = 0;
-                    if ((tid & 31) == 31) wbase = atomicAdd(&ctl->n_dirty_pairs, (unsigned)wtot);
-                    wbase = __shfl_sync(0xffffffffu, wbase, 31);
-                    const unsigned int mine = wbase + (unsigned)(inc - nwin);
-                    for (int q = 0; q < nwin; ++q) {
-                        if (mine + q < (unsigned)A.dirty_pairs_cap) W.dirty_pairs[mine + q] = win_pair[q];
-                        else ctl->dirty_ok = 0;
                     }
                 }
             }
@@ -1000,6 +996,7 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
             RS.size = size; RS.it = __ldcg(&ctl->iteration); RS.status = __ldcg(&ctl->status);
             RS.solution_slot = __ldcg(&ctl->solution_slot); RS.total_prev = __ldcg(&ctl->total_prev);
             RS.ve = ve; RS.iters = 0;
+            RS.claim_tag = __ldcg(&ctl->epoch_used) << A.claim_shift;
             unsigned long long t_start = 0;     // run clock origin; only the keeper thread uses it
             if (T.rank == 0) {
                 t_start = __ldcg(&ctl->t_reset_done);

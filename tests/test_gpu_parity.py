@@ -310,3 +310,25 @@ def test_stacked_integrators_with_block1_grid(kp, orc):
         env = kp.Environment(f"forest-{model.name}-g6", base.workspace_lo, base.workspace_hi, base.obstacles_min,
                              base.obstacles_max, start, base.goal)
         _step_compare(kp, orc, model, "forest", t_e, 5, "cuda", max_iters=12, env=env)
+
+
+def test_claim_epochs_run_out_and_wrap(kp):
+    """The first-visit table is epoch-tagged (no reset between queries) and refilled only when the epochs run out.
+    Crossing that boundary -- last epochs 1 and 0, then the dense refill -- must not change a single plan."""
+    from paper_2409_06807_b200 import _lib
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=6000, seed=4)
+    for backend in ("cuda", "cuda-f32"):
+        with kp.KinoPax(cfg, env, model, backend=backend) as eng:
+            ref = eng.solve(capture_tree=True)
+            _lib.check(eng._lib.kpx_plan_set_epoch(eng._handle, 2), "kpx_plan_set_epoch")
+            for _ in range(5):                      # epochs 1, 0, refill -> e_max, e_max - 1, ...
+                eng.reset(seed=4)
+                again = eng.solve(capture_tree=True)
+                assert again.status is ref.status and again.stats.iterations == ref.stats.iterations
+                assert again.stats.tree_size == ref.stats.tree_size
+                for k in ("parent", "tag", "region", "states"):
+                    assert np.array_equal(again.tree_snapshot[k], ref.tree_snapshot[k]), k
+                ra, rb = eng.region_state(), None
+                assert ra.visited.sum() > 0
