@@ -602,7 +602,6 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
         }
         bool cand = false;
         int steps = 1;
-        R dx = (R)0, dy = (R)0, dz = (R)0;
         if (run && ok) {
             // closed state box; the state is finite here, so !(x < lo || x > hi) == (x >= lo) & (x <= hi)
             bool inb = true;
@@ -611,7 +610,7 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
             ok = inb;
             if (!ok) box_end = s + 1;
             if (ok && n_obs > 0) {
-                dx = cur[0] - q0; dy = cur[1] - q1; dz = cur[2] - q2;
+                const R dx = cur[0] - q0, dy = cur[1] - q1, dz = cur[2] - q2;
                 const R d2 = dx * dx + dy * dy + dz * dz;
                 if (__builtin_expect(!grid, 0)) {
                     const int r = walk_segment<R>(&P, q0, q1, q2, dx, dy, dz, cur[0], cur[1], cur[2], d2);
@@ -681,7 +680,7 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
                     if (!conflict) {
                         if (cand) {
                             C.seg[0][lane] = q0; C.seg[1][lane] = q1; C.seg[2][lane] = q2;
-                            C.seg[3][lane] = dx; C.seg[4][lane] = dy; C.seg[5][lane] = dz;
+                            C.seg[3][lane] = cur[0] - q0; C.seg[4][lane] = cur[1] - q1; C.seg[5][lane] = cur[2] - q2;
                             C.seg[6][lane] = cur[0]; C.seg[7][lane] = cur[1]; C.seg[8][lane] = cur[2];
                             C.seg[9][lane] = (R)1 / (R)steps;
                             C.steps[lane] = steps;
