@@ -34,6 +34,9 @@ constexpr int kCoopSteps = 8;        // segments densified into more points than
 #ifndef KPX_INT_ATTR
 #define KPX_INT_ATTR __forceinline__
 #endif
+#ifndef KPX_SUBSTEP_UNROLL
+#define KPX_SUBSTEP_UNROLL 1         // unroll factor of the substep loop (2 trades code size for register moves)
+#endif
 #ifndef KPX_FLUSH_AT
 #define KPX_FLUSH_AT 12              // deferred segment walks per warp that trigger a cooperative pass
 #endif
@@ -586,7 +589,8 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
         pcy = occ_cell<R>(cur[1], P.occ_lo[1], P.occ_inv[1]);
         pcz = occ_cell<R>(cur[2], P.occ_lo[2], P.occ_inv[2]);
     }
-#pragma unroll 1
+    constexpr int kUnroll = KPX_SUBSTEP_UNROLL;
+#pragma unroll kUnroll
     for (int s = 0; s < Smax; ++s) {
         bool run = s < S;
         const R q0 = cur[0], q1 = cur[1], q2 = cur[2];      // start of this substep's segment
