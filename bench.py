@@ -466,10 +466,15 @@ def run_gpu(args):
     kern_ms = statistics.mean(step_ms)
     achieved = flops / (kern_ms * 1e-3) / 1e12
     peak = fp32_peak.value if "f32" in args.backend else fp64_peak.value
-    traffic = None
+    # DRAM bytes of one launch of the dominant kernel: measured once per round with `ncu --set full`
+    # (dram__bytes_read.sum + dram__bytes_write.sum, profiles/traffic.json), scaled to this run's queries per launch
+    traffic = traffic_src = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.isfile(prof):
-        traffic = json.load(open(prof)).get(args.workload)
+        tj = json.load(open(prof)).get(args.workload)
+        if tj and tj.get("queries_per_launch"):
+            traffic = float(tj["dram_bytes_per_launch"]) * q_per_gpu / float(tj["queries_per_launch"])
+            traffic_src = f"profiles/{tj['source']}: {tj['dram_bytes_per_launch'] / tj['queries_per_launch'] / 1e6:.1f} MB per query"
     line = {
         "metric": "plans_per_sec", "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -498,6 +503,9 @@ def run_gpu(args):
         "gpu_launches": 2 * args.steps,
         "roofline": {"bound": "fp32" if "f32" in args.backend else "fp64", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "hbm": ({"dram_gbs": traffic / (kern_ms * 1e-3) / 1e9, "peak_gbs": _measured_hbm(),
+                              "frac": traffic / (kern_ms * 1e-3) / 1e9 / _measured_hbm()} if traffic else None),
                      "kernel": "kpx::plan_kernel (one persistent launch per step; the validate kernel that follows "
                                "it is < 1 % of the step)", "kernel_ms": kern_ms,
                      "algorithmic_flops_per_launch": flops,
