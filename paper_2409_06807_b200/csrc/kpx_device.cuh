@@ -16,6 +16,9 @@
 
 #include "../../include/kpx.h"
 
+#ifndef KPX_DI_KAHAN
+#define KPX_DI_KAHAN 1               // Kahan-compensated float32 double-integrator step (0: plain, ~3 % faster, 10x the error)
+#endif
 #ifndef KPX_PACKED_F32
 #define KPX_PACKED_F32 1             // RK4 vector updates and paired sincos on packed float32 pairs (FFMA2 / FADD2 / FMUL2)
 #endif
@@ -455,7 +458,15 @@ __device__ __forceinline__ void rk4_step_f32(float* cur, float* comp, const floa
 // operations per block and with no stage vectors live.  (float64 keeps the staged form: it is pinned bit for
 // bit to the reference's rounding order.)
 __device__ __forceinline__ void di_step_f32(float* cur, float* comp, const float* u, float h, float half_h) {
-#if KPX_PACKED_F32
+#if !KPX_DI_KAHAN
+    // measured alternative without the compensation (profiles/tuning_r01.md): 6 packed + 3 scalar operations
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        cur[i] = __fmaf_rn(h, __fmaf_rn(half_h, u[i], cur[3 + i]), cur[i]);
+        cur[3 + i] = __fmaf_rn(h, u[i], cur[3 + i]);
+    }
+    (void)comp;
+#elif KPX_PACKED_F32
     // axes x and y as a packed pair (FFMA2 / FADD2), z on its own: 18 instead of 27 instructions
     {
         const float2 u2 = make_float2(u[0], u[1]), v2 = make_float2(cur[3], cur[4]), p2 = make_float2(cur[0], cur[1]);
