@@ -2,11 +2,14 @@
 //
 //  * counter RNG (SplitMix64 chain, bit-identical to reference rng.py:30-54)
 //  * robot models as compile-time traits (vector fields of _kernel.pyx:84-130)
-//  * propagate_item<M,R>: one tree extension = sample (u,dt), RK4 in registers,
-//    per-substep finite/box/AABB walk against obstacles staged in shared memory,
-//    clamped grid mapping.  Semantics follow _kernel.pyx:157-296 line by line
-//    (SURVEY.md section 9 lists the rules); R=double built with -fmad=false is
-//    bit-exact for the double integrator, R=float is the throughput path.
+//  * integrate_and_map<M,R> (warp-synchronous): one tree extension per lane = RK4 in
+//    registers (float32: packed pairs, Kahan-compensated), per substep finite / state
+//    box / obstacle walk against the scene staged in shared memory -- the walk as an
+//    exact segment cull through an occupancy grid plus a deferred, warp-cooperative
+//    point walk -- and the clamped grid mapping.  Verdicts and counters follow
+//    _kernel.pyx:157-296 (SURVEY.md section 9 lists the rules); R=double built with
+//    -fmad=false is bit-exact for the double integrator, R=float is the throughput path.
+//  * the shared-memory scene (Scene<R>), the chunked SoA index (soa_base)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -6,8 +6,11 @@
 // sense-reversing barrier in global memory; with one CTA per team it degrades
 // to __syncthreads().  Per iteration (reference planner.py:283-303):
 //
+//   S0  order the items by RK4 substep count (known from the RNG draw alone) so that a warp's 32 items are
+//       equally long: a global counting sort for many-CTA teams, tile by tile in shared memory and fused
+//       with S1 for one-CTA teams; skipped when one round of the team's threads covers the iteration
 //   S1  propagate every (EXPAND slot x extension) item, count outcomes per region
-//       (warp-aggregated atomics), claim fresh (region,sub) pairs with atomicMin(w)
+//       (warp-aggregated atomics), claim fresh (region,sub) pairs with atomicMin on the epoch-tagged table
 //   --- team barrier ---
 //   S2  resolve first-visit winners (lowest item index), acceptance gate against
 //       LAST iteration's p_accept, per-chunk keep counts + chunk-local ranks,
@@ -25,6 +28,11 @@
 // Ordering rules (ascending slot order of V_E, item w = i*lambda + ext, append in
 // item order) are kept by construction: compaction is chunk-ordered and ranks are
 // chunk prefix + in-chunk rank, so the tree is identical for any team size.
+//
+// Code structure: run_query = reset_query, then iteration_head / s1_propagate / iteration_tail until the run
+// ends, then finish_query.  The phases exchange the CTA-uniform run state through RunState in shared memory
+// and re-derive their locals, so nothing but the integrator's own registers is live across S1; everything is
+// __forceinline__ (an out-of-line call anywhere on the propagation path costs ~30 % of the throughput).
 #pragma once
 #include "kpx_device.cuh"
 
