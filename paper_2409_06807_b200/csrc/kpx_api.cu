@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "kpx_launch.h"
@@ -452,8 +454,22 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
                  o_r = c.take(8 * (size_t)items), o_s = c.take(8 * (size_t)items), o_e = c.take(8 * (size_t)items * n),
                  o_c = c.take(8 * (size_t)items * nu), o_d = c.take(8 * (size_t)items), o_a = c.take(8 * (size_t)items),
                  o_ss = c.take(8 * (size_t)items), o_pp = c.take(8 * (size_t)items);
-    if (cudaMalloc(&slab, c.off) != cudaSuccess) { cudaGetLastError(); return fail(KPX_E_CUDA, "cudaMalloc failed"); }
-    struct Guard { char* p; ~Guard() { cudaFree(p); } } guard{slab};
+    // device scratch of the seam call: one grow-only slab per device, kept between calls (the call itself stays
+    // stateless for the caller: nothing in it survives but capacity); serialised by a mutex like the reference's GIL
+    static std::mutex slab_mutex;
+    static std::map<int, std::pair<char*, size_t>> slabs;
+    std::lock_guard<std::mutex> lock(slab_mutex);
+    int dev_id = 0;
+    CU(cudaGetDevice(&dev_id));
+    auto& cached = slabs[dev_id];
+    if (cached.second < c.off) {
+        if (cached.first) cudaFree(cached.first);
+        cached = {nullptr, 0};
+        const size_t want = c.off + c.off / 4;
+        if (cudaMalloc(&cached.first, want) != cudaSuccess) { cudaGetLastError(); return fail(KPX_E_CUDA, "cudaMalloc failed"); }
+        cached.second = want;
+    }
+    slab = cached.first;
     CU(cudaMemcpyAsync(slab + o_states, states, 8 * (size_t)state_rows * n, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(slab + o_slots, e_slots, 8 * (size_t)m, cudaMemcpyHostToDevice, st));
     rc = upload_obstacles(*prob, precision, prob->n_obs, prob->obs_min, prob->obs_max, slab + o_obs, (uint32_t*)(slab + o_occ), st);
