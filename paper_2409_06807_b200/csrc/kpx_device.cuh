@@ -97,17 +97,20 @@ struct Params {
     double t_prop, epsilon, delta, vol;   // RNG / estimates always in f64
     double control_lo[KPX_MAX_CONTROL], control_span[KPX_MAX_CONTROL];  // span = hi - lo (f64, as reference)
     R check_res;
-    R state_lo[KPX_MAX_DIM], state_hi[KPX_MAX_DIM];
+    // the arrays the substep loop reads every iteration are 16-byte aligned: fewer, wider constant loads
+    alignas(16) R state_lo[KPX_MAX_DIM];
+    alignas(16) R state_hi[KPX_MAX_DIM];
     R grid_lo[KPX_MAX_DIM], grid_width[KPX_MAX_DIM];
     R grid_cmax[KPX_MAX_DIM];             // (R)(cells-1)
     int grid_strides[KPX_MAX_DIM];
     int n_regions, subs_per_region;
     // occupancy-mask grid over the position box (0 = disabled -> every obstacle is tested)
     int occ_g;
-    R occ_lo[3], occ_inv[3];
+    alignas(16) R occ_lo[3];
+    alignas(16) R occ_inv[3];
     // d2_thr[k] = largest d2 with sqrt(d2) <= check_res * 2^k: the densification count of a segment
     // (validity.py:26-31) follows from its squared length by compares alone, bit for bit
-    R d2_thr[4];
+    alignas(16) R d2_thr[4];
 };
 
 // largest x with fl(sqrt(x)) <= thr (sqrt is correctly rounded and monotone on host and device alike)
