@@ -178,6 +178,16 @@ int kpx_plan_solution(kpx_plan *p, int64_t max_segments, double *seg_start, doub
  * chain_from_root, from the previous segment's end (seg_start[0] = root).  sampled receives
  * S+1 rows per segment; seg_offset[n_seg+1] the row offsets.  No device work.
  */
+/*
+ * extract_trajectory of the solved plan in ONE host call (planner.py:325-341): fetch the device-built chain
+ * (already on the host in the result packet of kpx_plan_run), rebuild it in float64 like kpx_trajectory and -- when
+ * `start` is given, i.e. the chain is continued from the root (float32 trees) -- check it like kpx_trajectory_valid
+ * against `goal4` at resolution `res`.  Outputs: seg_control (n_seg, nu), seg_dt (n_seg), sampled (rows, n),
+ * seg_offset (n_seg + 1), *ok / *fail_code as kpx_trajectory_valid (ok = 1 when no check was asked for).
+ */
+int kpx_plan_trajectory(kpx_plan *p, const double *start, const double *goal4, double res, int64_t max_seg,
+                        int64_t max_rows, double *seg_control, double *seg_dt, double *sampled,
+                        int64_t *seg_offset, int64_t *n_seg, int32_t *ok, int32_t *fail_code);
 int kpx_trajectory(int32_t model_id, int32_t n, int32_t nu, int64_t n_seg, const double *seg_start,
                    const double *seg_control, const double *seg_dt, int32_t chain_from_root,
                    double *sampled, int64_t max_rows, int64_t *seg_offset);

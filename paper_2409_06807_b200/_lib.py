@@ -88,6 +88,8 @@ _SIGNATURES = {
     "kpx_plan_snapshot": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kpx_plan_regions": (C.c_int, [_vp] * 9),
     "kpx_plan_solution": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp]),
+    "kpx_plan_trajectory": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int64, C.c_int64, _vp, _vp, _vp, _vp,
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kpx_trajectory": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, _vp, _vp, _vp, C.c_int32, _vp, C.c_int64,
                                  _vp]),
     "kpx_trajectory_valid": (C.c_int, [C.POINTER(Problem), C.c_int64, _vp, _vp, _vp, C.c_double,

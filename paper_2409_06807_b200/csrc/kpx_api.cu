@@ -671,8 +671,9 @@ int kpx_plan_solution(kpx_plan* p, int64_t max_segments, double* seg_start, doub
     kpx_batch& b = p->b;
     CU(cudaSetDevice(b.device));
     Ctl c;
-    int rc = read_ctl(b, &c);
-    if (rc) return rc;
+    int rc = KPX_OK;
+    if (b.pk_valid) c = b.pk_host->ctl;                  // the result packet of the last run is on the host
+    else if ((rc = read_ctl(b, &c))) return rc;
     if (c.status != KPX_SOLVED) return fail(KPX_E_STATE, "plan is not solved");
     if (c.chain_len < 0) return fail(KPX_E_LIMIT, "solution chain longer than KPX_MAX_CHAIN");
     if (c.chain_len > max_segments) return fail(KPX_E_ARG, "need room for %d segments", c.chain_len);
@@ -929,6 +930,43 @@ int kpx_trajectory_valid(const kpx_problem* prob, int64_t n_seg, const double* s
         if (!(sqrt(d0 * d0 + d1 * d1 + d2 * d2) <= goal4[3])) { *ok = 0; if (fail_code) *fail_code = 4; }
     }
     return KPX_OK;
+}
+
+int kpx_plan_trajectory(kpx_plan* p, const double* start, const double* goal4, double res, int64_t max_seg,
+                        int64_t max_rows, double* seg_control, double* seg_dt, double* sampled, int64_t* seg_offset,
+                        int64_t* n_seg, int32_t* ok, int32_t* fail_code) {
+    if (!p || !seg_control || !seg_dt || !sampled || !seg_offset || !n_seg || !ok) return fail(KPX_E_ARG, "null argument");
+    kpx_batch& b = p->b;
+    const int n = b.prob.n, nu = b.prob.nu;
+    int status, chain_len;
+    if (b.pk_valid) { status = b.pk_host->ctl.status; chain_len = b.pk_host->ctl.chain_len; }
+    else {
+        CU(cudaSetDevice(b.device));
+        Ctl c;
+        int rc = read_ctl(b, &c);
+        if (rc) return rc;
+        status = c.status; chain_len = c.chain_len;
+    }
+    if (status != KPX_SOLVED) return fail(KPX_E_STATE, "plan is not solved");
+    if (chain_len < 0) return fail(KPX_E_LIMIT, "solution chain longer than KPX_MAX_CHAIN");
+    if (chain_len > max_seg) return fail(KPX_E_ARG, "need room for %d segments", chain_len);
+    const int64_t L = chain_len;
+    *n_seg = L; *ok = 1;
+    if (fail_code) *fail_code = 0;
+    seg_offset[0] = 0;
+    if (L == 0) return KPX_OK;
+    std::vector<double> seg_start((size_t)L * n);
+    int rc = kpx_plan_solution(p, L, seg_start.data(), seg_control, seg_dt, nullptr, nullptr);
+    if (rc) return rc;
+    if (start) memcpy(seg_start.data(), start, sizeof(double) * n);
+    rc = kpx_trajectory(b.prob.model_id, n, nu, L, seg_start.data(), seg_control, seg_dt, start ? 1 : 0, sampled, max_rows,
+                        seg_offset);
+    if (rc) return rc;
+    if (start) {
+        if (!goal4) return fail(KPX_E_ARG, "goal4 is needed to check a chain continued from the root");
+        rc = kpx_trajectory_valid(&b.prob, L, sampled, seg_offset, goal4, res > 0.0 ? res : b.prob.check_res, ok, fail_code);
+    }
+    return rc;
 }
 
 // ------------------------------------------------------------------ batches

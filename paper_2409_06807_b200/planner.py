@@ -17,6 +17,7 @@ compare tree and region state with the oracle after every iteration.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import time
 from dataclasses import dataclass
 from typing import Callable, Optional
@@ -111,6 +112,7 @@ class KinoPax:
         self._lib = _lib.load()
         self._prob_struct, self._keep = _lib.problem_from(self.problem)
         self._handle = _lib._vp()
+        self._traj_buf = None         # reusable host buffers of _trajectory
         _lib.check(self._lib.kpx_plan_create(C.byref(self._prob_struct), self.precision, int(team_ctas), int(device),
                                              C.byref(self._handle)), "kpx_plan_create")
         self.device = device
@@ -245,11 +247,42 @@ class KinoPax:
                        "kpx_plan_solution")
         return out
 
+    _TRAJ_SEGS = 64            # segments the result packet carries; longer chains take the general path
+
     def _trajectory(self) -> tuple:
-        """Segments from the device chain, rebuilt on the host in float64 (``kpx_trajectory`` restates
-        ``propagate_ode``).  f64: every segment starts at the stored parent state, as in the reference
-        (``planner.py:337-341``).  f32: the chain is re-integrated from the root (stored float32 node
-        states cannot chain to 1e-9) and must still be collision-free and end in the goal."""
+        """Segments from the device chain, rebuilt on the host in float64 by ONE native call
+        (``kpx_plan_trajectory`` = ``extract_trajectory`` + ``propagate_ode``, ``planner.py:325-341``,
+        ``dynamics.py:242-283``).  f64: every segment starts at the stored parent state, as in the reference.
+        f32: the chain is re-integrated from the root (stored float32 node states cannot chain to 1e-9) and must
+        still be collision-free and end in the goal (``validity.py:108-125``); ``ok`` reports that check."""
+        n, nu = self.model.n, self.model.control_dim
+        L = int(self.last_stats.chain_len)
+        if L > self._TRAJ_SEGS:
+            return self._trajectory_general()
+        buf = self._traj_buf
+        if buf is None:
+            S = self._TRAJ_SEGS
+            rows = S * (int(math.ceil(self.cfg.t_prop / 0.02)) + 2)
+            ctrl, dts = np.zeros((S, nu)), np.zeros(S)
+            sampled, off = np.empty((rows, n)), np.zeros(S + 1, np.int64)
+            buf = self._traj_buf = (ctrl, dts, sampled, off, rows, _lib.ptr(ctrl), _lib.ptr(dts), _lib.ptr(sampled),
+                                    _lib.ptr(off), C.c_int64(0), C.c_int32(0), C.c_int32(0))
+        ctrl, dts, sampled, off, rows, p_ctrl, p_dts, p_sampled, p_off, nseg, okc, code = buf
+        from_root = self.precision != _lib.F64
+        _lib.check(self._lib.kpx_plan_trajectory(self._handle, _lib.ptr(self.start) if from_root else None,
+                                                 _lib.ptr(self.goal4), self.problem.check_resolution, self._TRAJ_SEGS,
+                                                 rows, p_ctrl, p_dts, p_sampled, p_off, C.byref(nseg), C.byref(okc),
+                                                 C.byref(code)), "kpx_plan_trajectory")
+        L = int(nseg.value)
+        o = off[:L + 1].tolist()
+        states = sampled[:o[L]].copy()                    # one copy: the buffers are reused by the next solve
+        cc, dd = ctrl[:L].copy(), dts[:L].tolist()
+        segs = [TrajectorySegment(control=cc[i], dt=dd[i], end_state=states[o[i + 1] - 1],
+                                  sampled_states=states[o[i]:o[i + 1]]) for i in range(L)]
+        return segs, bool(okc.value)
+
+    def _trajectory_general(self) -> tuple:
+        """The same through the separate entry points, for chains longer than the result packet."""
         chain = self.solution_chain()
         from_root = self.precision != _lib.F64
         n, nu = self.model.n, self.model.control_dim
