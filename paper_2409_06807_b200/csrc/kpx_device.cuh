@@ -743,11 +743,17 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
     for (int s = 0; s < Smax; ++s) {
         bool run = s < S;
         const R q0 = cur[0], q1 = cur[1], q2 = cur[2];      // start of this substep's segment
+        // closed state box, evaluated beside the finite test (two independent predicate chains instead of one
+        // after the other: the warp runs both whenever any lane is still ok, and a lone warp saves the latency);
+        // for a finite state !(x < lo || x > hi) == (x >= lo) & (x <= hi), and the result is only used then
+        bool inb = true;
         if (run) {
             Stepper<M, R>::step(cur, comp, u, h, h6);
             bool fin = true;
 #pragma unroll
             for (int i = 0; i < N; ++i) fin = fin && isfinite(cur[i]);
+#pragma unroll
+            for (int i = 0; i < N; ++i) inb = inb & (cur[i] >= P.state_lo[i]) & (cur[i] <= P.state_hi[i]);
             if (!fin) {                                     // _kernel.pyx:226-232: stop integrating
                 if (ok) box_end = s;
                 alive = false; ok = false; run = false; S = s + 1;
@@ -756,10 +762,6 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
         bool cand = false;
         int steps = 1;
         if (run && ok) {
-            // closed state box; the state is finite here, so !(x < lo || x > hi) == (x >= lo) & (x <= hi)
-            bool inb = true;
-#pragma unroll
-            for (int i = 0; i < N; ++i) inb = inb & (cur[i] >= P.state_lo[i]) & (cur[i] <= P.state_hi[i]);
             ok = inb;
             if (!ok) box_end = s + 1;
             if (ok && n_obs > 0) {
