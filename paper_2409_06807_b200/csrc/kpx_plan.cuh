@@ -46,7 +46,7 @@
 #define KPX_MINS_F32_DI 2        // ... latency
 #endif
 #ifndef KPX_MINB_F32_TRIG6
-#define KPX_MINB_F32_TRIG6 3     // Dubins airplane, throughput
+#define KPX_MINB_F32_TRIG6 4     // Dubins airplane, throughput
 #endif
 #ifndef KPX_MINS_F32_TRIG6
 #define KPX_MINS_F32_TRIG6 3
