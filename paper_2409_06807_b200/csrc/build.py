@@ -1,9 +1,9 @@
 #!/usr/bin/env python3
 """Build libkpx.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-Three translation units: the f64 parity instantiations (``-fmad=false``, the
+Four translation units: the f64 parity instantiations (``-fmad=false``, the
 reference is built with ``-ffp-contract=off``), the f32 throughput
-instantiations, and the C ABI.  The shared library lands next to the Python
+instantiations, the f32 single-query (latency) instantiations, and the C ABI.  The shared library lands next to the Python
 package (``paper_2409_06807_b200/libkpx.so``) so it travels to the GPU box.
 """
 from __future__ import annotations
@@ -23,6 +23,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=o
 UNITS = [
     ("kpx_inst_f64.cu", ["-fmad=false"]),
     ("kpx_inst_f32.cu", []),
+    ("kpx_inst_f32lat.cu", []),
     ("kpx_api.cu", []),
 ]
 HEADERS = ["kpx_device.cuh", "kpx_plan.cuh", "kpx_launch.h", "kpx_inst.inl", os.path.join("..", "..", "include", "kpx.h")]
@@ -54,7 +55,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
         return r.stderr
 
-    with ThreadPoolExecutor(max_workers=3) as ex:
+    with ThreadPoolExecutor(max_workers=4) as ex:
         logs = list(ex.map(run, jobs))
     if verbose:
         for l in logs:

@@ -1,5 +1,14 @@
-// kpx_inst.inl -- included by kpx_inst_f64.cu / kpx_inst_f32.cu with KPX_REAL and KPX_SUFFIX set.
+// kpx_inst.inl -- included by the instantiation units with KPX_REAL and KPX_SUFFIX set:
+//   kpx_inst_f64.cu     double, one build of every kernel (-fmad=false)
+//   kpx_inst_f32.cu     float, THROUGHPUT build of the plan kernels + everything else; forwards single-query
+//                       launches to ...
+//   kpx_inst_f32lat.cu  float, LATENCY build of the plan kernels only (KPX_PLAN_ONLY; its own translation unit so
+//                       that the two float32 builds compile in parallel)
 #include "kpx_launch.h"
+
+#ifndef KPX_VARIANT
+#define KPX_VARIANT KPX_THROUGHPUT
+#endif
 
 namespace kpx {
 namespace {
@@ -17,9 +26,7 @@ cudaError_t do_launch_plan(const PlanLaunch& L, cudaStream_t st) {
     A.max_iters = L.max_iters; A.lam_override = L.lam_override; A.t_max_s = L.t_max_s;
     A.stop_flag = L.stop_flag; A.peer_flags = L.peer_flags; A.n_peers = L.n_peers;
     A.b_chain_start = L.b_chain_start; A.b_chain_control = L.b_chain_control; A.b_chain_dt = L.b_chain_dt;
-    // float64 has one build; float32 has a throughput and a latency build (MinBlocks)
-    constexpr int kLat = sizeof(Real) == 4 ? KPX_LATENCY : KPX_THROUGHPUT;
-    auto kern = L.latency ? plan_kernel<M, Real, kLat> : plan_kernel<M, Real, KPX_THROUGHPUT>;
+    auto kern = plan_kernel<M, Real, KPX_VARIANT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
     const dim3 grid((unsigned)(L.n_teams * L.team_ctas)), block(kBlock);
@@ -31,6 +38,7 @@ cudaError_t do_launch_plan(const PlanLaunch& L, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+#ifndef KPX_PLAN_ONLY
 template <class M>
 cudaError_t do_launch_batch(const BatchLaunch& L, cudaStream_t st) {
     BatchArgs<Real> A;
@@ -46,10 +54,11 @@ cudaError_t do_launch_batch(const BatchLaunch& L, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+#endif  // !KPX_PLAN_ONLY
+
 template <class M>
-int do_occupancy(size_t smem, bool latency) {
-    constexpr int kLat = sizeof(Real) == 4 ? KPX_LATENCY : KPX_THROUGHPUT;
-    auto kern = latency ? plan_kernel<M, Real, kLat> : plan_kernel<M, Real, KPX_THROUGHPUT>;
+int do_occupancy(size_t smem) {
+    auto kern = plan_kernel<M, Real, KPX_VARIANT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kBlock, smem) != cudaSuccess) return 0;
@@ -76,6 +85,9 @@ int do_occupancy(size_t smem, bool latency) {
 #define KPX_CAT(a, b) KPX_CAT2(a, b)
 
 cudaError_t KPX_CAT(launch_plan_, KPX_SUFFIX)(const PlanLaunch& L, cudaStream_t st) {
+#ifdef KPX_FORWARD_LATENCY
+    if (L.latency) return launch_plan_f32lat(L, st);
+#endif
     const int model_id = L.prob->model_id, n = L.prob->n;
 #define CALL(M) return do_launch_plan<M>(L, st)
     KPX_DISPATCH(CALL)
@@ -83,6 +95,7 @@ cudaError_t KPX_CAT(launch_plan_, KPX_SUFFIX)(const PlanLaunch& L, cudaStream_t 
     return cudaErrorInvalidValue;
 }
 
+#ifndef KPX_PLAN_ONLY
 cudaError_t KPX_CAT(launch_batch_, KPX_SUFFIX)(const BatchLaunch& L, cudaStream_t st) {
     const int model_id = L.prob->model_id, n = L.prob->n;
 #define CALL(M) return do_launch_batch<M>(L, st)
@@ -105,8 +118,14 @@ void KPX_CAT(cull_constants_, KPX_SUFFIX)(const kpx_problem& pr, double* thr4, d
     for (int a = 0; a < 3; ++a) { lo3[a] = (double)P.occ_lo[a]; inv3[a] = (double)P.occ_inv[a]; }
 }
 
+#endif  // !KPX_PLAN_ONLY
+
 int KPX_CAT(plan_blocks_per_sm_, KPX_SUFFIX)(int model_id, int n, size_t smem, bool latency) {
-#define CALL(M) return do_occupancy<M>(smem, latency)
+#ifdef KPX_FORWARD_LATENCY
+    if (latency) return plan_blocks_per_sm_f32lat(model_id, n, smem, true);
+#endif
+    (void)latency;
+#define CALL(M) return do_occupancy<M>(smem)
     KPX_DISPATCH(CALL)
 #undef CALL
     return 0;

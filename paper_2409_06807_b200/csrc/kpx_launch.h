@@ -58,7 +58,8 @@ struct ValidateLaunch {
 // each returns cudaErrorInvalidValue for an unsupported (model_id, n)
 cudaError_t launch_validate_f64(const ValidateLaunch& L, cudaStream_t st);
 cudaError_t launch_plan_f64(const PlanLaunch& L, cudaStream_t st);
-cudaError_t launch_plan_f32(const PlanLaunch& L, cudaStream_t st);
+cudaError_t launch_plan_f32(const PlanLaunch& L, cudaStream_t st);       // forwards L.latency launches to ...
+cudaError_t launch_plan_f32lat(const PlanLaunch& L, cudaStream_t st);    // the LATENCY build (own translation unit)
 cudaError_t launch_batch_f64(const BatchLaunch& L, cudaStream_t st);
 cudaError_t launch_batch_f32(const BatchLaunch& L, cudaStream_t st);
 // host: occupancy masks (kOccGrid^3 words) computed with the launch precision's own cell arithmetic
@@ -70,5 +71,6 @@ void cull_constants_f32(const kpx_problem& pr, double* thr4, double* lo3, double
 // co-resident CTAs per SM of the plan kernel for this model (0 if unsupported)
 int plan_blocks_per_sm_f64(int model_id, int n, size_t smem, bool latency);
 int plan_blocks_per_sm_f32(int model_id, int n, size_t smem, bool latency);
+int plan_blocks_per_sm_f32lat(int model_id, int n, size_t smem, bool latency);
 
 }  // namespace kpx
