@@ -332,3 +332,28 @@ def test_claim_epochs_run_out_and_wrap(kp):
                     assert np.array_equal(again.tree_snapshot[k], ref.tree_snapshot[k]), k
                 ra, rb = eng.region_state(), None
                 assert ra.visited.sum() > 0
+
+
+@pytest.mark.parametrize("backend", ["cuda", "cuda-f32"])
+def test_fused_trajectory_call_equals_the_separate_entry_points(kp, backend):
+    """kpx_plan_trajectory (one host call) returns exactly what kpx_plan_solution + kpx_trajectory +
+    kpx_trajectory_valid return together, for both tree precisions (and hence propagate_ode's samples,
+    test_native_trajectory_rebuild_and_check)."""
+    for model_name, scene, t_e in (("di6", "forest", 20000), ("quad12", "forest", 60000)):
+        model = kp.get_model(model_name)
+        env = kp.gen_environment(scene, model, seed=0)
+        cfg = small_cfg(kp, model, t_e=t_e, seed=0)
+        with kp.KinoPax(cfg, env, model, backend=backend) as eng:
+            for seed in range(8):                       # the first seed this small tree solves
+                eng.reset(seed=seed)
+                res = eng.solve()
+                if res.solved and len(res.trajectory) > 0:
+                    break
+            assert res.solved
+            a, ok_a = eng._trajectory()
+            b, ok_b = eng._trajectory_general()
+            assert ok_a == ok_b and len(a) == len(b) == len(res.trajectory) > 0
+            for x, y in zip(a, b):
+                assert x.dt == y.dt and np.array_equal(x.control, y.control)
+                assert np.array_equal(x.sampled_states, y.sampled_states) and np.array_equal(x.end_state, y.end_state)
+            assert kp.ValidityChecker(env, model, 0.05).trajectory_valid(a, start=env.start)
