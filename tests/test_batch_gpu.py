@@ -201,3 +201,19 @@ def test_full_size_outcomes_match_reference_golden(kp, name, model_name, scene, 
     band = 3.0 * np.sqrt(max(p * (1 - p), 0.01) * len(seeds)) + 1
     assert abs(int(r32.solved.sum()) - int(ref_solved.sum())) <= band, (int(r32.solved.sum()), int(ref_solved.sum()))
     assert not r32.rejected.any()                             # refused solutions were re-planned in float64
+
+
+def test_race_between_two_processes(kp):
+    """The OR-parallel race end to end with two ranks (torchrun, gloo rendezvous) sharing this GPU: the stop words
+    travel as CUDA IPC handles, the winner's kernel stores into the peer's word, the loser stops at its next
+    iteration boundary.  On a multi-GPU box the same store crosses NVLink (tools/race2.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KPX_RACE_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29533", os.path.join(root, "tools", "race2.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "race ok" in out.stdout, out.stdout[-2000:]
