@@ -196,9 +196,10 @@ int kpx_trajectory(int32_t model_id, int32_t n, int32_t nu, int64_t n_seg, const
 int kpx_trajectory_valid(const kpx_problem *prob, int64_t n_seg, const double *sampled, const int64_t *seg_offset,
                          const double *goal4, double res, int32_t *ok, int32_t *fail_code);
 int kpx_plan_trace(kpx_plan *p, int32_t max_records, kpx_trace *out, int32_t *n_records);
-/* the last iteration's per-item results in Batch layout + keep flag and parent slot (debug/parity) */
+/* the last iteration's per-item results in Batch layout + keep flag, parent slot and the kernel's own goal test
+ * of the end state (debug/parity; any output may be NULL) */
 int kpx_plan_items(kpx_plan *p, int64_t max_items, int64_t *n_items, uint8_t *valid, int64_t *region,
-                   int64_t *sub, double *end, uint8_t *keep, int64_t *parent_slot);
+                   int64_t *sub, double *end, uint8_t *keep, int64_t *parent_slot, uint8_t *goal_hit);
 /* restore a tree + region state produced elsewhere (checkpoint/resume; parity tests load oracle states) */
 int kpx_plan_load(kpx_plan *p, uint64_t seed, const double *goal4, int32_t iteration, int64_t rows,
                   const double *states, const int64_t *parent, const double *control, const double *dt,

@@ -5,6 +5,7 @@ Run in the build container (needs /root/reference; uses the reference's compiled
 kernel from oracle/_ref when built, else its Python backend):
 
     python oracle/make_golden.py small      # seconds: rng, scenes, batches, plan digests
+    python oracle/make_golden.py stacked    # ~a minute: stacked integrators (12D/24D) through the Python backend
     python oracle/make_golden.py outcomes   # minutes: full-size solves, seeds 0..N-1
 
 Outputs go to tests/golden/.  Nothing here imports the product package: every
@@ -187,6 +188,75 @@ def gen_checker(K):
     json.dump(out, open(os.path.join(GOLD, "checker.json"), "w"))
 
 
+def stacked_reference_model(K, blocks):
+    """BASELINE.json config 4 as the REFERENCE sees it: `blocks` stacked 3-D double integrators as a
+    custom DynamicsModel with kernel_id=None, which the reference runs through its Python backend (_purepy.py).
+    Built from the reference's own dataclass; nothing of the product package is involved."""
+    from kinopax.dynamics import DynamicsModel
+    n = 6 * blocks
+
+    def f(x, u, out):
+        for b in range(blocks):
+            out[6 * b:6 * b + 3] = x[6 * b + 3:6 * b + 6]
+            out[6 * b + 3:6 * b + 6] = u[3 * b:3 * b + 3]
+
+    lo = np.tile(np.array([0.0] * 3 + [-5.0] * 3), blocks)
+    hi = np.tile(np.array([10.0] * 3 + [5.0] * 3), blocks)
+    lo[:3] = np.nan
+    hi[:3] = np.nan
+    return DynamicsModel(name=f"di{n}", n=n, control_dim=3 * blocks, control_lo=np.full(3 * blocks, -2.0),
+                         control_hi=np.full(3 * blocks, 2.0), nonposition_lo=lo, nonposition_hi=hi, deriv_fn=f,
+                         wrap_dims=(), dim_kinds=np.tile(np.array([0, 0, 0, 1, 1, 1]), blocks), kernel_id=None,
+                         default_t_e=200_000, default_cells_per_dim={1: 4, 2: 3}.get(blocks, 1), default_t_prop=1.0)
+
+
+def stacked_reference_env(K, model):
+    """The di6 Trees scene with block 1 at the scene's start and the other blocks at the centre of their box, at rest."""
+    base = K.gen_environment("forest", "di6", seed=0)
+    start = np.tile(np.array([5.0, 5.0, 5.0, 0.0, 0.0, 0.0]), model.n // 6)
+    start[:3] = base.start[:3]
+    return K.Environment(name=f"forest-{model.name}", workspace_lo=base.workspace_lo, workspace_hi=base.workspace_hi,
+                         obstacles_min=base.obstacles_min, obstacles_max=base.obstacles_max, start=start, goal=base.goal)
+
+
+STACKED_CASES = [(2, 1200, 3, 7), (4, 900, 5, 6)]      # (blocks, t_e, seed, iterations)
+
+
+def gen_stacked(K):
+    """Pins oracle model id 3 (stacked integrators, 12D and 24D) to the reference's Python backend: per-iteration
+    digests of the tree, the counters and the estimates, plus the last iteration's whole Batch."""
+    from kinopax.planner import TAG_EXPAND, TAG_OPEN, KinoPax, compute_branching_factor
+    out = []
+    for blocks, t_e, seed, n_iter in STACKED_CASES:
+        model = stacked_reference_model(K, blocks)
+        env = stacked_reference_env(K, model)
+        cfg = _cfg(K, model, t_e, seed)
+        eng = KinoPax(cfg, env, model)
+        assert eng.backend.name == "python", eng.backend.name
+        iters = []
+        t0 = time.perf_counter()
+        for _ in range(n_iter):
+            eng.iteration += 1
+            e_slots = eng.arena.slots_with_tag(TAG_EXPAND)
+            lam = compute_branching_factor(cfg.t_e, eng.arena.size, len(e_slots), cfg.lambda_max)
+            batch = eng.backend.propagate_batch(eng.ctx, eng.arena.states, e_slots, lam, eng.iteration)
+            staged = eng.propagate_pass(lam)
+            eng.update_estimates_pass()
+            slot, exhausted, appended = eng.update_node_sets_pass(staged)
+            rec = {"iteration": eng.iteration, "branching": lam, "ve_size": int(len(e_slots)),
+                   "vo_size": int(len(eng.arena.slots_with_tag(TAG_OPEN))), "attempted": staged.attempted,
+                   "valid": staged.valid_count, "staged": len(staged), "appended": appended,
+                   "tree_size": eng.arena.size,
+                   "batch": _digest(batch.valid, batch.region, batch.sub, batch.end, batch.control, batch.dt, batch.accept_u)}
+            rec.update(_step_digest(eng))
+            iters.append(rec)
+            if slot is not None or exhausted:
+                break
+        out.append({"blocks": blocks, "t_e": t_e, "seed": seed, "cells": model.default_cells_per_dim, "iterations": iters})
+        print("stacked", model.name, "iters", len(iters), "size", eng.arena.size, f"{time.perf_counter() - t0:.1f} s")
+    json.dump(out, open(os.path.join(GOLD, "plans_stacked.json"), "w"), indent=1)
+
+
 # ------------------------------------------------------------------ full-size outcomes
 
 CONFIGS = {
@@ -246,6 +316,8 @@ def main():
         gen_batches(K)
         gen_plans(K)
         gen_checker(K)
+    elif what == "stacked":
+        gen_stacked(K)
     elif what == "outcomes":
         names = sys.argv[2].split(",") if len(sys.argv) > 2 else ["di6_forest"]
         n_seeds = int(sys.argv[3]) if len(sys.argv) > 3 else 100

@@ -105,6 +105,8 @@ def lib():
         L.kpo_plan_destroy.argtypes = [C.POINTER(Plan)]
         L.kpo_plan_step.restype = C.c_int
         L.kpo_plan_step.argtypes = [C.POINTER(Plan), C.c_int]
+        L.kpo_plan_step_given.restype = C.c_int
+        L.kpo_plan_step_given.argtypes = [C.POINTER(Plan), C.c_int, C.c_int64, _P, _P, _P, _P, _P]
         L.kpo_plan_solve.restype = C.c_int
         L.kpo_plan_solve.argtypes = [C.POINTER(Plan), C.c_double, C.c_int64, C.POINTER(C.c_double)]
         L.kpo_plan_chain.restype = C.c_int64
@@ -229,6 +231,20 @@ class OraclePlan:
 
     def step(self, lam_override=0) -> int:
         return self._L.kpo_plan_step(self._p, int(lam_override))
+
+    def step_given(self, valid, region, sub, end, goal_hit=None, lam_override=0) -> int:
+        """One iteration on a supplied Batch (another integrator's verdicts / cells / end states): the
+        bookkeeping of planner.py:185-265 alone.  Raises if the item count differs from this plan's |V_E| x lambda."""
+        valid = np.ascontiguousarray(valid, dtype=np.uint8)
+        region = np.ascontiguousarray(region, dtype=np.int64)
+        sub = np.ascontiguousarray(sub, dtype=np.int64)
+        end = _f64(end)
+        goal = None if goal_hit is None else np.ascontiguousarray(goal_hit, dtype=np.uint8)
+        st = self._L.kpo_plan_step_given(self._p, int(lam_override), len(valid), _ptr(valid), _ptr(region), _ptr(sub),
+                                         _ptr(end), None if goal is None else _ptr(goal))
+        if st < 0:
+            raise ValueError("supplied batch does not match this plan's item count")
+        return st
 
     def solve(self, t_max=60.0, max_iters=0):
         el = C.c_double(0.0)

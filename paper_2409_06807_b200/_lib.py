@@ -95,7 +95,7 @@ _SIGNATURES = {
     "kpx_trajectory_valid": (C.c_int, [C.POINTER(Problem), C.c_int64, _vp, _vp, _vp, C.c_double,
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kpx_plan_trace": (C.c_int, [_vp, C.c_int32, _vp, C.POINTER(C.c_int32)]),
-    "kpx_plan_items": (C.c_int, [_vp, C.c_int64, C.POINTER(C.c_int64), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "kpx_plan_items": (C.c_int, [_vp, C.c_int64, C.POINTER(C.c_int64), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kpx_plan_load": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int32, C.c_int64] + [_vp] * 13),
     "kpx_batch_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                    C.POINTER(_vp)]),

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -86,6 +87,13 @@ int upload_obstacles(const kpx_problem& pr, int precision, int n_obs, const doub
     return KPX_OK;
 }
 
+// a pair of timing events that is destroyed on every return path
+struct EventPair {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaError_t create() { cudaError_t e = cudaEventCreate(&e0); return e != cudaSuccess ? e : cudaEventCreate(&e1); }
+    ~EventPair() { if (e0) cudaEventDestroy(e0); if (e1) cudaEventDestroy(e1); }
+};
+
 struct Carver {
     size_t off = 0;
     size_t take(size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; }
@@ -98,6 +106,7 @@ struct kpx_batch {
     std::vector<double> obs_min, obs_max;
     int precision = KPX_F64, n_teams = 1, team_ctas = 1, device = 0;
     int max_chunks = 0, max_trace = 4096, max_chain = KPX_MAX_CHAIN;
+    int obs_cap = 0;                   // obstacles the device buffers (and the shared-memory scene) were sized for
     bool cooperative = false, latency = false;
     size_t rs = 8, smem = 0;
     int cap = 0, cap_pad = 0, regions = 0, subs = 0, claim_shift = 30;
@@ -165,7 +174,10 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     for (int d = 0; d < prob->grid_n; ++d) regions *= prob->grid_cells[d];
     b.regions = (int)regions;
     b.subs = prob->subcells * prob->subcells * prob->subcells;
-    b.smem = scene_smem_bytes(prob->n_obs, b.rs) + align_up((size_t)(b.max_chunks + 1) * sizeof(int), 16);
+    // after the scene: one int array shared by the chunk prefixes (max_chunks + 1) and the block prefix of the
+    // estimate list (one entry per 1024 regions + 1)
+    const size_t n_blocks = ((size_t)b.regions + 1023) / 1024;
+    b.smem = scene_smem_bytes(prob->n_obs, b.rs) + align_up((std::max((size_t)b.max_chunks, n_blocks) + 2) * sizeof(int), 16);
     if (b.smem > 200 * 1024) return fail(KPX_E_LIMIT, "t_e / obstacle count need more shared memory than one SM has");
 
     cudaDeviceProp dp;
@@ -190,7 +202,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     const size_t cp = (size_t)b.cap_pad, R = (size_t)b.regions, pairs = R * (size_t)b.subs;
     Carver c;
     struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, bits, dregions, it_end,
-                        it_code, it_rank, it_parent, it_bin, order, pos_of, bin_cursor, e_local, cnt_e, cnt_k, partial, bar, ctl, trace, ch_start, ch_ctrl,
+                        it_code, it_rank, it_parent, it_bin, order, pos_of, bin_cursor, e_local, cnt_e, cnt_k, est_ids, leaf_sum, bar, ctl, trace, ch_start, ch_ctrl,
                         ch_dt, ch_slot, ch_end, packet; } o;
     o.states = c.take(b.rs * n * cp); o.control = c.take(b.rs * nu * cp); o.dt = c.take(b.rs * cp);
     o.parent = c.take(4 * cp); o.region = c.take(4 * cp); o.tag = c.take(cp);
@@ -203,7 +215,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     o.it_end = c.take(b.rs * n * cp); o.it_code = c.take(4 * cp); o.it_rank = c.take(4 * cp); o.it_parent = c.take(4 * cp);
     o.it_bin = c.take(cp); o.order = c.take(4 * cp); o.pos_of = c.take(4 * cp); o.bin_cursor = c.take(4 * (size_t)kBins);
     o.e_local = c.take(4 * cp); o.cnt_e = c.take(4 * (size_t)b.max_chunks); o.cnt_k = c.take(4 * (size_t)b.max_chunks);
-    o.partial = c.take(8 * (size_t)team_ctas); o.bar = c.take(256); o.ctl = c.take(sizeof(Ctl));
+    o.est_ids = c.take(4 * (R + 32)); o.leaf_sum = c.take(8 * (R / 64 + 2)); o.bar = c.take(256); o.ctl = c.take(sizeof(Ctl));
     o.trace = c.take(sizeof(kpx_trace) * (size_t)b.max_trace);
     o.ch_start = c.take(8 * (size_t)b.max_chain * n); o.ch_ctrl = c.take(8 * (size_t)b.max_chain * nu);
     o.ch_dt = c.take(8 * (size_t)b.max_chain); o.ch_slot = c.take(8 * (size_t)b.max_chain); o.ch_end = c.take(8 * n);
@@ -227,7 +239,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         w.it_end = s + o.it_end; w.it_code = (uint32_t*)(s + o.it_code); w.it_rank = (int*)(s + o.it_rank);
         w.it_parent = (int*)(s + o.it_parent); w.e_local = (int*)(s + o.e_local);
         w.it_bin = (uint8_t*)(s + o.it_bin); w.order = (int*)(s + o.order); w.pos_of = (int*)(s + o.pos_of); w.bin_cursor = (unsigned int*)(s + o.bin_cursor);
-        w.cnt_expand = (int*)(s + o.cnt_e); w.cnt_keep = (int*)(s + o.cnt_k); w.partial = (double*)(s + o.partial);
+        w.cnt_expand = (int*)(s + o.cnt_e); w.cnt_keep = (int*)(s + o.cnt_k); w.est_ids = (int*)(s + o.est_ids); w.leaf_sum = (double*)(s + o.leaf_sum);
         w.bar = (unsigned int*)(s + o.bar); w.ctl = (Ctl*)(s + o.ctl); w.trace = (kpx_trace*)(s + o.trace);
         w.chain_start = (double*)(s + o.ch_start); w.chain_control = (double*)(s + o.ch_ctrl);
         w.chain_dt = (double*)(s + o.ch_dt); w.chain_slot = (long long*)(s + o.ch_slot);
@@ -244,6 +256,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     }
     CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
     CU(cudaMemcpy(b.ws_dev, b.ws_host.data(), sizeof(Workspace) * (size_t)n_teams, cudaMemcpyHostToDevice));
+    b.obs_cap = prob->n_obs;
     CU(cudaMalloc(&b.obs_dev, 8 * (size_t)std::max(prob->n_obs, 1) * b.rs));
     CU(cudaMalloc(&b.occ_dev, 2 * sizeof(uint32_t) * (size_t)kOccCells));
     rc = upload_obstacles(b.prob, precision, prob->n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
@@ -350,8 +363,9 @@ int measure_fma(int sms, double ms_target, double* tflops) {
     T* d = nullptr;
     const int blocks = sms * 8, threads = 256;
     CU(cudaMalloc(&d, sizeof(T) * (size_t)blocks * threads));
-    cudaEvent_t e0, e1;
-    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
+    EventPair ev;
+    CU(ev.create());
+    const cudaEvent_t e0 = ev.e0, e1 = ev.e1;
     int iters = 2000;
     double best = 0.0;
     for (int rep = 0; rep < 6; ++rep) {
@@ -365,7 +379,7 @@ int measure_fma(int sms, double ms_target, double* tflops) {
         if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
         if (ms < ms_target) iters = (int)std::min(2.0e6, iters * std::max(1.5, ms_target / std::max(ms, 1e-3f)));
     }
-    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaFree(d);
+    cudaFree(d);
     *tflops = best;
     return KPX_OK;
 }
@@ -483,8 +497,9 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
     L.o_substeps = (long long*)(slab + o_ss); L.o_points = (long long*)(slab + o_pp);
     L.grid = (int)std::min<int64_t>((items + kBlock - 1) / kBlock, 148 * 16);
     L.smem = scene_smem_bytes(prob->n_obs, rs);
-    cudaEvent_t e0, e1;
-    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
+    EventPair ev;
+    CU(ev.create());
+    const cudaEvent_t e0 = ev.e0, e1 = ev.e1;
     CU(cudaEventRecord(e0, st));
     cudaError_t e = precision == KPX_F64 ? launch_batch_f64(L, st) : launch_batch_f32(L, st);
     if (e != cudaSuccess) return fail(e == cudaErrorInvalidValue ? KPX_E_ARG : KPX_E_CUDA,
@@ -502,7 +517,6 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
     if (o_points) CU(cudaMemcpyAsync(o_points, slab + o_pp, 8 * (size_t)items, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (o_kernel_ms) { float ms = 0; CU(cudaEventElapsedTime(&ms, e0, e1)); *o_kernel_ms = ms; }
-    cudaEventDestroy(e0); cudaEventDestroy(e1);
     return KPX_OK;
 }
 
@@ -551,12 +565,14 @@ int kpx_plan_set_epoch(kpx_plan* p, uint32_t epoch_used) {
 int kpx_plan_set_obstacles(kpx_plan* p, int32_t n_obs, const double* omin, const double* omax) {
     if (!p) return fail(KPX_E_ARG, "null plan");
     kpx_batch& b = p->b;
-    if (n_obs < 0 || n_obs > std::max<int>((int)b.obs_min.size() / 3, 1) || (n_obs && (!omin || !omax)))
-        return fail(KPX_E_ARG, "obstacle count exceeds the capacity the plan was created with");
+    if (n_obs < 0 || (n_obs && (!omin || !omax))) return fail(KPX_E_ARG, "bad obstacle arguments");
+    if (n_obs > b.obs_cap)
+        return fail(KPX_E_ARG, "obstacle count %d exceeds the capacity (%d) the plan was created with", n_obs, b.obs_cap);
     CU(cudaSetDevice(b.device));
     b.prob.n_obs = n_obs;
-    std::copy(omin, omin + 3 * (size_t)n_obs, b.obs_min.begin());
-    std::copy(omax, omax + 3 * (size_t)n_obs, b.obs_max.begin());
+    b.obs_min.assign(omin, omin + 3 * (size_t)n_obs);
+    b.obs_max.assign(omax, omax + 3 * (size_t)n_obs);
+    b.prob.obs_min = b.obs_min.data(); b.prob.obs_max = b.obs_max.data();
     cudaFree(b.boxes64_dev); b.boxes64_dev = nullptr;      // rebuilt on the next validation
     return upload_obstacles(b.prob, b.precision, n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
 }
@@ -582,6 +598,8 @@ int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_overr
         L.peer_flags = b.peers_dev; L.n_peers = n_peers;
     }
     const unsigned long long l0 = b.launches;
+    if (!b.fresh)   // a continued run starts with a clear stop word (its status word says why the last launch ended)
+        CU(cudaMemsetAsync((char*)b.ws_host[0].ctl + offsetof(Ctl, stop), 0, sizeof(int), st));
     if (b.fresh) {
         *b.q_pinned = b.q_host;
         CU(cudaMemcpyAsync(b.q_dev, b.q_pinned, sizeof(QueryIn), cudaMemcpyHostToDevice, st));
@@ -596,7 +614,7 @@ int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_overr
     const Ctl& c = b.pk_host->ctl;
     out->status = c.status; out->iterations = c.iteration; out->tree_size = c.size;
     out->solution_slot = c.solution_slot; out->chain_len = c.chain_len;
-    out->device_ms = (double)(c.t_end - c.t_reset_done) * 1e-6;
+    out->device_ms = (double)c.elapsed_ns * 1e-6;      // run clock: summed over the launches since the reset
     out->reset_ms = (double)(c.t_reset_done - c.t_begin) * 1e-6;
     out->items = c.sum_items; out->substeps = c.sum_substeps; out->points = c.sum_points;
     out->boxsteps = c.sum_boxsteps;
@@ -714,7 +732,7 @@ int kpx_plan_trace(kpx_plan* p, int32_t max_records, kpx_trace* out, int32_t* n_
 }
 
 int kpx_plan_items(kpx_plan* p, int64_t max_items, int64_t* n_items, uint8_t* valid, int64_t* region, int64_t* sub,
-                   double* end, uint8_t* keep, int64_t* parent_slot) {
+                   double* end, uint8_t* keep, int64_t* parent_slot, uint8_t* goal_hit) {
     if (!p || !n_items) return fail(KPX_E_ARG, "null argument");
     kpx_batch& b = p->b;
     CU(cudaSetDevice(b.device));
@@ -742,6 +760,7 @@ int kpx_plan_items(kpx_plan* p, int64_t max_items, int64_t* n_items, uint8_t* va
         if (region) region[i] = v ? (int64_t)(pair / (uint32_t)b.subs) : -1;
         if (sub) sub[i] = v ? (int64_t)(pair % (uint32_t)b.subs) : 0;
         if (keep) keep[i] = v && rank[i] >= 0;
+        if (goal_hit) goal_hit[i] = v && (code[ip] & kItemGoalBit) != 0;
         if (parent_slot) parent_slot[i] = par[i];
         if (end) for (int d = 0; d < b.prob.n; ++d) end[i * b.prob.n + d] = v ? e[(size_t)ip * b.prob.n + d] : 0.0;
     }
@@ -1092,8 +1111,9 @@ int kpx_batch_run(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const
     const int want = chain_start && chain_control && chain_dt;
     int rc = kpx_batch_upload(bp, n_queries, seeds, starts, goals, want, stream);
     if (rc) return rc;
-    cudaEvent_t e0, e1;
-    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1));
+    EventPair ev;
+    CU(ev.create());
+    const cudaEvent_t e0 = ev.e0, e1 = ev.e1;
     CU(cudaEventRecord(e0, st));
     rc = kpx_batch_launch(bp, t_max, stream);
     if (rc) return rc;
@@ -1102,7 +1122,6 @@ int kpx_batch_run(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const
     rc = kpx_batch_download(bp, results, chain_start, chain_control, chain_dt, stream);
     if (rc) return rc;
     if (o_kernel_ms) { float ms = 0; CU(cudaEventElapsedTime(&ms, e0, e1)); *o_kernel_ms = ms; }
-    cudaEventDestroy(e0); cudaEventDestroy(e1);
     return KPX_OK;
 }
 

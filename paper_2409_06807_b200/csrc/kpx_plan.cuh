@@ -73,6 +73,7 @@ struct Ctl {                      // one per workspace, global memory
     // persistent run state (valid between launches: stepped runs, resume)
     int size, iteration, status, solution_slot;
     double total_prev;            // sum of scores of the last estimate pass
+    double total_pub;             // exchange word for the total when one CTA combines it for the team
     int ve;                       // |V_E| for the next iteration
     int lam_last;
     // per-iteration exchange words
@@ -95,6 +96,10 @@ struct Ctl {                      // one per workspace, global memory
     // reset of the claim table and the region arrays (fresh state loaded from the host)
     int epoch_valid;
     unsigned int epoch_used;
+    // run clock: device time the loop has been running over all launches since the reset (stepped / resumed runs
+    // do not count the host's idle time between launches; planner.py:282 compares against t_max)
+    unsigned long long elapsed_ns;
+    int n_est;                    // regions in Workspace::est_ids (those the next estimate pass covers)
 };
 
 constexpr int kBins = 64;          // substep-count bins of the S0 counting sort (S >= 63 share the last bin)
@@ -114,6 +119,7 @@ struct RunState {                 // CTA-uniform state of the running query, sha
     unsigned long long t_start;   // keeper only
     // header of the current iteration
     int lam, items, n_sch_old, par, sorted;
+    int n_est;                    // available regions, i.e. entries of Workspace::est_ids, for this iteration's estimate pass
     uint32_t claim_tag;           // epoch of this query << claim_shift
     unsigned long long h0;
     unsigned long long tp[7];     // keeper only: phase boundary timestamps
@@ -143,7 +149,8 @@ struct Workspace {                // device pointers of one team's state
     unsigned int* bin_cursor;     // [kBins] per-bin fill cursor / histogram of the current iteration
     int *e_local;                 // [cap]  chunk-major compacted EXPAND slots
     int *cnt_expand, *cnt_keep;   // [max_chunks]
-    double* partial;              // [team_ctas]
+    int* est_ids;                 // [R] available regions in ascending order: the reference's avail_ids (decomposition.py:175)
+    double* leaf_sum;             // [R/64 + 2] leaf sums of the pairwise score total (see estimate_leaves)
     unsigned int* bar;            // {count, generation}
     Ctl* ctl;
     kpx_trace* trace;             // [max_trace]
@@ -280,6 +287,141 @@ __device__ __forceinline__ void count_outcome(int* __restrict__ n_valid, int* __
             atomicOr(touched_bits + (region >> 5), 1u << (region & 31));
         }
     }
+}
+
+
+// ---- estimate total in NumPy's pairwise order (decomposition.py:199: score[avail_ids].sum()) ---------------
+// np.sum over a contiguous float64 array of n elements is a fixed recursion: n > 128 splits at
+// n2 = n/2 - (n/2) % 8 into sum(a[0:n2]) + sum(a[n2:n]); a block of 8 <= n <= 128 elements keeps 8 strided
+// accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and then adds the n % 8 tail in order; n < 8 is a
+// plain left-to-right sum.  Every node of n > 128 elements has children of >= 64 elements, so the leaves are
+// 64..128 elements long and the compact indices 0, 64, 128, ... ("probes") each fall into one leaf, every leaf
+// containing one or two of them: the leaf that starts at compact index lo belongs to probe ceil(lo / 64).
+// The tree therefore needs no list: each probe finds its node by descending from the root (<= ~20 steps).
+__device__ __forceinline__ int pw_left(int n) { int n2 = n >> 1; return n2 - (n2 & 7); }
+// node of depth <= max_depth that contains compact index i: returns its depth, (*lo, *n) its range
+__device__ __forceinline__ int pw_descend(int na, int i, int max_depth, int* lo, int* n) {
+    int l = 0, m = na, d = 0;
+    while (m > 128 && d < max_depth) {
+        const int n2 = pw_left(m);
+        if (i < l + n2) m = n2; else { l += n2; m -= n2; }
+        ++d;
+    }
+    *lo = l; *n = m;
+    return d;
+}
+
+// S3: one warp per leaf computes the scores of its <= 128 regions (Eq. 3-4, decomposition.py:175-187), stores
+// them, and sums them in NumPy's order into leaf_sum[probe].  Leaves are spread over the team's warps.
+// `buf`: 128 doubles of shared memory per warp.
+template <class R>
+__device__ __forceinline__ void estimate_leaves(const Params<R>& P, const Workspace& W, const Team& T, int na, double* buf) {
+    const int lane = threadIdx.x & 31;
+    const int n_probe = (na + 63) >> 6;
+    const int team_warps = T.ctas * kWarps;
+    for (int k = T.rank * kWarps + (threadIdx.x >> 5); k < n_probe; k += team_warps) {
+        int lo, n;
+        pw_descend(na, k << 6, 0x7fffffff, &lo, &n);
+        if (k != ((lo + 63) >> 6)) continue;                 // the leaf's other probe (warp-uniform)
+        for (int e = lane; e < n; e += 32) {
+            const int r = __ldcg(W.est_ids + lo + e);
+            const double nv = (double)__ldcg(W.n_valid + r), ni = (double)__ldcg(W.n_invalid + r);
+            // rn intrinsics: never contracted to FMA, so both precision builds agree bit for bit
+            const double dn = __dadd_rn(P.delta, nv);
+            const double fv = __ddiv_rn(__dmul_rn(dn, P.vol), __dadd_rn(dn, ni));
+            const double tt = __dadd_rn(nv, ni);
+            const double f2 = __dmul_rn(fv, fv);
+            const double sc = __ddiv_rn(__dmul_rn(f2, f2), __dmul_rn(__dadd_rn(1.0, (double)__ldcg(W.cov + r)),
+                                                                      __dadd_rn(1.0, __dmul_rn(tt, tt))));
+            __stcg(W.score + r, sc);
+            buf[e] = sc;
+        }
+        __syncwarp();
+        double res = 0.0;
+        if (n < 8) {
+            if (lane == 0) for (int i = 0; i < n; ++i) res = __dadd_rn(res, buf[i]);
+        } else {
+            const int body = n - (n & 7);
+            double acc = buf[lane & 7];
+            for (int i = 8 + (lane & 7); i < body; i += 8) acc = __dadd_rn(acc, buf[i]);
+            acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));       // r0+r1 | r2+r3 | r4+r5 | r6+r7
+            acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));       // (r0+r1)+(r2+r3) | (r4+r5)+(r6+r7)
+            acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+            res = acc;
+            if (lane == 0) for (int i = body; i < n; ++i) res = __dadd_rn(res, buf[i]);
+        }
+        if (lane == 0) __stcg(W.leaf_sum + k, res);
+        __syncwarp();
+    }
+}
+
+// S4: the tree above the leaves, level by level from the deepest, in place: the result of the node that
+// starts at compact index lo lives in slot ceil(lo / 64) (the slot of its leftmost leaf).  GLOBAL = false: `v` is
+// n_probe doubles of shared memory private to the CTA, filled from leaf_sum here (every CTA of a team combines
+// for itself); GLOBAL = true: one CTA combines in leaf_sum itself.  Returns the total to every calling thread.
+template <bool GLOBAL>
+__device__ __forceinline__ double combine_leaves(double* leaf_sum, int na, double* v) {
+    if (na <= 0) return 0.0;
+    const int n_probe = (na + 63) >> 6;
+    if (GLOBAL) v = leaf_sum;
+    else for (int k = threadIdx.x; k < n_probe; k += kBlock) v[k] = __ldcg(leaf_sum + k);   // non-owner slots are never read
+    int depth = 0;
+    for (int m = na; m > 128; m -= pw_left(m)) ++depth;      // the right child is the larger one
+    __syncthreads();
+    for (int d = depth - 1; d >= 0; --d) {
+        for (int k = threadIdx.x; k < n_probe; k += kBlock) {
+            int lo, n;
+            const int dd = pw_descend(na, k << 6, d, &lo, &n);
+            if (dd == d && n > 128 && k == ((lo + 63) >> 6)) {
+                const int kr = (lo + pw_left(n) + 63) >> 6;
+                if (GLOBAL) __stcg(v + k, __dadd_rn(__ldcg(v + k), __ldcg(v + kr)));
+                else v[k] = __dadd_rn(v[k], v[kr]);
+            }
+        }
+        __syncthreads();
+    }
+    const double total = GLOBAL ? __ldcg(v) : v[0];
+    __syncthreads();
+    return total;
+}
+constexpr int kMaxProbes = 2048;   // leaf slots a CTA can combine in shared memory: up to 131 072 available regions
+
+// Ascending list of the available regions (= the regions the NEXT estimate pass covers) out of the availability
+// bitmap: every CTA counts the 1024-region blocks into shared memory (s_pre[n_blocks + 1], exclusive prefix),
+// then the team's warps expand the blocks.  Readers are separated from this by at least one team barrier.
+// Returns the number of available regions (the same value in every thread of the team).
+__device__ __forceinline__ int build_est_list(const Workspace& W, const Team& T, int n_regions, int* s_pre, int* s_w) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int n_words = (n_regions + 31) >> 5, n_blocks = (n_words + 31) >> 5;
+    __syncthreads();
+    for (int b = wid; b < n_blocks; b += kWarps) {
+        const int wi = b * 32 + lane;
+        const int c = __reduce_add_sync(0xffffffffu, wi < n_words ? __popc(__ldcg(W.avail_bits + wi)) : 0);
+        if (lane == 0) s_pre[b] = c;
+    }
+    __syncthreads();
+    int carry = 0;
+    for (int base = 0; base < n_blocks; base += kBlock) {
+        const int i = base + threadIdx.x;
+        const int v = i < n_blocks ? s_pre[i] : 0;
+        int tot;
+        const int ex = block_excl_scan(v, s_w, &tot);
+        if (i < n_blocks) s_pre[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) s_pre[n_blocks] = carry;
+    __syncthreads();
+    const int team_warps = T.ctas * kWarps;
+    for (int b = T.rank * kWarps + wid; b < n_blocks; b += team_warps) {
+        if (s_pre[b + 1] == s_pre[b]) continue;
+        const int wi = b * 32 + lane;
+        uint32_t bits = wi < n_words ? __ldcg(W.avail_bits + wi) : 0u;
+        const int c = __popc(bits);
+        int at = s_pre[b] + warp_incl_scan(c) - c;
+        while (bits) { __stcg(W.est_ids + at++, wi * 32 + __ffs(bits) - 1); bits &= bits - 1; }
+    }
+    __syncthreads();
+    return carry;
 }
 
 // ---- S1: propagation ---------------------------------------------------------------------------------
@@ -759,49 +901,29 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                 }
             }
         }
-        {   // estimate sweep 1 (decomposition.py:175-187) over regions available before this append
-            double part = 0.0;
-            // walk the availability bitmap: word order then bit order, so each thread's partial sum has a fixed
-            // order (deterministic total) while only available regions are ever touched
-            // Few regions per thread: plain dense sweep (most parallel).  Many: walk the availability bitmap in
-            // word order then bit order, touching only available regions.  Either way every thread's partial sum
-            // has a fixed order, so the total is deterministic for a given team size.
-            const bool dense = (long long)RG <= 32 * tthreads;
-            const long long n_outer = dense ? (long long)RG : (long long)((RG + 31) >> 5);
-            for (long long wi = ttid; wi < n_outer; wi += tthreads) {
-                uint32_t bits = dense ? 1u : __ldcg(W.avail_bits + wi);
-                while (bits) {
-                    const int r = dense ? (int)wi : (int)wi * 32 + __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    const int a = __ldcg(W.avail_it + r);
-                    if (a != 0 && a <= it) {
-                        const double nv = (double)__ldcg(W.n_valid + r), ni = (double)__ldcg(W.n_invalid + r);
-                        // rn intrinsics: never contracted to FMA, so both precision builds agree bit for bit
-                        const double dn = __dadd_rn(P.delta, nv);
-                        const double fv = __ddiv_rn(__dmul_rn(dn, P.vol), __dadd_rn(dn, ni));
-                        const double tt = __dadd_rn(nv, ni);
-                        const double f2 = __dmul_rn(fv, fv);
-                        const double sc = __ddiv_rn(__dmul_rn(f2, f2),
-                                                    __dmul_rn(__dadd_rn(1.0, (double)__ldcg(W.cov + r)),
-                                                              __dadd_rn(1.0, __dmul_rn(tt, tt))));
-                        __stcg(W.score + r, sc);
-                        part += sc;
-                    }
-                }
-            }
-            part = block_sum_f64(part, s_d);
-            if (tid == 0) __stcg(W.partial + T.rank, part);
-        }
+        // estimate pass (decomposition.py:175-203) over the regions available before this append (est_ids, built in
+        // the previous iteration's epilogue): scores and the leaf sums of NumPy's pairwise total
+        estimate_leaves<R>(P, W, T, RS.n_est, (double*)&Scene<R>::coop());
         const int new_size = size + n_app;
         team_sync(T);
         if (keeper) RS.tp[4] = gtimer();
 
         // ================================================================= S4
+        // sum of the scores in NumPy's pairwise order (bit-identical to the reference's `total`, and the same for
+        // any team size); every CTA combines the leaf sums for itself
         double total;
         {
-            double v = 0.0;
-            for (int b = tid; b < T.ctas; b += kBlock) v += __ldcg(W.partial + b);
-            total = block_sum_f64(v, s_d);
+            const int na = RS.n_est;
+            if (((na + 63) >> 6) <= kMaxProbes) {
+                total = combine_leaves<false>(W.leaf_sum, na, (double*)(kpx_dyn_smem + Scene<R>::kCoop));
+            } else {            // more leaves than a CTA holds in shared memory: CTA 0 combines in place and publishes
+                if (T.rank == 0) {
+                    const double t = combine_leaves<true>(W.leaf_sum, na, nullptr);
+                    if (tid == 0) __stcg(&ctl->total_pub, t);
+                }
+                team_sync(T);
+                total = __ldcg(&ctl->total_pub);
+            }
         }
         {
             const int n_sch = (new_size + kChunk - 1) / kChunk;
@@ -874,6 +996,8 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
         if (keeper) RS.tp[5] = gtimer();
 
         // ================================================= epilogue of the iteration
+        // regions made available by this append join the estimate pass from the next iteration on (planner.py:246)
+        const int n_est_next = build_est_list(W, T, RG, s_prefix, s_w);
         int ve = scan_counts(W.cnt_expand, (new_size + kChunk - 1) / kChunk, s_prefix, s_w);
         if (ve == 0) {
             // rescue rule (planner.py:259-265): OPEN slot with max p_accept, lowest slot on ties
@@ -919,7 +1043,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
         }
         __syncthreads();                        // every thread is done with this iteration's state
         if (tid == 0) {
-            RS.size = new_size; RS.total_prev = total; RS.ve = ve;
+            RS.size = new_size; RS.total_prev = total; RS.ve = ve; RS.n_est = n_est_next;
             if (found) { RS.status = KPX_SOLVED; RS.solution_slot = new_size - 1; }              // planner.py:297-303
             else if (exhausted) RS.status = KPX_CAPACITY_EXHAUSTED;
         }
@@ -936,7 +1060,8 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
     if (keeper) {
         const int size = RS.size, it = RS.it, status = RS.status, solution_slot = RS.solution_slot;
         ctl->size = size; ctl->iteration = it; ctl->status = status; ctl->solution_slot = solution_slot;
-        ctl->total_prev = RS.total_prev; ctl->ve = RS.ve;
+        ctl->total_prev = RS.total_prev; ctl->ve = RS.ve; ctl->n_est = RS.n_est;
+        ctl->elapsed_ns = gtimer() - RS.t_start;
         int len = 0;
         if (status == KPX_SOLVED) {
             // parent chain (planner.py:325-336), written root-first
@@ -999,16 +1124,27 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
     {   // run state out of Ctl (valid between launches: stepped runs, resume)
         Ctl* const ctl = W.ctl;
         const int size = __ldcg(&ctl->size);
+        const int n_est = build_est_list(W, T, A.P.n_regions, s_prefix, s_w);   // fresh: the root's region
         const int ve = scan_counts(W.cnt_expand, (size + kChunk - 1) / kChunk, s_prefix, s_w);
+        // Run clock (planner.py:282): the time this loop has been running, summed over the launches since the
+        // reset, so a stepped / resumed run does not count the host's idle time.  A launch that continues a run
+        // which a time-out or a race peer stopped carries on (the caller asked for more); a run that has already
+        // used up t_max -- t_max = 0 on a fresh query included -- ends before its first iteration, as the
+        // reference's `while elapsed < t_max` does.  Every CTA of the team evaluates the same words.
+        const unsigned long long elapsed0 = A.resume ? __ldcg(&ctl->elapsed_ns) : 0ull;
+        int status = __ldcg(&ctl->status);
+        if (A.resume && (status == KPX_TIMEOUT || status == KPX_STOPPED)) status = KPX_RUNNING;
+        if (status == KPX_RUNNING && !((double)elapsed0 * 1e-9 < A.t_max_s)) status = KPX_TIMEOUT;
         if (threadIdx.x == 0) {
-            RS.size = size; RS.it = __ldcg(&ctl->iteration); RS.status = __ldcg(&ctl->status);
+            RS.size = size; RS.it = __ldcg(&ctl->iteration); RS.status = status;
             RS.solution_slot = __ldcg(&ctl->solution_slot); RS.total_prev = __ldcg(&ctl->total_prev);
-            RS.ve = ve; RS.iters = 0;
+            RS.ve = ve; RS.iters = 0; RS.n_est = n_est;
             RS.claim_tag = __ldcg(&ctl->epoch_used) << A.claim_shift;
             unsigned long long t_start = 0;     // run clock origin; only the keeper thread uses it
             if (T.rank == 0) {
-                t_start = __ldcg(&ctl->t_reset_done);
-                if (t_start == 0) { t_start = gtimer(); ctl->t_reset_done = t_start; ctl->t_begin = t_start; }  // loaded state
+                t_start = gtimer() - elapsed0;
+                // (a resumed launch finds ctl->stop cleared by the host: kpx_plan_run)
+                if (A.resume && __ldcg(&ctl->t_reset_done) == 0) { ctl->t_reset_done = t_start; ctl->t_begin = t_start; }  // loaded state
             }
             RS.t_start = t_start;
         }

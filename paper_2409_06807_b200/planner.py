@@ -202,10 +202,12 @@ class KinoPax:
         cap, n = self.cfg.t_e, self.model.n
         cnt = C.c_int64(0)
         out = {"valid": np.zeros(cap, np.uint8), "region": np.zeros(cap, np.int64), "sub": np.zeros(cap, np.int64),
-               "end": np.zeros((cap, n)), "keep": np.zeros(cap, np.uint8), "parent_slot": np.zeros(cap, np.int64)}
+               "end": np.zeros((cap, n)), "keep": np.zeros(cap, np.uint8), "parent_slot": np.zeros(cap, np.int64),
+               "goal_hit": np.zeros(cap, np.uint8)}
         _lib.check(self._lib.kpx_plan_items(self._handle, cap, C.byref(cnt), _lib.ptr(out["valid"]),
                                             _lib.ptr(out["region"]), _lib.ptr(out["sub"]), _lib.ptr(out["end"]),
-                                            _lib.ptr(out["keep"]), _lib.ptr(out["parent_slot"])), "kpx_plan_items")
+                                            _lib.ptr(out["keep"]), _lib.ptr(out["parent_slot"]),
+                                            _lib.ptr(out["goal_hit"])), "kpx_plan_items")
         return {k: v[: cnt.value] for k, v in out.items()}
 
     def traces(self) -> list:

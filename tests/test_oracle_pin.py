@@ -121,6 +121,72 @@ def test_checker_known_answers(kp, orc):
             assert kp.ValidityChecker(env, model, float(res)).trajectory_valid(segs, start=env.start) == verdict
 
 
+def _stacked_problem(kp, blocks, t_e, seed):
+    model = kp.stacked_double_integrator(blocks)
+    base = kp.gen_environment("forest", "di6", seed=0)
+    start = np.tile(np.array([5.0, 5.0, 5.0, 0.0, 0.0, 0.0]), blocks)
+    start[:3] = base.start[:3]
+    env = kp.Environment(f"forest-{model.name}", base.workspace_lo, base.workspace_hi, base.obstacles_min,
+                         base.obstacles_max, start, base.goal)
+    return kp.build_problem(small_cfg(kp, model, t_e=t_e, seed=seed), env, model)
+
+
+def test_stacked_integrators_match_reference_python_backend(kp, orc):
+    """BASELINE.json config 4: oracle model id 3 (stacked 3-D double integrators, 12D and 24D) against what the
+    reference's PYTHON backend produced for a custom DynamicsModel(kernel_id=None) -- SURVEY 8(d)'s oracle for
+    this configuration (fixture: oracle/make_golden.py stacked).  Every iteration: the whole Batch, the tree, the
+    counters and the estimates, bit for bit."""
+    for case in json.load(open(os.path.join(GOLDEN, "plans_stacked.json"))):
+        prob = _stacked_problem(kp, case["blocks"], case["t_e"], case["seed"])
+        assert prob.cfg.cells_per_dim == case["cells"]
+        op = orc.plan_from_problem(prob)
+        for rec in case["iterations"]:
+            op.step()
+            tr = op.trace()
+            for k in ("iteration", "branching", "ve_size", "vo_size", "attempted", "valid", "staged", "appended",
+                      "tree_size"):
+                assert tr[k] == rec[k], (case["blocks"], rec["iteration"], k)
+            b = op.last_batch()
+            assert _digest(b["valid"], b["region"], b["sub"], b["end"], b["control"], b["dt"], b["accept_u"]) == rec["batch"]
+            s, d = op.snapshot(), op.decomposition()
+            assert _digest(s["states"], s["parent"], s["control"], s["dt"], s["tag"], s["region"]) == rec["tree"]
+            assert _digest(d["n_valid"], d["n_invalid"], d["cov"], d["visited"], d["avail"]) == rec["counters"]
+            assert _digest(d["free_vol"], d["score"], d["p_accept"]) == rec["estimates"]
+
+
+def test_step_given_equals_step(kp, orc):
+    """The bookkeeping-only entry point (kpo_plan_step_given: passes 1b/2/3 on a supplied Batch) reproduces the full
+    step when it is handed the full step's own Batch -- with and without the supplied goal flags -- and refuses a
+    Batch of the wrong length."""
+    for model_name, scene, t_e, seed in (("di6", "forest", 6000, 1), ("quad12", "narrow", 8000, 3)):
+        a, prob = _oracle_for(kp, orc, model_name, scene, t_e, seed)
+        b, _ = _oracle_for(kp, orc, model_name, scene, t_e, seed)
+        c, _ = _oracle_for(kp, orc, model_name, scene, t_e, seed)
+        goal = np.asarray(prob.goal4)
+        with pytest.raises(ValueError):
+            b.step_given(np.zeros(3, np.uint8), np.zeros(3, np.int64), np.zeros(3, np.int64), np.zeros((3, prob.model.n)))
+        assert int(b.raw.iteration) == 0
+        for it in range(60):
+            st = a.step()
+            ba = a.last_batch()
+            hit = (np.sqrt(((ba["end"][:, :3] - goal[:3]) ** 2).sum(axis=1)) <= goal[3]).astype(np.uint8)
+            assert b.step_given(ba["valid"], ba["region"], ba["sub"], ba["end"]) == st
+            assert c.step_given(ba["valid"], ba["region"], ba["sub"], ba["end"], goal_hit=hit) == st
+            for o in (b, c):
+                sa, so = a.snapshot(), o.snapshot()
+                assert sa["size"] == so["size"]
+                for k in ("states", "parent", "control", "dt", "tag", "region"):
+                    assert np.array_equal(sa[k], so[k]), (it, k)
+                da, do = a.decomposition(), o.decomposition()
+                for k in da:
+                    assert np.array_equal(da[k], do[k]), (it, k)
+                assert np.array_equal(a.last_batch()["staged_idx"], o.last_batch()["staged_idx"])
+                assert a.trace() == o.trace()
+            if st != 4:
+                break
+        assert a.status == b.status == c.status and a.status in ("solved", "capacity_exhausted")
+
+
 def test_outcome_fixtures_are_consistent():
     """Full-size reference outcomes (100 seeds per config) that the GPU success-rate test compares against."""
     for name, min_solved in (("di6_forest", 100), ("dubins6_building", 100), ("quad12_narrow", 50),
@@ -168,6 +234,38 @@ def test_step_by_step_against_live_reference(kp, orc, model_name, scene, t_e, se
             assert np.array_equal(d[k], v), k
         if slot is not None or exhausted:
             break
+
+
+@pytest.mark.reference
+def test_stacked_integrators_against_live_reference_python_backend(kp, orc):
+    """Live form of the config-4 pin: the reference's Python backend (custom DynamicsModel, kernel_id=None) and the
+    oracle's model id 3 stepped side by side at 12D (full-state grid, cells 3) and 24D (cells 1)."""
+    K = _reference()
+    import make_golden
+    from kinopax.planner import TAG_EXPAND, KinoPax
+    for blocks, t_e, seed, n_iter in ((2, 500, 11, 5), (4, 400, 12, 4)):
+        rm = make_golden.stacked_reference_model(K, blocks)
+        eng = KinoPax(K.PlannerConfig(t_e=t_e, t_prop=rm.default_t_prop, cells_per_dim=rm.default_cells_per_dim, seed=seed),
+                      make_golden.stacked_reference_env(K, rm), rm)
+        assert eng.backend.name == "python"
+        op = orc.plan_from_problem(_stacked_problem(kp, blocks, t_e, seed))
+        for _ in range(n_iter):
+            eng.iteration += 1
+            ve = len(eng.arena.slots_with_tag(TAG_EXPAND))
+            staged = eng.propagate_pass(K.compute_branching_factor(t_e, eng.arena.size, ve, 32))
+            eng.update_estimates_pass()
+            slot, exhausted, _ = eng.update_node_sets_pass(staged)
+            op.step()
+            a, b = eng.arena.snapshot(), op.snapshot()
+            assert a["size"] == b["size"]
+            for k in ("states", "parent", "control", "dt", "tag", "region"):
+                assert np.array_equal(a[k], b[k]), k
+            d = op.decomposition()
+            for k, v in (("n_valid", eng.decomp.n_valid), ("n_invalid", eng.decomp.n_invalid), ("cov", eng.decomp.cov),
+                         ("visited", eng.decomp.visited), ("score", eng.decomp.score), ("p_accept", eng.decomp.p_accept)):
+                assert np.array_equal(d[k], v), k
+            if slot is not None or exhausted:
+                break
 
 
 @pytest.mark.reference
