@@ -120,6 +120,17 @@ int kpx_fma_peak(int device, double ms_target, double *tflops, double *tflops_f6
 int kpx_cull_thresholds(const kpx_problem *prob, int32_t precision, double *out4);
 int kpx_cull_tables(const kpx_problem *prob, int32_t precision, uint32_t *masks8192, double *lo3, double *inv3);
 
+/*
+ * Batched goal sampler of BASELINE.json's config 5 (8192 queries with random goals): goal of query id q = centre
+ * uniform in [lo, hi]^3 from the reference's GENERIC stream of seed q (rng.py:57-95, RngStream(q, phase=5)), three
+ * draws per try, rejected while closer than min_dist to start3 or inside an obstacle grown by radius + margin;
+ * goals (host, n_queries x 4) = centre + radius.  One device thread per query; bit-identical to the host loop
+ * batch.goal_for_query.  The reference has no batched sampler: its scenes carry one goal (envgen.py:127-163).
+ */
+int kpx_sample_goals(int64_t n_queries, const uint64_t *query_ids, int32_t n_obs, const double *obs_min,
+                     const double *obs_max, const double *start3, double lo, double hi, double radius,
+                     double min_dist, double margin, double *goals, void *stream);
+
 int kpx_device_info(int device, int32_t *sm_count, int32_t *max_coop_blocks_f32, int32_t *max_coop_blocks_f64);
 
 /*

@@ -6,8 +6,8 @@ package is the host-side mirror of the reference's planner interface.
 """
 from .backend import (Batch, CudaBackend, CudaF32Backend, PlanContext, available_backends, cuda_available,
                       get_backend)
-from .batch import (BatchPlanner, BatchResult, RaceFlags, gather_records, goal_for_query, plan_batch, race,
-                    shard_queries)
+from .batch import (BatchPlanner, BatchResult, RaceFlags, gather_records, goal_for_query, goals_for_queries, plan_batch,
+                    race, shard_queries)
 from .core import (ConfigError, DeviceError, Environment, EnvironmentFormatError, EnvironmentIOError, GoalBall,
                    KinopaxError, PlannerConfig, PlanResult, PlanStats, PlanStatus, TrajectorySegment,
                    environment_from_dict, environment_to_dict, load_environment, save_environment,

@@ -75,6 +75,8 @@ _SIGNATURES = {
     "kpx_fma_peak": (C.c_int, [C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "kpx_cull_thresholds": (C.c_int, [C.POINTER(Problem), C.c_int32, _vp]),
     "kpx_cull_tables": (C.c_int, [C.POINTER(Problem), C.c_int32, _vp, _vp, _vp]),
+    "kpx_sample_goals": (C.c_int, [C.c_int64, _vp, C.c_int32, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double,
+                                   C.c_double, C.c_double, _vp, _vp]),
     "kpx_device_info": (C.c_int, [C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kpx_propagate_batch": (C.c_int, [C.POINTER(Problem), _vp, C.c_int64, _vp, C.c_int64, C.c_int32, C.c_uint64,
                                       C.c_uint64, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

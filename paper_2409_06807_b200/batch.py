@@ -73,6 +73,18 @@ class BatchResult:
         return self.records["checked"] == -1
 
 
+def as_seed_array(seeds) -> np.ndarray:
+    """Seeds as uint64 over the whole 64-bit domain: negative seeds wrap and seeds >= 2^63 are kept, exactly as
+    ``KinoPax.reset`` masks a single seed (reference: tests/test_rng.py:32)."""
+    a = np.asarray(seeds)
+    if a.dtype.kind == "u":
+        return np.ascontiguousarray(a.ravel(), dtype=np.uint64)
+    if a.dtype.kind == "i":
+        return np.ascontiguousarray(a.ravel().astype(np.int64).astype(np.uint64))
+    return np.ascontiguousarray([int(s) & 0xFFFFFFFFFFFFFFFF for s in np.asarray(seeds, dtype=object).ravel()],
+                                dtype=np.uint64)
+
+
 class BatchPlanner:
     """Persistent multi-query planner bound to one GPU."""
 
@@ -115,6 +127,23 @@ class BatchPlanner:
     def __exit__(self, *exc):
         self.close()
 
+    def _queries(self, seeds, starts, goals) -> tuple:
+        """Host arrays of a batch of queries, checked as the reference checks a single one (planner.py:144-145:
+        the start must be a valid state): seeds over the whole uint64 domain (negative seeds wrap, as in
+        ``KinoPax.reset``), starts (Q, n) inside the state box and outside every obstacle, goals (Q, 4)."""
+        q, n = len(seeds), self.model.n
+        seeds = as_seed_array(seeds)
+        default_start = starts is None
+        starts = np.ascontiguousarray(np.tile(self.env.start, (q, 1)) if starts is None else starts, dtype=np.float64)
+        goals = np.ascontiguousarray(np.tile(self.problem.goal4, (q, 1)) if goals is None else goals, dtype=np.float64)
+        if starts.shape != (q, n) or goals.shape != (q, 4):
+            raise ConfigError("starts must be (Q, n) and goals (Q, 4)")
+        if not default_start and not self.problem.checker.state_valid_batch(starts).all():
+            raise ConfigError("a start state is invalid (outside the state box or in collision)")
+        if not (np.isfinite(goals).all() and (goals[:, 3] > 0).all()):
+            raise ConfigError("goals must be finite with a positive radius")
+        return seeds, starts, goals
+
     def run(self, seeds: Sequence[int], starts=None, goals=None, t_max: Optional[float] = None,
             want_chains: bool = True, stream=None, replan_rejected: bool = True,
             validate_resolution: Optional[float] = None) -> BatchResult:
@@ -130,11 +159,7 @@ class BatchPlanner:
         if q < 1:
             raise ConfigError("need at least one query")
         n, nu = self.model.n, self.model.control_dim
-        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64).astype(np.uint64))
-        starts = np.ascontiguousarray(np.tile(self.env.start, (q, 1)) if starts is None else starts, dtype=np.float64)
-        goals = np.ascontiguousarray(np.tile(self.problem.goal4, (q, 1)) if goals is None else goals, dtype=np.float64)
-        if starts.shape != (q, n) or goals.shape != (q, 4):
-            raise ConfigError("starts must be (Q, n) and goals (Q, 4)")
+        seeds, starts, goals = self._queries(seeds, starts, goals)
         tm = float(self.cfg.t_max if t_max is None else t_max)
         t0 = time.perf_counter()
         if validate_resolution is None or not want_chains:
@@ -150,7 +175,7 @@ class BatchPlanner:
                                                stream), "kpx_batch_run")
             res = BatchResult(rec, cs, cc, cd, ms.value, 0.0, starts, goals)
         else:
-            self.upload(seeds.astype(np.int64), starts, goals, want_chains=True, stream=stream)
+            self.upload(seeds, starts, goals, want_chains=True, stream=stream)
             self.launch(tm, stream=stream)
             self.validate(validate_resolution, stream=stream)
             res = self.download(stream=stream)
@@ -161,7 +186,7 @@ class BatchPlanner:
                     self._f64 = BatchPlanner(self.cfg, self.env, self.model, self.problem.check_resolution, "cuda",
                                              n_teams=int(min(len(bad), 8)), team_ctas=1, max_chain=self.max_chain,
                                              device=self.device)
-                r64 = self._f64.run(seeds[bad].astype(np.int64), starts[bad], goals[bad], tm, True, stream, False,
+                r64 = self._f64.run(seeds[bad], starts[bad], goals[bad], tm, True, stream, False,
                                     validate_resolution)
                 res.records[bad] = r64.records
                 res.chain_start[bad], res.chain_control[bad], res.chain_dt[bad] = r64.chain_start, r64.chain_control, r64.chain_dt
@@ -172,12 +197,7 @@ class BatchPlanner:
     # -- resident-input form: upload once, launch many times (what bench.py times with CUDA events) ---
     def upload(self, seeds, starts=None, goals=None, want_chains: bool = False, stream=None) -> int:
         q = len(seeds)
-        n = self.model.n
-        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64).astype(np.uint64))
-        starts = np.ascontiguousarray(np.tile(self.env.start, (q, 1)) if starts is None else starts, dtype=np.float64)
-        goals = np.ascontiguousarray(np.tile(self.problem.goal4, (q, 1)) if goals is None else goals, dtype=np.float64)
-        if starts.shape != (q, n) or goals.shape != (q, 4):
-            raise ConfigError("starts must be (Q, n) and goals (Q, 4)")
+        seeds, starts, goals = self._queries(seeds, starts, goals)
         _lib.check(self._lib.kpx_batch_upload(self._handle, q, _lib.ptr(seeds), _lib.ptr(starts), _lib.ptr(goals),
                                               1 if want_chains else 0, stream), "kpx_batch_upload")
         self._uploaded = (q, starts, goals, want_chains)
@@ -290,6 +310,22 @@ def goal_for_query(q: int, env: Environment, radius: float = 1.3, min_dist: floa
     raise ConfigError("could not sample a goal for this scene")
 
 
+def goals_for_queries(query_ids, env: Environment, radius: float = 1.3, min_dist: float = 4.0, margin: float = 0.4,
+                      stream=None) -> np.ndarray:
+    """``goal_for_query`` for a whole batch on the device (``kpx_sample_goals``: one thread per query, the same
+    GENERIC streams and float64 operations): (Q, 4) goals, bit-identical to the host loop."""
+    ids = np.ascontiguousarray([int(q) & 0xFFFFFFFFFFFFFFFF for q in np.asarray(query_ids).ravel()], dtype=np.uint64)
+    out = np.zeros((len(ids), 4))
+    omin = np.ascontiguousarray(env.obstacles_min, dtype=np.float64)
+    omax = np.ascontiguousarray(env.obstacles_max, dtype=np.float64)
+    start3 = np.ascontiguousarray(env.start[:3], dtype=np.float64)
+    _lib.check(_lib.load().kpx_sample_goals(len(ids), _lib.ptr(ids), env.n_obstacles, _lib.ptr(omin) if env.n_obstacles else None,
+                                            _lib.ptr(omax) if env.n_obstacles else None, _lib.ptr(start3), 1.0, 9.0,
+                                            float(radius), float(min_dist), float(margin), _lib.ptr(out), stream),
+               "kpx_sample_goals")
+    return out
+
+
 class RaceFlags:
     """Stop words of an OR-parallel race across the ranks of one node.
 
@@ -334,8 +370,11 @@ class RaceFlags:
 
 
 def race(engine, flags: "RaceFlags", seed: int, t_max: Optional[float] = None):
-    """One rank's leg of the race: plan with ``seed`` until solved or a peer's store stops us."""
+    """One rank's leg of the race: plan with ``seed`` until solved or a peer's store stops us.
+
+    Returns the ``PlanResult`` of ``KinoPax.solve``: a solved leg has had its trajectory rebuilt and re-validated
+    in float64 (a float32 winner's kernel has already stopped the peers by then, so if that check refuses the
+    solution this rank plans the query again with the float64 kernels -- unstoppable, the race is over -- and
+    still hands back a valid plan).  ``result.device["status_code"]`` tells a stopped leg (5) from a time-out (1)."""
     engine.reset(seed=seed)
-    st = engine._run(engine.cfg.t_max if t_max is None else t_max, stop_flag=C.c_void_p(flags.own_ptr),
-                     peer_flags=[p for p in flags.peer_ptrs])
-    return st
+    return engine.solve(t_max=t_max, stop_flag=C.c_void_p(flags.own_ptr), peer_flags=[p for p in flags.peer_ptrs])

@@ -51,8 +51,8 @@ int check_problem(const kpx_problem* pr) {
     if (pr->subcells < 1 || pr->lambda_max < 1 || pr->t_e < 1) return fail(KPX_E_ARG, "bad configuration");
     double regions = 1.0;
     for (int d = 0; d < pr->grid_n; ++d) regions *= (double)pr->grid_cells[d];
-    if (regions * pr->subcells * pr->subcells * pr->subcells >= 2147483646.0)
-        return fail(KPX_E_LIMIT, "regions x sub-cells must stay below 2^31");
+    if (regions * pr->subcells * pr->subcells * pr->subcells >= 1073741824.0)
+        return fail(KPX_E_LIMIT, "regions x sub-cells must stay below 2^30");
     if (pr->t_e >= (1ll << 30)) return fail(KPX_E_LIMIT, "t_e too large");
     return KPX_OK;
 }
@@ -385,7 +385,69 @@ int measure_fma(int sms, double ms_target, double* tflops) {
 }
 }  // namespace
 
+namespace {
+// Goal of query q (BASELINE.json config 5): centre uniform in [lo, hi]^3 drawn from the GENERIC stream of
+// seed q (rng.py:57-95: key(seed = q, 0, 0, 0, phase 5), draws 0, 1, 2, ...), three draws per try; a try is rejected
+// if the centre is closer than min_dist to the start or inside an obstacle grown by `grow` on every side.  One thread
+// per query, the same float64 operations in the same order as batch.goal_for_query (no FMA contraction).
+__global__ void sample_goals_kernel(int n, const unsigned long long* __restrict__ ids, const double* __restrict__ obs /* [k][6] */,
+                                    int n_obs, double sx, double sy, double sz, double lo, double hi, double radius,
+                                    double min_dist, double grow, int max_tries, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t key = mix64(ids[i]);
+    key = mix64(key ^ 0ull); key = mix64(key ^ 0ull); key = mix64(key ^ 0ull); key = mix64(key ^ 5ull);
+    const double span = __dsub_rn(hi, lo);
+    uint64_t idx = 0;
+    double c[3] = {0.0, 0.0, 0.0};
+    bool found = false;
+    for (int t = 0; t < max_tries && !found; ++t) {
+        for (int a = 0; a < 3; ++a) c[a] = __dadd_rn(lo, __dmul_rn(unit53(draw_u64(key, idx++)), span));
+        const double d0 = __dsub_rn(c[0], sx), d1 = __dsub_rn(c[1], sy), d2 = __dsub_rn(c[2], sz);
+        const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2)));
+        if (dist < min_dist) continue;
+        bool inside = false;
+        for (int k = 0; k < n_obs && !inside; ++k) {
+            bool in = true;
+            for (int a = 0; a < 3; ++a)
+                in = in && c[a] >= __dsub_rn(obs[6 * k + a], grow) && c[a] <= __dadd_rn(obs[6 * k + 3 + a], grow);
+            inside = in;
+        }
+        found = !inside;
+    }
+    out[4 * i + 0] = found ? c[0] : nan(""); out[4 * i + 1] = found ? c[1] : nan(""); out[4 * i + 2] = found ? c[2] : nan("");
+    out[4 * i + 3] = radius;
+}
+}  // namespace
+
 extern "C" {
+
+int kpx_sample_goals(int64_t n_queries, const uint64_t* query_ids, int32_t n_obs, const double* obs_min,
+                     const double* obs_max, const double* start3, double lo, double hi, double radius, double min_dist,
+                     double margin, double* goals, void* stream) {
+    if (n_queries < 0 || !query_ids || !start3 || !goals || n_obs < 0 || (n_obs && (!obs_min || !obs_max)))
+        return fail(KPX_E_ARG, "bad goal-sampler arguments");
+    if (n_queries == 0) return KPX_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<double> boxes(6 * (size_t)std::max(n_obs, 1), 0.0);
+    for (int k = 0; k < n_obs; ++k)
+        for (int a = 0; a < 3; ++a) { boxes[6 * k + a] = obs_min[3 * k + a]; boxes[6 * k + 3 + a] = obs_max[3 * k + a]; }
+    char* dev = nullptr;
+    const size_t o_ids = 0, o_box = align_up(8 * (size_t)n_queries, 256), o_out = o_box + align_up(8 * boxes.size(), 256);
+    if (cudaMalloc(&dev, o_out + 32 * (size_t)n_queries) != cudaSuccess) { cudaGetLastError(); return fail(KPX_E_CUDA, "cudaMalloc failed"); }
+    struct Free { char* p; ~Free() { cudaFree(p); } } guard{dev};
+    CU(cudaMemcpyAsync(dev + o_ids, query_ids, 8 * (size_t)n_queries, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dev + o_box, boxes.data(), 8 * boxes.size(), cudaMemcpyHostToDevice, st));
+    sample_goals_kernel<<<(unsigned)((n_queries + 127) / 128), 128, 0, st>>>(
+        (int)n_queries, (const unsigned long long*)(dev + o_ids), (const double*)(dev + o_box), n_obs, start3[0], start3[1],
+        start3[2], lo, hi, radius, min_dist, radius + margin, 1000, (double*)(dev + o_out));
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(goals, dev + o_out, 32 * (size_t)n_queries, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < n_queries; ++i)
+        if (std::isnan(goals[4 * i])) return fail(KPX_E_STATE, "no admissible goal for query id %llu in 1000 tries", (unsigned long long)query_ids[i]);
+    return KPX_OK;
+}
 
 int kpx_fma_peak(int device, double ms_target, double* tflops, double* tflops_f64) {
     cudaDeviceProp dp;
@@ -754,10 +816,11 @@ int kpx_plan_items(kpx_plan* p, int64_t max_items, int64_t* n_items, uint8_t* va
     if (c.last_sorted && (rc = d2h(pos, w.pos_of, (size_t)I))) return rc;
     for (int64_t i = 0; i < I; ++i) {
         const int64_t ip = c.last_sorted ? pos[i] : i;
-        const bool v = code[ip] != kItemInvalid;
+        const bool v = !(code[ip] & kItemDeadBit);
         const uint32_t pair = code[ip] & ~kItemGoalBit;
         if (valid) valid[i] = v;
-        if (region) region[i] = v ? (int64_t)(pair / (uint32_t)b.subs) : -1;
+        if (region) region[i] = v ? (int64_t)(pair / (uint32_t)b.subs)
+                                  : (code[ip] == kItemInvalid ? -1 : (int64_t)(code[ip] & (kItemDeadBit - 1u)));
         if (sub) sub[i] = v ? (int64_t)(pair % (uint32_t)b.subs) : 0;
         if (keep) keep[i] = v && rank[i] >= 0;
         if (goal_hit) goal_hit[i] = v && (code[ip] & kItemGoalBit) != 0;

@@ -52,8 +52,12 @@ constexpr int kCoopSteps = 8;        // segments densified into more points than
 #endif
 constexpr uint32_t kUnclaimed = 0xFFFFFFFFu;
 
+// per-item result word of an iteration: a VALID item holds its (region, sub) pair in bits 0..29 and the goal test
+// of its end state in bit 31; an INVALID item has bit 30 set, with its region below (the region still counts
+// towards n_invalid, _kernel.pyx:261-271) -- or all ones if the integration went non-finite (region -1)
 constexpr uint32_t kItemInvalid = 0xFFFFFFFFu;
 constexpr uint32_t kItemGoalBit = 0x80000000u;
+constexpr uint32_t kItemDeadBit = 0x40000000u;
 
 enum : int { PH_SAMPLE = 1, PH_ACCEPT = 2, PH_DEMOTE = 3, PH_PROMOTE = 4 };
 

@@ -141,7 +141,7 @@ struct Workspace {                // device pointers of one team's state
     // nothing beats "visited".  The table is refilled with 0xFF only when the epochs run out (2^(32-s) - 1 queries).
     uint32_t* claim;
     void* it_end;                 // chunked SoA like `states`: end states of this iteration's valid items
-    uint32_t* it_code;            // [cap] kItemInvalid | (goal bit | pair)
+    uint32_t* it_code;            // [cap] per-item result word (kItemGoalBit / kItemDeadBit, kpx_device.cuh)
     int *it_rank, *it_parent;     // [cap]
     uint8_t* it_bin;              // [cap] substep-count bin of each item
     int* order;                   // [cap] item numbers sorted by substep count, longest first
@@ -476,7 +476,7 @@ __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Works
     int region = -1; bool valid = false;
     if (active) {
         region = o.region; valid = o.valid;
-        uint32_t code = kItemInvalid;
+        uint32_t code = region >= 0 ? (kItemDeadBit | (uint32_t)region) : kItemInvalid;
         if (valid) {
             const uint32_t pair = (uint32_t)region * (uint32_t)P.subs_per_region + (uint32_t)o.sub;
             const R d0 = o.end[0] - (R)Q.goal[0], d1 = o.end[1] - (R)Q.goal[1], d2 = o.end[2] - (R)Q.goal[2];
@@ -824,7 +824,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 keep[j] = false;
-                if (code[j] != kItemInvalid) {
+                if (!(code[j] & kItemDeadBit)) {
                     const int w = base + j;
                     const uint32_t pair = code[j] & ~kItemGoalBit;
                     const int region = (int)(pair / (uint32_t)SUBS);

@@ -146,6 +146,16 @@ class KinoPax:
     def reset(self, seed: Optional[int] = None, start=None, goal4=None) -> None:
         """Arm the handle for a (new) query on the same problem; the device reset runs inside the kernel."""
         self.seed = self.cfg.seed if seed is None else int(seed)
+        if start is not None:          # the reference refuses an invalid start in __init__ (planner.py:144-145)
+            start = np.ascontiguousarray(start, dtype=np.float64)
+            if start.shape != (self.model.n,):
+                raise ConfigError(f"start must have shape ({self.model.n},), got {start.shape}")
+            if not self.checker.state_valid(start):
+                raise ConfigError("start state is invalid (outside the state box or in collision)")
+        if goal4 is not None:
+            goal4 = np.ascontiguousarray(goal4, dtype=np.float64)
+            if goal4.shape != (4,) or not np.isfinite(goal4).all() or not goal4[3] > 0:
+                raise ConfigError("goal4 must be (cx, cy, cz, r) with a positive radius")
         self.start = np.ascontiguousarray(self.env.start if start is None else start, dtype=np.float64)
         self.goal4 = np.ascontiguousarray(self.problem.goal4 if goal4 is None else goal4, dtype=np.float64)
         _lib.check(self._lib.kpx_plan_reset(self._handle, self.seed & 0xFFFFFFFFFFFFFFFF, _lib.ptr(self.start),
@@ -312,9 +322,11 @@ class KinoPax:
         return segs, ok
 
     def solve(self, trace_fn: Optional[Callable[[IterationTrace], None]] = None,
-              capture_tree: bool = False) -> PlanResult:
+              capture_tree: bool = False, t_max: Optional[float] = None, stop_flag=None, peer_flags=None) -> PlanResult:
+        """``KinoPax.solve`` (``planner.py:271-316``).  ``stop_flag`` / ``peer_flags`` wire an OR-parallel race
+        (``batch.race``): a device word that stops this run, device words this run raises when it solves."""
         t0 = time.perf_counter()
-        st = self._run(self.cfg.t_max)
+        st = self._run(self.cfg.t_max if t_max is None else t_max, stop_flag=stop_flag, peer_flags=peer_flags)
         status = _STATUS.get(st.status, PlanStatus.ERROR)
         trajectory, duration = [], 0.0
         retried = False
@@ -334,7 +346,10 @@ class KinoPax:
                                             solution_duration_s=duration))
         result.device = {"device_ms": st.device_ms, "reset_ms": st.reset_ms, "items": int(st.items),
                          "substeps": int(st.substeps), "points": int(st.points), "boxsteps": int(st.boxsteps), "launches": int(st.launches),
-                         "precision": "f64" if self.precision == _lib.F64 else "f32", "f64_retry": retried}
+                         "precision": "f64" if self.precision == _lib.F64 else "f32", "f64_retry": retried,
+                         # the raw device status: PlanStatus keeps the reference's four values, so a run stopped by a
+                         # race peer (5) reads TIMEOUT there; this tells the two apart
+                         "status_code": int(st.status), "stopped_by_peer": int(st.status) == _lib.STOPPED}
         if trace_fn is not None:
             for tr in self.traces():
                 trace_fn(tr)

@@ -62,6 +62,32 @@ def test_batch_with_per_query_goals(kp):
             assert np.linalg.norm(end - goals[i, :3]) <= goals[i, 3] + 1e-9
 
 
+def test_config5_queries_match_oracle_query_by_query(kp, orc):
+    """BASELINE.json config 5 (quadcopter, Trees scene, per-query random goals, full-size configuration): the
+    float64 batch against the CPU oracle planning the same (seed, goal) -- status, iteration count, tree size,
+    solution slot and chain length identical for every query; the twin of test_batch_equals_single_queries."""
+    import dataclasses
+    model = kp.get_model("quad12")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = kp.PlannerConfig(t_e=model.default_t_e, lambda_max=32, t_prop=model.default_t_prop, epsilon=0.005, delta=1.0,
+                           cells_per_dim=model.default_cells_per_dim, subcells_per_dim=4, t_max=60.0, seed=0)
+    q = 16
+    goals = np.stack([kp.goal_for_query(i, env) for i in range(q)])
+    with kp.BatchPlanner(cfg, env, model, backend="cuda", n_teams=16, team_ctas=1) as bp:
+        res = bp.run(np.arange(q), goals=goals)
+    names = {0: "solved", 1: "timeout", 2: "capacity_exhausted", 3: "error"}
+    for i in range(q):
+        env_i = dataclasses.replace(env, goal=kp.GoalBall(center=goals[i, :3].copy(), radius=float(goals[i, 3])))
+        op = orc.plan_from_problem(kp.build_problem(cfg.with_seed(i), env_i, model))
+        op.solve(t_max=120.0)
+        r = res.records[i]
+        assert names[int(r["status"])] == op.status, i
+        assert int(r["iterations"]) == int(op.raw.iteration) and int(r["tree_size"]) == int(op.raw.size), i
+        if op.status == "solved":
+            assert int(r["solution_slot"]) == int(op.raw.solution_slot) and int(r["chain_len"]) == len(op.chain()), i
+    assert res.solved.sum() >= q - 2 and res.validated.sum() == res.solved.sum()
+
+
 @pytest.mark.parametrize("model_name,scene,backend,t_e", [("di6", "forest", "cuda-f32", 20000), ("di6", "forest", "cuda", 8000),
                                                           ("dubins6", "building", "cuda-f32", 30000),
                                                           ("quad12", "forest", "cuda-f32", 60000)])
@@ -147,8 +173,9 @@ def test_race_flag_stops_a_run(kp):
     with kp.KinoPax(cfg, env, model, backend="cuda-f32") as eng:
         flags.flag[0] = 1
         torch.cuda.synchronize()
-        st = kp.race(eng, flags, seed=0)
-        assert st.status == 5 and st.iterations == 1          # KPX_STOPPED after one iteration
+        res = kp.race(eng, flags, seed=0)
+        assert res.device["status_code"] == 5 and res.device["stopped_by_peer"] and res.stats.iterations == 1   # KPX_STOPPED
+        assert res.status is kp.PlanStatus.TIMEOUT and res.trajectory == []
         flags.clear()
         eng.reset(seed=0)
         st = eng._run(60.0, stop_flag=C.c_void_p(flags.own_ptr), peer_flags=[peer.data_ptr()])
@@ -188,10 +215,12 @@ def test_full_size_outcomes_match_reference_golden(kp, name, model_name, scene, 
             L = int(res.records["chain_len"][i])
             ok = L == r["segments"] and abs(float(res.chain_dt[i, :L].sum()) - r["solution_duration_s"]) < 1e-9
         same[i] = ok
+    # measured on B200: 100/100 seeds identical for every configuration.  The trig models may lose a seed to a
+    # last-ulp difference between CUDA's and glibc's sin/cos flipping one cell decision: at most 2 of 100.
     if exact:
         assert same.all(), np.flatnonzero(~same)
     else:
-        assert same.mean() >= 0.9, (same.mean(), np.flatnonzero(~same))
+        assert same.sum() >= len(seeds) - 2, (same.sum(), np.flatnonzero(~same))
     assert int(res.solved.sum()) == int(ref_solved.sum()) or not exact
     assert res.validated.sum() == res.solved.sum()            # float64 trees always pass their own re-validation
     with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", team_ctas=1) as bp32:
@@ -217,3 +246,80 @@ def test_race_between_two_processes(kp):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=root)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "race ok" in out.stdout, out.stdout[-2000:]
+
+
+def test_sharded_plan_two_ranks_equals_one(kp):
+    """Multi-GPU path end to end with two torchrun ranks (gloo rendezvous) sharing this GPU: queries sharded q mod 2,
+    planned per rank, records gathered once -- identical, query by query, to one rank planning them all
+    (tools/shard2.py).  On a multi-GPU box the same script runs one rank per device."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KPX_SHARD_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29541", os.path.join(root, "tools", "shard2.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "shard ok: 48 queries over 2 ranks" in out.stdout, out.stdout[-2000:]
+
+
+def test_bench_spawns_its_own_ranks(kp):
+    """`python bench.py --gpus 2` outside torchrun launches two ranks itself (here both on this GPU, gloo, through
+    the bench's test hooks) and reports n_gpus = 2 with the queries of both ranks in the job total."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env.update(KPX_BENCH_DIST_BACKEND="gloo", KPX_BENCH_DEVICE="0")
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3", "--queries", "96",
+           "--no-latency", "--no-kernel-seam", "--no-configs", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["config"]["queries_per_gpu_per_step"] == 96
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["batch"]["queries"] == 96
+
+
+def test_device_goal_sampler_equals_host_loop(kp):
+    """kpx_sample_goals (one device thread per query) draws exactly the goals of the host loop goal_for_query:
+    same GENERIC streams (rng.py:57-95), same float64 operations, same rejections."""
+    for model_name, scene in (("quad12", "forest"), ("di6", "building"), ("di6", "narrow")):
+        env = kp.gen_environment(scene, model_name, seed=0)
+        ids = np.concatenate([np.arange(300), np.array([8191, 2 ** 40 + 7], dtype=np.int64)])
+        dev = kp.goals_for_queries(ids, env)
+        host = np.stack([kp.goal_for_query(int(q), env) for q in ids])
+        assert np.array_equal(dev, host)
+    empty = kp.Environment("empty", np.zeros(3), np.full(3, 10.0), np.zeros((0, 3)), np.zeros((0, 3)), env.start, env.goal)
+    assert np.array_equal(kp.goals_for_queries(np.arange(50), empty),
+                          np.stack([kp.goal_for_query(q, empty) for q in range(50)]))
+
+
+def test_batch_refuses_invalid_starts_and_takes_any_seed(kp):
+    """planner.py:144-145 for a batch: a start in collision or outside the state box is a ConfigError, not a silent
+    plan; seeds cover the whole uint64 domain like KinoPax.reset (negative seeds wrap, seeds >= 2^63 are kept)."""
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=6000, seed=0)
+    inside = env.start.copy()
+    inside[:3] = (env.obstacles_min[0] + env.obstacles_max[0]) / 2
+    with kp.BatchPlanner(cfg, env, model, backend="cuda", n_teams=4, team_ctas=1) as bp:
+        with pytest.raises(kp.ConfigError):
+            bp.run([0, 1], starts=np.stack([env.start, inside]))
+        with pytest.raises(kp.ConfigError):
+            bp.run([0], starts=np.array([[1.0, 1.0, 11.0, 0, 0, 0]]))
+        with pytest.raises(kp.ConfigError):
+            bp.run([0], starts=np.zeros((1, 3)))
+        seeds = [2 ** 63 + 5, -1, 7]
+        res = bp.run(seeds)
+        with kp.KinoPax(cfg, env, model, backend="cuda") as eng:
+            with pytest.raises(kp.ConfigError):
+                eng.reset(start=inside)
+            with pytest.raises(kp.ConfigError):
+                eng.reset(start=np.zeros(3))
+            for i, sd in enumerate(seeds):
+                eng.reset(seed=sd)
+                one = eng.solve()
+                assert one.stats.iterations == res.records["iterations"][i] and one.stats.tree_size == res.records["tree_size"][i]

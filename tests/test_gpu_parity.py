@@ -72,11 +72,22 @@ def test_batch_parity_f32_tolerance(kp, model_name):
     scale = np.maximum(np.abs(g["end"]), 1.0)
     rel = (_wrap_diff(b.end, g["end"], model.wrap_dims) / scale)[both_valid]
     assert np.max(rel) < F32_RTOL, np.max(rel)
-    # verdicts / cells may flip only for items that sit within float32 rounding of a boundary
+    # Verdicts / cells may flip only for items that sit within float32 rounding of a boundary.  Measured on B200:
+    # no flip at all on these batches (1200-1600 items); the bar leaves room for one such item per thousand, and
+    # every flip must be explained by a boundary within a few float32 ulps of the float64 end state.
     agree = (b.valid == g["valid"]) & (b.region == g["region"])
-    assert agree.mean() > 0.995, agree.mean()
     both = (b.valid == 1) & (g["valid"] == 1) & (b.region == g["region"])
-    assert (b.sub[both] == g["sub"][both]).mean() > 0.99
+    sub_ok = b.sub[both] == g["sub"][both]
+    assert agree.mean() >= 0.999, agree.mean()
+    assert sub_ok.mean() >= 0.999, sub_ok.mean()
+    flipped = np.flatnonzero((b.region != g["region"]) & (b.valid == 1) & (g["valid"] == 1))
+    ulp = 8 * np.finfo(np.float32).eps
+    for w in flipped:        # a cell flip: some grid coordinate of the float64 end state is within ulps of a cell edge
+        rel = (g["end"][w] - g["grid_lo"]) / g["grid_width"]
+        assert np.min(np.abs(rel - np.round(rel))) <= ulp * np.max(np.abs(g["end"][w]) / g["grid_width"] + 1), w
+    for w in np.flatnonzero(both)[~sub_ok]:
+        rel = (g["end"][w][:3] - g["grid_lo"][:3]) / g["grid_width"][:3] * int(g["subcells"])
+        assert np.min(np.abs(rel - np.round(rel))) <= ulp * int(g["subcells"]) * np.max(np.abs(g["end"][w][:3]) / g["grid_width"][:3] + 1), w
 
 
 def test_kernel_rng_matches_stream(kp):
@@ -149,8 +160,10 @@ def _step_compare(kp, orc, model_name, scene, t_e, seed, backend, max_iters=60, 
             for k in ("n_valid", "n_invalid", "cov", "visited"):
                 assert np.array_equal(getattr(ra, k), rb[k]), (it, k)
             assert np.array_equal(ra.avail_mask, rb["avail"].astype(bool)), it
-            assert np.allclose(ra.score, rb["score"], rtol=1e-13, atol=0), it
-            assert np.allclose(ra.p_accept, rb["p_accept"], rtol=1e-12, atol=0), it
+            # scores use the reference's expression order; the total is summed in NumPy's pairwise order on the
+            # device (decomposition.py:199), so the estimates are bit-identical
+            assert np.array_equal(ra.score, rb["score"]), it
+            assert np.array_equal(ra.p_accept, rb["p_accept"]), it
             tr, orc_tr = eng.traces()[-1], op.trace()
             for k in ("iteration", "branching", "ve_size", "vo_size", "attempted", "valid", "staged", "appended",
                       "tree_size"):
@@ -159,7 +172,8 @@ def _step_compare(kp, orc, model_name, scene, t_e, seed, backend, max_iters=60, 
             items, ob = eng.last_items(), op.last_batch()
             assert np.array_equal(items["valid"], ob["valid"]), it
             v = ob["valid"].astype(bool)
-            assert np.array_equal(items["region"][v], ob["region"][v]) and np.array_equal(items["sub"][v], ob["sub"][v])
+            # regions of ALL items (an invalid item still counts towards its end state's region; -1 = non-finite)
+            assert np.array_equal(items["region"], ob["region"]) and np.array_equal(items["sub"][v], ob["sub"][v])
             keep = np.zeros(len(v), np.uint8)
             keep[ob["staged_idx"]] = 1
             assert np.array_equal(items["keep"], keep), it
@@ -200,14 +214,18 @@ def test_team_size_does_not_change_the_tree(kp):
     model = kp.get_model("di6")
     env = kp.gen_environment("narrow", model, seed=0)
     cfg = small_cfg(kp, model, t_e=3000, seed=2)
-    snaps = []
+    snaps, regs = [], []
     for team in (0, 1, 3, 16):
         with kp.KinoPax(cfg, env, model, backend="cuda", team_ctas=team) as eng:
             snaps.append(eng.solve(capture_tree=True).tree_snapshot)
-    for s in snaps[1:]:
+            regs.append(eng.region_state())
+    for s, r in zip(snaps[1:], regs[1:]):
         assert s["size"] == snaps[0]["size"]
         for k in ("states", "parent", "tag", "region", "dt"):
             assert np.array_equal(s[k], snaps[0][k]), k
+        # the score total is summed in one fixed (NumPy pairwise) order whatever the team size
+        for k in ("n_valid", "n_invalid", "cov", "visited", "score", "p_accept"):
+            assert np.array_equal(getattr(r, k), getattr(regs[0], k)), k
 
 
 def test_capacity_exhaustion_start_in_goal_and_enclosed_goal(kp, orc):
@@ -357,3 +375,108 @@ def test_fused_trajectory_call_equals_the_separate_entry_points(kp, backend):
                 assert x.dt == y.dt and np.array_equal(x.control, y.control)
                 assert np.array_equal(x.sampled_states, y.sampled_states) and np.array_equal(x.end_state, y.end_state)
             assert kp.ValidityChecker(env, model, 0.05).trajectory_valid(a, start=env.start)
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# float32 production loop: integer bookkeeping held to the reference's rules GIVEN ITS OWN SEGMENTS
+
+@pytest.mark.parametrize("model_name,scene,t_e,seed,team", [("di6", "forest", 6000, 1, 0), ("di6", "forest", 20000, 2, 1),
+                                                            ("dubins6", "building", 5000, 2, 0),
+                                                            ("quad12", "narrow", 8000, 3, 0), ("quad12", "forest", 30000, 5, 1)])
+def test_f32_bookkeeping_is_exact_given_its_own_items(kp, orc, model_name, scene, t_e, seed, team):
+    """north_star: "collision verdicts, region counts and compaction indices are bit-exact for the same segments".
+    The float32 engine is stepped; after every iteration its own per-item results (valid, region, sub, end state,
+    goal test) are handed to the oracle's bookkeeping (kpo_plan_step_given = planner.py:185-265 on a supplied
+    Batch).  Region counters, first-visit winners (visited / cov), the kept set, the appended slots (parent,
+    region, states), the demote / promote tags, the estimates and the trace counters must then be IDENTICAL --
+    for the whole-GPU team (latency build, global sort) and the one-CTA team (throughput build, tile sort)."""
+    model = kp.get_model(model_name)
+    env = kp.gen_environment(scene, model, seed=0)
+    cfg = small_cfg(kp, model, t_e=t_e, seed=seed)
+    op = orc.plan_from_problem(kp.build_problem(cfg, env, model))
+    f32 = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)   # noqa: E731
+    with kp.KinoPax(cfg, env, model, backend="cuda-f32", team_ctas=team) as eng:
+        for it in range(1, 80):
+            st = eng.step()
+            items = eng.last_items()
+            ost = op.step_given(items["valid"], items["region"], items["sub"], items["end"], goal_hit=items["goal_hit"])
+            ob = op.last_batch()
+            # the kernel's parent slots are the oracle's e_slots repeated lambda times (ascending V_E order)
+            lam = len(items["valid"]) // len(ob["e_slots"])
+            assert np.array_equal(items["parent_slot"], np.repeat(ob["e_slots"], lam)), it
+            keep = np.zeros(len(items["valid"]), np.uint8)
+            keep[ob["staged_idx"]] = 1
+            assert np.array_equal(items["keep"], keep), it                       # the kept set (compaction input)
+            a, b = eng.snapshot(), op.snapshot()
+            assert a["size"] == b["size"], (it, a["size"], b["size"])
+            for k in ("parent", "tag", "region"):                                 # appended slots, demote / promote
+                assert np.array_equal(a[k], b[k]), (it, k)
+            assert np.array_equal(a["states"][1:], b["states"][1:]), it           # the float32 end states, where appended
+            assert np.array_equal(a["states"][0], f32(env.start))                 # the root is the start rounded once
+            assert np.array_equal(a["control"], f32(b["control"])) and np.array_equal(a["dt"], f32(b["dt"])), it
+            ra, rb = eng.region_state(), op.decomposition()
+            for k in ("n_valid", "n_invalid", "cov", "visited", "score", "p_accept"):
+                assert np.array_equal(getattr(ra, k), rb[k]), (it, k)
+            assert np.array_equal(ra.avail_mask, rb["avail"].astype(bool)), it
+            tr, otr = eng.traces()[-1], op.trace()
+            for k in ("iteration", "branching", "ve_size", "vo_size", "attempted", "valid", "staged", "appended", "tree_size"):
+                assert getattr(tr, k) == otr[k], (it, k)
+            assert {0: 0, 2: 2, 4: 4}[st.status] == ost, (it, st.status, ost)
+            if st.status != 4:
+                break
+        if st.status == 0:
+            assert int(st.solution_slot) == int(op.raw.solution_slot)
+        assert it >= 4
+
+
+def test_time_budget_rules(kp):
+    """planner.py:282: the clock is tested BEFORE each iteration -- t_max = 0 runs no iteration at all and reports
+    TIMEOUT; a stepped run only counts the time its launches were running, not the host's pauses between them."""
+    import time
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    res = kp.plan(small_cfg(kp, model, t_e=6000, seed=1, t_max=0.0), env, model, backend="cuda")
+    assert res.status is kp.PlanStatus.TIMEOUT and res.stats.iterations == 0 and res.stats.tree_size == 1
+    cfg = small_cfg(kp, model, t_e=6000, seed=1, t_max=0.25)
+    with kp.KinoPax(cfg, env, model, backend="cuda") as eng:
+        st = eng.step()
+        assert st.status == 4 and st.iterations == 1
+        time.sleep(0.6)                                  # longer than t_max: must not count
+        st = eng.step()
+        assert st.status == 4 and st.iterations == 2, (st.status, st.iterations)
+        assert st.device_ms < 250.0
+        full = eng._run(60.0)
+        assert full.status == 0
+    ref = kp.plan(small_cfg(kp, model, t_e=6000, seed=1), env, model, backend="cuda")
+    assert ref.stats.iterations == full.iterations and ref.stats.tree_size == full.tree_size
+    # a run that timed out can be continued with a larger budget
+    sealed = kp.Environment("sealed", np.zeros(3), np.full(3, 10.0), np.array([[7.0, 7, 7]]), np.array([[10.0, 10, 10]]),
+                            env.start, kp.GoalBall(np.array([8.5, 8.5, 8.5]), 0.5))
+    with kp.KinoPax(small_cfg(kp, model, t_e=200000, seed=0, t_max=0.0003), sealed, model, backend="cuda-f32") as eng:
+        a = eng._run(0.0003)
+        assert a.status == 1 and a.iterations >= 1
+        b = eng._run(0.0008)
+        assert b.status in (1, 2) and b.iterations > a.iterations
+
+
+def test_set_obstacles_capacity(kp):
+    """kpx_plan_set_obstacles: a plan created without obstacles has no room for one (error, no write); a plan
+    created with k obstacles accepts up to k and plans against the new set."""
+    from paper_2409_06807_b200 import _lib
+    model = kp.get_model("di6")
+    cfg = small_cfg(kp, model, t_e=3000, seed=2)
+    one_min, one_max = np.array([[4.0, 0.0, 0.0]]), np.array([[6.0, 10.0, 10.0]])          # a wall across the cube
+    with kp.KinoPax(cfg, make_empty_env(kp), model, backend="cuda") as eng:
+        rc = eng._lib.kpx_plan_set_obstacles(eng._handle, 1, _lib.ptr(one_min), _lib.ptr(one_max))
+        assert rc == _lib.E_ARG
+        assert eng.solve().solved                        # untouched: still the empty scene
+    env = kp.gen_environment("narrow", model, seed=0)
+    with kp.KinoPax(cfg, env, model, backend="cuda") as eng:
+        rc = eng._lib.kpx_plan_set_obstacles(eng._handle, 3, _lib.ptr(np.zeros((3, 3))), _lib.ptr(np.ones((3, 3))))
+        assert rc == _lib.E_ARG                          # created with 2
+        _lib.check(eng._lib.kpx_plan_set_obstacles(eng._handle, 1, _lib.ptr(one_min), _lib.ptr(one_max)), "set")
+        res = eng.solve()
+        assert res.status is not kp.PlanStatus.SOLVED    # the wall seals the goal side off
+        _lib.check(eng._lib.kpx_plan_set_obstacles(eng._handle, 0, None, None), "set")
+        eng.reset()
+        assert eng.solve().solved

@@ -18,12 +18,14 @@ with kp.KinoPax(cfg, env, model, backend="cuda-f32") as eng:
     flags.clear()
     dist.barrier()
     t0 = time.perf_counter()
-    st = kp.race(eng, flags, seed=rank)
+    res = kp.race(eng, flags, seed=rank)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) * 1e3
     dist.barrier()
     out = [None] * world
-    dist.all_gather_object(out, (rank, int(st.status), int(st.iterations), bool(flags.fired()), dt))
+    if res.solved:      # a winner's plan has been rebuilt and re-validated in float64 before it is reported
+        assert kp.ValidityChecker(env, model, 0.05).trajectory_valid(res.trajectory, start=env.start)
+    dist.all_gather_object(out, (rank, int(res.device["status_code"]), int(res.stats.iterations), bool(flags.fired()), dt))
     if rank == 0:
         for r in out: print("rank %d: status %d iterations %d own_flag_fired %s %.3f ms" % r)
         winners = [r for r in out if r[1] == 0]
