@@ -87,6 +87,7 @@ typedef struct kpx_stats {
     uint64_t points;         /* collision points tested */
     uint64_t boxsteps;       /* substeps whose state-box test ran */
     uint64_t launches;       /* kernel launches issued by this call */
+    uint64_t free_items;     /* extensions certified valid and finished from the closed form (float32 double integrators) */
 } kpx_stats;
 
 /* IterationTrace (planner.py:121-131). */
@@ -227,7 +228,7 @@ typedef struct kpx_query_result {
     int32_t status, iterations;
     int64_t tree_size, solution_slot, chain_len;
     double device_ms;
-    uint64_t items, substeps, points, boxsteps;
+    uint64_t items, substeps, points, boxsteps, free_items;
     int32_t checked;     /* kpx_batch_validate: 1 = solution re-validated in float64, -1 = rejected, 0 = not checked */
     int32_t check_code;  /* 0 ok, 3 a state or interpolant is invalid, 4 goal missed, 5 chain longer than max_chain */
 } kpx_query_result;

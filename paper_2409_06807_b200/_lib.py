@@ -43,6 +43,7 @@ class Stats(C.Structure):
         ("status", C.c_int32), ("iterations", C.c_int32), ("tree_size", C.c_int64), ("solution_slot", C.c_int64),
         ("chain_len", C.c_int64), ("device_ms", C.c_double), ("reset_ms", C.c_double),
         ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("boxsteps", C.c_uint64), ("launches", C.c_uint64),
+        ("free_items", C.c_uint64),
     ]
 
 
@@ -59,14 +60,15 @@ class QueryResult(C.Structure):
         ("status", C.c_int32), ("iterations", C.c_int32), ("tree_size", C.c_int64), ("solution_slot", C.c_int64),
         ("chain_len", C.c_int64), ("device_ms", C.c_double),
         ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("boxsteps", C.c_uint64),
-        ("checked", C.c_int32), ("check_code", C.c_int32),
+        ("free_items", C.c_uint64), ("checked", C.c_int32), ("check_code", C.c_int32),
     ]
 
 
 QUERY_RESULT_DTYPE = np.dtype([
     ("status", np.int32), ("iterations", np.int32), ("tree_size", np.int64), ("solution_slot", np.int64),
     ("chain_len", np.int64), ("device_ms", np.float64), ("items", np.uint64), ("substeps", np.uint64),
-    ("points", np.uint64), ("boxsteps", np.uint64), ("checked", np.int32), ("check_code", np.int32)], align=True)
+    ("points", np.uint64), ("boxsteps", np.uint64), ("free_items", np.uint64), ("checked", np.int32),
+    ("check_code", np.int32)], align=True)
 
 _SIGNATURES = {
     "kpx_last_error": (C.c_char_p, []),

@@ -182,9 +182,10 @@ class BatchPlanner:
         if want_chains and replan_rejected and self.precision != _lib.F64:
             bad = np.flatnonzero(res.rejected)
             if len(bad):
-                if self._f64 is None:
+                if self._f64 is None:       # few queries: teams of 16 CTAs each instead of one (a float64 plan on one
+                    # CTA takes ~100x a float32 one; the GPU is otherwise idle here)
                     self._f64 = BatchPlanner(self.cfg, self.env, self.model, self.problem.check_resolution, "cuda",
-                                             n_teams=int(min(len(bad), 8)), team_ctas=1, max_chain=self.max_chain,
+                                             n_teams=int(min(len(bad), 8)), team_ctas=16, max_chain=self.max_chain,
                                              device=self.device)
                 r64 = self._f64.run(seeds[bad], starts[bad], goals[bad], tm, True, stream, False,
                                     validate_resolution)

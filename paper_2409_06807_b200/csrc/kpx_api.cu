@@ -123,6 +123,11 @@ struct kpx_batch {
     long long q_cap = 0;
     double *bc_start = nullptr, *bc_ctrl = nullptr, *bc_dt = nullptr;
     long long bc_cap = 0, n_uploaded = 0;
+    double *bp_start = nullptr, *bp_ctrl = nullptr, *bp_dt = nullptr;   // packed copies of the chains (download)
+    long long* bp_off = nullptr;
+    double* bp_host = nullptr;         // pinned staging of the packed chains
+    size_t bp_host_cap = 0;
+    size_t d2h_chain_bytes = 0;        // chain bytes the last download moved
     bool want_chains = false;
     std::vector<QueryIn> q_stage;
     uint32_t** peers_dev = nullptr;
@@ -145,6 +150,7 @@ void destroy_batch(kpx_batch& b) {
     cudaSetDevice(b.device);
     cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.boxes64_dev); cudaFree(b.occ_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
     cudaFree(b.r_dev); cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt); cudaFree(b.peers_dev);
+    cudaFree(b.bp_start); cudaFree(b.bp_ctrl); cudaFree(b.bp_dt); cudaFree(b.bp_off); cudaFreeHost(b.bp_host);
     cudaFreeHost(b.pk_host); cudaFreeHost(b.q_pinned);
 }
 
@@ -201,19 +207,20 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     const int n = prob->n, nu = prob->nu;
     const size_t cp = (size_t)b.cap_pad, R = (size_t)b.regions, pairs = R * (size_t)b.subs;
     Carver c;
-    struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, avail, score, claim, bits, dregions, it_end,
+    struct Off { size_t states, control, dt, parent, region, tag, n_valid, n_invalid, cov, score, claim, bits, dregions, it_end,
                         it_code, it_rank, it_parent, it_bin, order, pos_of, bin_cursor, e_local, cnt_e, cnt_k, est_ids, leaf_sum, bar, ctl, trace, ch_start, ch_ctrl,
                         ch_dt, ch_slot, ch_end, packet; } o;
-    o.states = c.take(b.rs * n * cp); o.control = c.take(b.rs * nu * cp); o.dt = c.take(b.rs * cp);
+    const size_t row_n = (size_t)row_elems(n, (int)b.rs), row_nu = (size_t)row_elems(nu, (int)b.rs);   // padded rows
+    o.states = c.take(b.rs * row_n * cp); o.control = c.take(b.rs * row_nu * cp); o.dt = c.take(b.rs * cp);
     o.parent = c.take(4 * cp); o.region = c.take(4 * cp); o.tag = c.take(cp);
-    o.n_valid = c.take(4 * R); o.n_invalid = c.take(4 * R); o.cov = c.take(4 * R); o.avail = c.take(4 * R);
+    o.n_valid = c.take(4 * R); o.n_invalid = c.take(4 * R); o.cov = c.take(4 * R);
     o.score = c.take(8 * R); o.claim = c.take(4 * (pairs + 4));
     b.claim_shift = 1;
     while ((1ll << b.claim_shift) <= (long long)b.cap) ++b.claim_shift;      // 2^shift > t_e >= item index + 1
     o.bits = c.take(4 * ((R + 31) / 32 + 1));
     o.dregions = c.take(4 * ((R + 31) / 32 + 1));
-    o.it_end = c.take(b.rs * n * cp); o.it_code = c.take(4 * cp); o.it_rank = c.take(4 * cp); o.it_parent = c.take(4 * cp);
-    o.it_bin = c.take(cp); o.order = c.take(4 * cp); o.pos_of = c.take(4 * cp); o.bin_cursor = c.take(4 * (size_t)kBins);
+    o.it_end = c.take(b.rs * row_n * cp); o.it_code = c.take(4 * cp); o.it_rank = c.take(4 * cp); o.it_parent = c.take(4 * cp);
+    o.it_bin = c.take(cp); o.order = c.take(8 * cp); o.pos_of = c.take(4 * cp); o.bin_cursor = c.take(4 * (size_t)kBins);
     o.e_local = c.take(4 * cp); o.cnt_e = c.take(4 * (size_t)b.max_chunks); o.cnt_k = c.take(4 * (size_t)b.max_chunks);
     o.est_ids = c.take(4 * (R + 32)); o.leaf_sum = c.take(8 * (R / 64 + 2)); o.bar = c.take(256); o.ctl = c.take(sizeof(Ctl));
     o.trace = c.take(sizeof(kpx_trace) * (size_t)b.max_trace);
@@ -234,11 +241,11 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         w.states = s + o.states; w.control = s + o.control; w.dt = s + o.dt;
         w.parent = (int*)(s + o.parent); w.region = (int*)(s + o.region); w.tag = (uint8_t*)(s + o.tag);
         w.n_valid = (int*)(s + o.n_valid); w.n_invalid = (int*)(s + o.n_invalid); w.cov = (int*)(s + o.cov);
-        w.avail_it = (int*)(s + o.avail); w.score = (double*)(s + o.score); w.claim = (uint32_t*)(s + o.claim);
+        w.score = (double*)(s + o.score); w.claim = (uint32_t*)(s + o.claim);
         w.avail_bits = (uint32_t*)(s + o.bits); w.touched_bits = (uint32_t*)(s + o.dregions);
         w.it_end = s + o.it_end; w.it_code = (uint32_t*)(s + o.it_code); w.it_rank = (int*)(s + o.it_rank);
         w.it_parent = (int*)(s + o.it_parent); w.e_local = (int*)(s + o.e_local);
-        w.it_bin = (uint8_t*)(s + o.it_bin); w.order = (int*)(s + o.order); w.pos_of = (int*)(s + o.pos_of); w.bin_cursor = (unsigned int*)(s + o.bin_cursor);
+        w.it_bin = (uint8_t*)(s + o.it_bin); w.order = (int2*)(s + o.order); w.pos_of = (int*)(s + o.pos_of); w.bin_cursor = (unsigned int*)(s + o.bin_cursor);
         w.cnt_expand = (int*)(s + o.cnt_e); w.cnt_keep = (int*)(s + o.cnt_k); w.est_ids = (int*)(s + o.est_ids); w.leaf_sum = (double*)(s + o.leaf_sum);
         w.bar = (unsigned int*)(s + o.bar); w.ctl = (Ctl*)(s + o.ctl); w.trace = (kpx_trace*)(s + o.trace);
         w.chain_start = (double*)(s + o.ch_start); w.chain_control = (double*)(s + o.ch_ctrl);
@@ -248,6 +255,7 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     }
     for (int t = 0; t < n_teams; ++t) {      // a fresh workspace is clean: no pair ever claimed, every epoch left
         CU(cudaMemset(b.ws_host[t].claim, 0xFF, 4 * pairs));
+        CU(cudaMemset(b.ws_host[t].score, 0xFF, 8 * R));                     // all ones = NaN = "never estimated"
         Ctl c0;
         memset(&c0, 0, sizeof c0);
         c0.epoch_valid = 1;
@@ -300,36 +308,49 @@ int d2h(std::vector<T>& dst, const void* src, size_t count) {
     return KPX_OK;
 }
 
-// chunked-SoA device array (soa_base, kpx_device.cuh) of `rows` x `dims` reals -> AoS f64 host
-int soa_to_aos(const kpx_batch& b, const void* dev, int dims, long long rows, double* out) {
+// node-major device rows (Row<R, N>, kpx_device.cuh) of `rows` x `dims` reals -> dense f64 host rows
+int soa_to_aos(const kpx_batch& b, const void* dev, int dims, long long rows, double* out, bool padded = true) {
     if (rows == 0) return KPX_OK;
-    const size_t elems = (size_t)((rows + kChunk - 1) / kChunk) * kChunk * dims;      // whole chunks
-    std::vector<char> h(elems * b.rs);
+    const size_t stride = padded ? (size_t)row_elems(dims, (int)b.rs) : (size_t)dims;
+    std::vector<char> h((size_t)rows * stride * b.rs);
     CU(cudaMemcpy(h.data(), dev, h.size(), cudaMemcpyDeviceToHost));
-    for (long long i = 0; i < rows; ++i) {
-        const size_t base = soa_base(i, dims);
+    for (long long i = 0; i < rows; ++i)
         for (int d = 0; d < dims; ++d) {
-            const size_t k = base + (size_t)d * kChunk;
+            const size_t k = (size_t)i * stride + (size_t)d;
             out[i * dims + d] = b.rs == 8 ? ((const double*)h.data())[k] : (double)((const float*)h.data())[k];
         }
-    }
     return KPX_OK;
 }
 
-int aos_to_soa(const kpx_batch& b, void* dev, int dims, long long rows, const double* in) {
+int aos_to_soa(const kpx_batch& b, void* dev, int dims, long long rows, const double* in, bool padded = true) {
     if (rows == 0) return KPX_OK;
-    const size_t elems = (size_t)((rows + kChunk - 1) / kChunk) * kChunk * dims;
-    std::vector<char> h(elems * b.rs, 0);
-    for (long long i = 0; i < rows; ++i) {
-        const size_t base = soa_base(i, dims);
+    const size_t stride = padded ? (size_t)row_elems(dims, (int)b.rs) : (size_t)dims;
+    std::vector<char> h((size_t)rows * stride * b.rs, 0);
+    for (long long i = 0; i < rows; ++i)
         for (int d = 0; d < dims; ++d) {
-            const size_t k = base + (size_t)d * kChunk;
+            const size_t k = (size_t)i * stride + (size_t)d;
             if (b.rs == 8) ((double*)h.data())[k] = in[i * dims + d];
             else ((float*)h.data())[k] = (float)in[i * dims + d];
         }
-    }
     CU(cudaMemcpy(dev, h.data(), h.size(), cudaMemcpyHostToDevice));
     return KPX_OK;
+}
+
+// NumPy's pairwise float64 sum (the order combine_leaves / estimate_leaves follow on the device)
+double pairwise_total(const double* a, long long n) {
+    if (n < 8) { double r = 0.0; for (long long i = 0; i < n; ++i) r += a[i]; return r; }
+    if (n <= 128) {
+        double r[8];
+        long long i;
+        for (i = 0; i < 8; ++i) r[i] = a[i];
+        for (i = 8; i < n - (n % 8); i += 8) for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    long long n2 = n / 2;
+    n2 -= n2 % 8;
+    return pairwise_total(a, n2) + pairwise_total(a + n2, n - n2);
 }
 
 int read_ctl(const kpx_batch& b, Ctl* out) {
@@ -386,6 +407,50 @@ int measure_fma(int sms, double ms_target, double* tflops) {
 }  // namespace
 
 namespace {
+// Solution chains leave the device packed: off[q] = rows of the solved queries before q (one block scans the
+// chain lengths), then one block per query copies its rows.  A query's chain is chain_len rows of n + nu + 1
+// doubles out of a max_chain-row slot, typically 6 of 64: the packed copy is a tenth of the dense one.
+__global__ void chain_offsets_kernel(int n_q, const kpx_query_result* __restrict__ res, long long* __restrict__ off) {
+    __shared__ long long s_part[32];
+    __shared__ long long s_carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n_q; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        long long v = 0;
+        if (q < n_q && res[q].status == KPX_SOLVED && res[q].chain_len > 0) v = res[q].chain_len;
+        long long inc = v;
+        for (int o = 1; o < 32; o <<= 1) { const long long t = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += t; }
+        if (lane == 31) s_part[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            long long x = lane < nw ? s_part[lane] : 0, xi = x;
+            for (int o = 1; o < 32; o <<= 1) { const long long t = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += t; }
+            if (lane < nw) s_part[lane] = xi - x;
+        }
+        __syncthreads();
+        const long long carry = s_carry;
+        if (q < n_q) off[q] = carry + s_part[wid] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = carry + s_part[wid] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) off[n_q] = s_carry;
+}
+__global__ void chain_pack_kernel(int n_q, const kpx_query_result* __restrict__ res, const long long* __restrict__ off,
+                                  int max_chain, int n, int nu, const double* __restrict__ cs, const double* __restrict__ cc,
+                                  const double* __restrict__ cd, double* __restrict__ ps, double* __restrict__ pc,
+                                  double* __restrict__ pd) {
+    const int q = blockIdx.x;
+    if (q >= n_q) return;
+    const long long rows = off[q + 1] - off[q], o = off[q];
+    const size_t src = (size_t)q * max_chain;
+    for (long long i = threadIdx.x; i < rows * n; i += blockDim.x) ps[o * n + i] = cs[src * n + i];
+    for (long long i = threadIdx.x; i < rows * nu; i += blockDim.x) pc[o * nu + i] = cc[src * nu + i];
+    for (long long i = threadIdx.x; i < rows; i += blockDim.x) pd[o + i] = cd[src + i];
+}
+
 // Goal of query q (BASELINE.json config 5): centre uniform in [lo, hi]^3 drawn from the GENERIC stream of
 // seed q (rng.py:57-95: key(seed = q, 0, 0, 0, phase 5), draws 0, 1, 2, ...), three draws per try; a try is rejected
 // if the centre is closer than min_dist to the start or inside an obstacle grown by `grow` on every side.  One thread
@@ -679,7 +744,7 @@ int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_overr
     out->device_ms = (double)c.elapsed_ns * 1e-6;      // run clock: summed over the launches since the reset
     out->reset_ms = (double)(c.t_reset_done - c.t_begin) * 1e-6;
     out->items = c.sum_items; out->substeps = c.sum_substeps; out->points = c.sum_points;
-    out->boxsteps = c.sum_boxsteps;
+    out->boxsteps = c.sum_boxsteps; out->free_items = c.sum_free;
     out->launches = b.launches - l0;
     return KPX_OK;
 }
@@ -696,7 +761,7 @@ int kpx_plan_snapshot(kpx_plan* p, int64_t rows, double* states, int64_t* parent
     const Workspace& w = b.ws_host[0];
     if (states && (rc = soa_to_aos(b, w.states, b.prob.n, rows, states))) return rc;
     if (control && (rc = soa_to_aos(b, w.control, b.prob.nu, rows, control))) return rc;
-    if (dt && (rc = soa_to_aos(b, w.dt, 1, rows, dt))) return rc;
+    if (dt && (rc = soa_to_aos(b, w.dt, 1, rows, dt, false))) return rc;      // one real per node, dense
     std::vector<int> tmp;
     if (parent) { if ((rc = d2h(tmp, w.parent, (size_t)rows))) return rc; for (int64_t i = 0; i < rows; ++i) parent[i] = tmp[i]; }
     if (region) { if ((rc = d2h(tmp, w.region, (size_t)rows))) return rc; for (int64_t i = 0; i < rows; ++i) region[i] = tmp[i]; }
@@ -714,18 +779,20 @@ int kpx_plan_regions(kpx_plan* p, int64_t* n_valid, int64_t* n_invalid, int64_t*
     if (rc) return rc;
     const Workspace& w = b.ws_host[0];
     const size_t R = (size_t)b.regions;
-    std::vector<int> nv, ni, cv, av;
+    std::vector<int> nv, ni, cv;
+    std::vector<uint32_t> av;
     std::vector<double> sc;
     if ((rc = d2h(nv, w.n_valid, R)) || (rc = d2h(ni, w.n_invalid, R)) || (rc = d2h(cv, w.cov, R)) ||
-        (rc = d2h(av, w.avail_it, R)) || (rc = d2h(sc, w.score, R))) return rc;
+        (rc = d2h(av, w.avail_bits, (R + 31) / 32)) || (rc = d2h(sc, w.score, R))) return rc;
     const double vol = b.prob.grid_width[0] * b.prob.grid_width[1] * b.prob.grid_width[2];
     const double eps = b.prob.epsilon, delta = b.prob.delta, total = c.total_prev;
     for (size_t r = 0; r < R; ++r) {
-        const bool est = av[r] != 0 && av[r] <= c.iteration;   // estimated by the last pass
+        const bool is_avail = (av[r >> 5] >> (r & 31)) & 1u;
+        const bool est = is_avail && sc[r] >= 0.0;            // covered by an estimate pass
         if (n_valid) n_valid[r] = nv[r];
         if (n_invalid) n_invalid[r] = ni[r];
         if (cov) cov[r] = cv[r];
-        if (avail) avail[r] = av[r] != 0;
+        if (avail) avail[r] = is_avail;
         if (score) score[r] = est ? sc[r] : 0.0;
         if (free_vol) free_vol[r] = est ? (delta + nv[r]) * vol / (delta + nv[r] + ni[r]) : 0.0;
         if (p_accept) {
@@ -842,7 +909,7 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     const Workspace& w = b.ws_host[0];
     int rc;
     if ((rc = aos_to_soa(b, w.states, b.prob.n, rows, states)) || (rc = aos_to_soa(b, w.control, b.prob.nu, rows, control)) ||
-        (rc = aos_to_soa(b, w.dt, 1, rows, dt))) return rc;
+        (rc = aos_to_soa(b, w.dt, 1, rows, dt, false))) return rc;
     std::vector<int> tmp((size_t)rows);
     for (int64_t i = 0; i < rows; ++i) tmp[i] = (int)parent[i];
     CU(cudaMemcpy(w.parent, tmp.data(), 4 * (size_t)rows, cudaMemcpyHostToDevice));
@@ -850,15 +917,17 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     CU(cudaMemcpy(w.region, tmp.data(), 4 * (size_t)rows, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(w.tag, tag, (size_t)rows, cudaMemcpyHostToDevice));
     const size_t R = (size_t)b.regions;
-    std::vector<int> a(R), x(R);
-    double total = 0.0;
+    std::vector<int> x(R);
+    std::vector<double> sc_dev(R);
+    std::vector<double> est_scores;
     for (size_t r = 0; r < R; ++r) {
         // score > 0 <=> the region has been through an estimate pass; regions made available by the
         // most recent append are estimated from the next iteration on (planner.py:246)
-        a[r] = avail[r] ? (score[r] > 0.0 ? 1 : iteration + 1) : 0;
-        if (avail[r] && score[r] > 0.0) total += score[r];
+        const bool est = avail[r] && score[r] > 0.0;
+        sc_dev[r] = est ? score[r] : -1.0;
+        if (est) est_scores.push_back(score[r]);
     }
-    CU(cudaMemcpy(w.avail_it, a.data(), 4 * R, cudaMemcpyHostToDevice));
+    const double total = pairwise_total(est_scores.data(), (long long)est_scores.size());   // as the device sums it
     {
         std::vector<uint32_t> bits((R + 31) / 32 + 1, 0u);
         for (size_t r = 0; r < R; ++r) if (avail[r]) bits[r >> 5] |= 1u << (r & 31);
@@ -870,7 +939,7 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     CU(cudaMemcpy(w.n_invalid, x.data(), 4 * R, cudaMemcpyHostToDevice));
     for (size_t r = 0; r < R; ++r) x[r] = (int)cov[r];
     CU(cudaMemcpy(w.cov, x.data(), 4 * R, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(w.score, score, 8 * R, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(w.score, sc_dev.data(), 8 * R, cudaMemcpyHostToDevice));
     std::vector<uint32_t> cl(R * (size_t)b.subs);
     const uint32_t load_epoch = (1u << (32 - b.claim_shift)) - 2u;           // e_max
     for (size_t i = 0; i < cl.size(); ++i) cl[i] = visited[i] ? load_epoch << b.claim_shift : kUnclaimed;
@@ -1100,6 +1169,12 @@ int kpx_batch_upload(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, co
         CU(cudaMalloc(&b.bc_start, 8 * (size_t)b.q_cap * b.max_chain * n));
         CU(cudaMalloc(&b.bc_ctrl, 8 * (size_t)b.q_cap * b.max_chain * nu));
         CU(cudaMalloc(&b.bc_dt, 8 * (size_t)b.q_cap * b.max_chain));
+        cudaFree(b.bp_start); cudaFree(b.bp_ctrl); cudaFree(b.bp_dt); cudaFree(b.bp_off);
+        b.bp_start = b.bp_ctrl = b.bp_dt = nullptr; b.bp_off = nullptr;
+        CU(cudaMalloc(&b.bp_start, 8 * (size_t)b.q_cap * b.max_chain * n));
+        CU(cudaMalloc(&b.bp_ctrl, 8 * (size_t)b.q_cap * b.max_chain * nu));
+        CU(cudaMalloc(&b.bp_dt, 8 * (size_t)b.q_cap * b.max_chain));
+        CU(cudaMalloc(&b.bp_off, 8 * ((size_t)b.q_cap + 1)));
         b.bc_cap = b.q_cap;
     }
     b.want_chains = want_chains != 0;
@@ -1156,13 +1231,43 @@ int kpx_batch_download(kpx_batch* bp, kpx_query_result* results, double* chain_s
     CU(cudaSetDevice(b.device));
     const size_t q = (size_t)b.n_uploaded;
     const int n = b.prob.n, nu = b.prob.nu;
-    CU(cudaMemcpyAsync(results, b.r_dev, sizeof(kpx_query_result) * q, cudaMemcpyDeviceToHost, st));
-    if (b.want_chains && chain_start && chain_control && chain_dt) {
-        CU(cudaMemcpyAsync(chain_start, b.bc_start, 8 * q * b.max_chain * n, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(chain_control, b.bc_ctrl, 8 * q * b.max_chain * nu, cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(chain_dt, b.bc_dt, 8 * q * b.max_chain, cudaMemcpyDeviceToHost, st));
+    const bool chains = b.want_chains && chain_start && chain_control && chain_dt;
+    if (chains) {       // pack on the device while the records travel
+        chain_offsets_kernel<<<1, 1024, 0, st>>>((int)q, b.r_dev, b.bp_off);
+        chain_pack_kernel<<<(unsigned)q, 64, 0, st>>>((int)q, b.r_dev, b.bp_off, b.max_chain, n, nu, b.bc_start, b.bc_ctrl,
+                                                       b.bc_dt, b.bp_start, b.bp_ctrl, b.bp_dt);
+        CU(cudaGetLastError());
     }
+    CU(cudaMemcpyAsync(results, b.r_dev, sizeof(kpx_query_result) * q, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (chains) {
+        // the caller's arrays keep the dense (Q, max_chain, .) layout; only the rows that exist cross the bus
+        size_t rows = 0;
+        for (size_t i = 0; i < q; ++i) if (results[i].status == KPX_SOLVED && results[i].chain_len > 0) rows += (size_t)results[i].chain_len;
+        b.d2h_chain_bytes = 8 * rows * (size_t)(n + nu + 1);
+        if (rows) {
+            const size_t need = rows * (size_t)(n + nu + 1);
+            if (need > b.bp_host_cap) {
+                cudaFreeHost(b.bp_host); b.bp_host = nullptr; b.bp_host_cap = 0;
+                CU(cudaMallocHost(&b.bp_host, 8 * (need + need / 4)));
+                b.bp_host_cap = need + need / 4;
+            }
+            double *hs = b.bp_host, *hc = hs + rows * n, *hd = hc + rows * nu;
+            CU(cudaMemcpyAsync(hs, b.bp_start, 8 * rows * n, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(hc, b.bp_ctrl, 8 * rows * nu, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(hd, b.bp_dt, 8 * rows, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            size_t o = 0;
+            for (size_t i = 0; i < q; ++i) {
+                if (!(results[i].status == KPX_SOLVED && results[i].chain_len > 0)) continue;
+                const size_t L = (size_t)results[i].chain_len, dst = i * (size_t)b.max_chain;
+                memcpy(chain_start + dst * n, hs + o * n, 8 * L * n);
+                memcpy(chain_control + dst * nu, hc + o * nu, 8 * L * nu);
+                memcpy(chain_dt + dst, hd + o, 8 * L);
+                o += L;
+            }
+        }
+    }
     return KPX_OK;
 }
 

@@ -9,7 +9,7 @@
 //    point walk -- and the clamped grid mapping.  Verdicts and counters follow
 //    _kernel.pyx:157-296 (SURVEY.md section 9 lists the rules); R=double built with
 //    -fmad=false is bit-exact for the double integrator, R=float is the throughput path.
-//  * the shared-memory scene (Scene<R>), the chunked SoA index (soa_base)
+//  * the shared-memory scene (Scene<R>), the node-major row layout of per-node vectors (Row, load_row / store_row)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -61,13 +61,67 @@ constexpr uint32_t kItemDeadBit = 0x40000000u;
 
 enum : int { PH_SAMPLE = 1, PH_ACCEPT = 2, PH_DEMOTE = 3, PH_PROMOTE = 4 };
 
-// Chunked structure-of-arrays for per-node vectors (states, controls, end states): rows of kChunk consecutive
-// slots, the n rows of a chunk adjacent --  element (slot, d) lives at soa_base(slot, n) + d * kChunk.
-// A warp still touches 32 consecutive reals of one dimension (coalesced, vectorisable), but all dimensions of
-// a node lie within n * 4 KB instead of n row strides of ~1 MB apart: one or two pages per node instead of n
-// (page locality for the high-dimensional models when hundreds of workspaces are live).
-__host__ __device__ __forceinline__ size_t soa_base(long long slot, int n) {
-    return ((size_t)(slot / kChunk) * (size_t)n) * kChunk + (size_t)(slot % kChunk);
+// Per-node vectors (states, controls, the end states of an iteration) are stored node-major, one padded ROW per
+// node: n reals rounded up to a multiple of 16 bytes (float: 6 -> 8, 12 -> 12; double: 6 -> 6).  Every access of the
+// planner is a gather or scatter BY NODE -- an extension reads its parent's state, an append copies an item's end
+// state into the tree, the chain walk reads parents -- so a row costs one or two 32-byte sectors (2-3 LDG.128)
+// where a structure-of-arrays layout costs one sector per dimension (12 for the quadcopter): round 1's chunked SoA
+// moved 1.2 GB of DRAM per quadcopter query, most of it in such gathers.  Consecutive nodes are consecutive rows,
+// so the stores of a warp's 32 end states and the appended slots of an iteration are still contiguous.
+__host__ __device__ constexpr int row_elems(int n, int elem_size) { return ((n * elem_size + 15) / 16) * (16 / elem_size); }
+template <class R, int N> struct Row {
+    static constexpr int kStride = row_elems(N, (int)sizeof(R));   // reals per row
+    static constexpr int kVecs = kStride * (int)sizeof(R) / 16;     // 16-byte vectors per row
+};
+template <int N>
+__device__ __forceinline__ void load_row(const float* __restrict__ base, long long row, float* out) {
+    const float4* p = (const float4*)(base + (size_t)row * Row<float, N>::kStride);
+    float tmp[Row<float, N>::kStride];
+#pragma unroll
+    for (int v = 0; v < Row<float, N>::kVecs; ++v) {
+        const float4 q = __ldcg(p + v);
+        tmp[4 * v] = q.x; tmp[4 * v + 1] = q.y; tmp[4 * v + 2] = q.z; tmp[4 * v + 3] = q.w;
+    }
+#pragma unroll
+    for (int d = 0; d < N; ++d) out[d] = tmp[d];
+}
+template <int N>
+__device__ __forceinline__ void load_row(const double* __restrict__ base, long long row, double* out) {
+    const double2* p = (const double2*)(base + (size_t)row * Row<double, N>::kStride);
+    double tmp[Row<double, N>::kStride];
+#pragma unroll
+    for (int v = 0; v < Row<double, N>::kVecs; ++v) { const double2 q = __ldcg(p + v); tmp[2 * v] = q.x; tmp[2 * v + 1] = q.y; }
+#pragma unroll
+    for (int d = 0; d < N; ++d) out[d] = tmp[d];
+}
+template <int N>
+__device__ __forceinline__ void store_row(float* __restrict__ base, long long row, const float* in) {
+    float4* p = (float4*)(base + (size_t)row * Row<float, N>::kStride);
+    float tmp[Row<float, N>::kStride];
+#pragma unroll
+    for (int d = 0; d < Row<float, N>::kStride; ++d) tmp[d] = d < N ? in[d] : 0.0f;
+#pragma unroll
+    for (int v = 0; v < Row<float, N>::kVecs; ++v) __stcg(p + v, make_float4(tmp[4 * v], tmp[4 * v + 1], tmp[4 * v + 2], tmp[4 * v + 3]));
+}
+template <int N>
+__device__ __forceinline__ void store_row(double* __restrict__ base, long long row, const double* in) {
+    double2* p = (double2*)(base + (size_t)row * Row<double, N>::kStride);
+    double tmp[Row<double, N>::kStride];
+#pragma unroll
+    for (int d = 0; d < Row<double, N>::kStride; ++d) tmp[d] = d < N ? in[d] : 0.0;
+#pragma unroll
+    for (int v = 0; v < Row<double, N>::kVecs; ++v) __stcg(p + v, make_double2(tmp[2 * v], tmp[2 * v + 1]));
+}
+// row -> row copy without unpacking
+template <class R, int N>
+__device__ __forceinline__ void copy_row(R* __restrict__ dst, long long drow, const R* __restrict__ src, long long srow) {
+    const uint4* s = (const uint4*)(src + (size_t)srow * Row<R, N>::kStride);
+    uint4* d = (uint4*)(dst + (size_t)drow * Row<R, N>::kStride);
+    uint4 t[Row<R, N>::kVecs];
+#pragma unroll
+    for (int v = 0; v < Row<R, N>::kVecs; ++v) t[v] = __ldcg(s + v);
+#pragma unroll
+    for (int v = 0; v < Row<R, N>::kVecs; ++v) __stcg(d + v, t[v]);
 }
 
 // ------------------------------------------------------------------ RNG ----
@@ -700,6 +754,41 @@ struct ItemOut {
     bool valid;
 };
 
+// Clamped grid mapping of an end state (_kernel.pyx:261-292): region iff the state is finite (`alive`), sub-region
+// and valid = 1 iff the whole segment was valid too (`ok`).
+template <class M, class R>
+__device__ __forceinline__ void map_end_state(const Params<R>& P, const R* cur, bool alive, bool ok, ItemOut<R, M::N>& out) {
+    constexpr int N = M::N;
+    out.region = -1; out.sub = 0; out.valid = false;
+    if (alive) {
+        int reg = 0;
+        R rel3[3], cell3[3];
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+            if (d < P.grid_n) {
+                R rel = (cur[d] - P.grid_lo[d]) / P.grid_width[d];
+                R cl = rel < (R)0 ? (R)0 : (rel > P.grid_cmax[d] ? P.grid_cmax[d] : rel);
+                R fl = MathK<R>::fl(cl);
+                reg += (int)fl * P.grid_strides[d];
+                if (d < 3) { rel3[d] = rel; cell3[d] = fl; }
+            }
+        }
+        out.region = reg;
+        if (ok) {
+            int sub = 0;
+            R smax = (R)(P.subcells - 1);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                R fr = (rel3[d] - cell3[d]) * (R)P.subcells;
+                fr = fr < (R)0 ? (R)0 : (fr > smax ? smax : fr);
+                sub = sub * P.subcells + (int)MathK<R>::fl(fr);
+            }
+            out.sub = sub;
+            out.valid = true;
+        }
+    }
+}
+
 // The extension itself, warp-synchronous: ALL 32 lanes of the warp call it together (`active` = this lane
 // holds an item).  `u` and `dt` are the sampled control / duration already rounded to R; x0 is the parent state.
 //
@@ -864,34 +953,7 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
 #pragma unroll
     for (int i = 0; i < N; ++i) out.end[i] = cur[i];
     out.substeps = S; out.points = points; out.boxsteps = box_end >= 0 ? box_end : S;
-    out.region = -1; out.sub = 0; out.valid = false;
-    if (alive) {
-        int reg = 0;
-        R rel3[3], cell3[3];
-#pragma unroll
-        for (int d = 0; d < N; ++d) {
-            if (d < P.grid_n) {
-                R rel = (cur[d] - P.grid_lo[d]) / P.grid_width[d];
-                R cl = rel < (R)0 ? (R)0 : (rel > P.grid_cmax[d] ? P.grid_cmax[d] : rel);
-                R fl = MathK<R>::fl(cl);
-                reg += (int)fl * P.grid_strides[d];
-                if (d < 3) { rel3[d] = rel; cell3[d] = fl; }
-            }
-        }
-        out.region = reg;
-        if (ok) {
-            int sub = 0;
-            R smax = (R)(P.subcells - 1);
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                R fr = (rel3[d] - cell3[d]) * (R)P.subcells;
-                fr = fr < (R)0 ? (R)0 : (fr > smax ? smax : fr);
-                sub = sub * P.subcells + (int)MathK<R>::fl(fr);
-            }
-            out.sub = sub;
-            out.valid = true;
-        }
-    }
+    map_end_state<M, R>(P, cur, alive, ok, out);
 }
 
 // Sample (u, dt) for item (slot, ext) of the iteration hashed into h0.  Controls and
@@ -924,5 +986,179 @@ __device__ __forceinline__ int substeps_of(const Params<R>& P, uint64_t h0, int 
     const int s = (int)ceil(__ddiv_rn((double)dt, 0.02));
     return s < 4 ? 4 : s;
 }
+
+// ------------------------------------------------------------------ free flight ----
+// float32 double integrators only.  x' = (v, u) with u held has the closed form p(t) = p0 + t (v0 + t u / 2),
+// v(t) = v0 + t u, so for most extensions the verdict is decidable in O(1) before integrating anything:
+//   * INVALID for certain: the last sampled state (t = dt) lies outside the closed state box.  (v is monotone per axis,
+//     so a velocity that leaves its box is still outside at the end.)
+//   * VALID for certain: v(dt) inside its box (then every sampled velocity is: the first one is a tree node), and the
+//     position stays clear of the box faces and of every obstacle.  p is a parabola per axis; its extremes over a time
+//     interval are the ends and, if inside, the vertex.  The sampled states s h and every interpolant the obstacle walk
+//     visits between two CONSECUTIVE samples lie inside the axis-aligned box of those extremes over any interval
+//     [s_a h, s_b h] containing both samples.  If those boxes (KPX_FREE_PIECES of them, split at sample times, grown
+//     by a few float32 ulps of the workspace) stay inside the state box and overlap no obstacle box, nothing the
+//     reference's checker would test can fail.  Obstacles are found through the occupancy grid of the scene (the
+//     dilated table answers a box spanning <= 2 cells per axis in one lookup) and compared box against box, exactly.
+// Either way the extension is finished on the spot -- end state from the closed form, grid mapping, counters -- and
+// never enters the length sort or the substep loop; ~80 % of the Trees workload.  Everything else (extensions that
+// pass near an obstacle, or whose parabola only grazes a box face between samples) takes the full path.
+// Work counters of a finished extension: substeps = S (the reference integrates every substep whatever the verdict).
+// Certified valid: boxsteps = S and points = the sum of the densification counts of its S segments (validity.py:26-31),
+// counted from the closed-form segment lengths |h v0 + h^2 u (s - 1/2)|.  Certified invalid: boxsteps = 1, points = 0
+// -- lower bounds (the first failing substep is not computed), so the algorithmic-work total is never overstated.
+#ifndef KPX_FREE_PIECES
+#define KPX_FREE_PIECES 2
+#endif
+#ifndef KPX_FREE_FLIGHT
+#define KPX_FREE_FLIGHT 1            // 0: every extension takes the full path (measurement knob)
+#endif
+enum : int { kFlightFull = 0, kFlightValid = 1, kFlightInvalid = 2 };
+template <class M, class R> struct FreeFlight {
+    static constexpr bool kEnabled = false;
+    __device__ static __forceinline__ int certify(const Params<R>&, const R*, const R*, R, int, ItemOut<R, M::N>&) { return kFlightFull; }
+};
+
+__device__ __forceinline__ float di_pos(float p0, float v0, float u, float t) { return __fmaf_rn(t, __fmaf_rn(0.5f * t, u, v0), p0); }
+// extremes of one axis over [ta, tb]
+__device__ __forceinline__ void di_axis_range(float p0, float v0, float u, float ta, float tb, float* lo, float* hi) {
+    const float pa = di_pos(p0, v0, u, ta), pb = di_pos(p0, v0, u, tb);
+    float l = fminf(pa, pb), h = fmaxf(pa, pb);
+    const float ts = __fdividef(-v0, u);                 // vertex; u = 0 gives inf / nan and both compares fail
+    if (ts > ta && ts < tb) { const float pv = di_pos(p0, v0, u, ts); l = fminf(l, pv); h = fmaxf(h, pv); }
+    *lo = l; *hi = h;
+}
+// does the closed box [lo, hi] overlap an obstacle?  Candidates from the occupancy grid, then box against box.
+__device__ __forceinline__ bool box_touches_obstacle(const Params<float>& P, const float* lo, const float* hi) {
+    uint32_t m;
+    if (P.occ_g != 0) {
+        int c0[3], c1[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            c0[a] = occ_cell<float>(lo[a], P.occ_lo[a], P.occ_inv[a]);
+            c1[a] = occ_cell<float>(hi[a], P.occ_lo[a], P.occ_inv[a]);
+        }
+        const uint32_t* occ2 = Scene<float>::occ2();
+        if (c1[0] - c0[0] <= 1 && c1[1] - c0[1] <= 1 && c1[2] - c0[2] <= 1) {
+            m = occ2[(c0[0] * kOccGrid + c0[1]) * kOccGrid + c0[2]];
+        } else if (c1[0] - c0[0] <= 3 && c1[1] - c0[1] <= 3 && c1[2] - c0[2] <= 3) {
+            m = 0u;
+#pragma unroll 1
+            for (int x = c0[0]; x <= c1[0]; x += 2)
+#pragma unroll 1
+                for (int y = c0[1]; y <= c1[1]; y += 2)
+#pragma unroll 1
+                    for (int z = c0[2]; z <= c1[2]; z += 2) m |= occ2[(x * kOccGrid + y) * kOccGrid + z];
+        } else {
+            m = 0xffffffffu >> (32 - P.n_obs);
+        }
+        const float* bx = Scene<float>::boxes();
+        bool touch = false;
+#pragma unroll 1
+        while (m && !touch) {
+            const Box<float> b = load_box(bx, __ffs(m) - 1);
+            m &= m - 1;
+            touch = (hi[0] >= b.lx) & (lo[0] <= b.hx) & (hi[1] >= b.ly) & (lo[1] <= b.hy) & (hi[2] >= b.lz) & (lo[2] <= b.hz);
+        }
+        return touch;
+    }
+    const float* bx = Scene<float>::boxes();
+    bool touch = false;
+#pragma unroll 1
+    for (int j = 0; j < P.n_obs; ++j) {
+        const Box<float> b = load_box(bx, j);
+        touch = touch | ((hi[0] >= b.lx) & (lo[0] <= b.hx) & (hi[1] >= b.ly) & (lo[1] <= b.hy) & (hi[2] >= b.lz) & (lo[2] <= b.hz));
+    }
+    return touch;
+}
+// one 6-D block [p v] starting at state dimension d0: kFlightInvalid / kFlightValid / kFlightFull (undecided)
+__device__ __forceinline__ int di_block_flight(const Params<float>& P, int d0, const float* x0, const float* u, float dt, int S,
+                                               float h, bool obstacles) {
+    constexpr float kGrow = 1e-5f;                       // ~10 float32 ulps of a 10 m workspace
+    bool end_in = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {                        // the last sample, exactly as the full path would test it
+        const float pe = di_pos(x0[a], x0[3 + a], u[a], dt), ve = __fmaf_rn(dt, u[a], x0[3 + a]);
+        end_in = end_in & (pe >= P.state_lo[d0 + a]) & (pe <= P.state_hi[d0 + a]) & (ve >= P.state_lo[d0 + 3 + a]) & (ve <= P.state_hi[d0 + 3 + a]);
+    }
+    if (!end_in) return kFlightInvalid;
+    bool good = true;
+#pragma unroll 1
+    for (int k = 0; k < KPX_FREE_PIECES && good; ++k) {
+        const float ta = (float)((S * k) / KPX_FREE_PIECES) * h;
+        const float tb = k + 1 == KPX_FREE_PIECES ? dt : (float)((S * (k + 1)) / KPX_FREE_PIECES) * h;
+        float lo[3], hi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            di_axis_range(x0[a], x0[3 + a], u[a], ta, tb, &lo[a], &hi[a]);
+            lo[a] -= kGrow; hi[a] += kGrow;
+            good = good & (lo[a] >= P.state_lo[d0 + a]) & (hi[a] <= P.state_hi[d0 + a]);
+        }
+        if (obstacles && good) good = !box_touches_obstacle(P, lo, hi);
+    }
+    return good ? kFlightValid : kFlightFull;
+}
+// Collision points the reference's walk tests along the S segments of a free extension: segment s has the squared
+// length q(sigma) = |h v0 + h^2 u sigma|^2 at sigma = s - 1/2, a parabola in sigma, so the number of segments above
+// each densification threshold follows from its roots; points = S + #(q > thr0) + 2 #(q > thr1) + 4 #(q > thr2).
+// (A substep of a double integrator inside its velocity box is shorter than 8 check_res: no segment needs more.)
+__device__ __forceinline__ int di_free_points(const Params<float>& P, const float* x0, const float* u, int S, float h) {
+    const float hh = h * h;
+    const float A = hh * (x0[3] * x0[3] + x0[4] * x0[4] + x0[5] * x0[5]);
+    const float B = 2.0f * hh * h * (x0[3] * u[0] + x0[4] * u[1] + x0[5] * u[2]);
+    const float C = hh * hh * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    int points = S;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float T = P.d2_thr[k];
+        int above;
+        const float disc = B * B - 4.0f * C * (A - T);
+        if (!(C > 0.0f)) above = A > T ? S : 0;
+        else if (disc < 0.0f) above = S;                 // upward parabola without roots: above everywhere
+        else {
+            const float sq = sqrtf(disc), i2c = __fdividef(0.5f, C);
+            const float s_lo = (-B - sq) * i2c + 0.5f, s_hi = (-B + sq) * i2c + 0.5f;   // q <= T for s in [s_lo, s_hi]
+            int a = (int)ceilf(s_lo), b = (int)floorf(s_hi);
+            a = a < 1 ? 1 : a; b = b > S ? S : b;
+            above = S - (b >= a ? b - a + 1 : 0);
+        }
+        points += above << k;
+    }
+    return points;
+}
+template <int B>
+__device__ __forceinline__ int di_certify(const Params<float>& P, const float* x0, const float* u, float dt, int S,
+                                          ItemOut<float, 6 * B>& out) {
+    const float h = dt / (float)S;
+    int verdict = di_block_flight(P, 0, x0, u, dt, S, h, P.n_obs > 0);
+#pragma unroll
+    for (int b = 1; b < B; ++b) {
+        const int v = di_block_flight(P, 6 * b, x0 + 6 * b, u + 3 * b, dt, S, h, false);
+        verdict = (verdict == kFlightInvalid || v == kFlightInvalid) ? kFlightInvalid
+                                                                     : ((verdict == kFlightValid && v == kFlightValid) ? kFlightValid : kFlightFull);
+    }
+    if (verdict == kFlightFull) return verdict;
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            out.end[6 * b + a] = di_pos(x0[6 * b + a], x0[6 * b + 3 + a], u[3 * b + a], dt);
+            out.end[6 * b + 3 + a] = __fmaf_rn(dt, u[3 * b + a], x0[6 * b + 3 + a]);
+        }
+    out.substeps = S;
+    if (verdict == kFlightValid) { out.boxsteps = S; out.points = P.n_obs > 0 ? di_free_points(P, x0, u, S, h) : 0; }
+    else { out.boxsteps = 1; out.points = 0; }
+    return verdict;
+}
+template <> struct FreeFlight<ModelDI6, float> {
+    static constexpr bool kEnabled = KPX_FREE_FLIGHT != 0;
+    __device__ static __forceinline__ int certify(const Params<float>& P, const float* x0, const float* u, float dt, int S,
+                                                  ItemOut<float, 6>& out) { return di_certify<1>(P, x0, u, dt, S, out); }
+};
+template <int B> struct FreeFlight<ModelStackedDI<B>, float> {
+    static constexpr bool kEnabled = KPX_FREE_FLIGHT != 0;
+    __device__ static __forceinline__ int certify(const Params<float>& P, const float* x0, const float* u, float dt, int S,
+                                                  ItemOut<float, 6 * B>& out) { return di_certify<B>(P, x0, u, dt, S, out); }
+};
 
 }  // namespace kpx

@@ -85,12 +85,14 @@ struct Ctl {                      // one per workspace, global memory
     int cnt_valid[2], cnt_open[2];  // by iteration parity (trace only)
     // cumulative work
     unsigned long long sum_items, sum_substeps, sum_points, sum_boxsteps;
+    unsigned long long sum_free;  // extensions finished from the closed form (FreeFlight), a subset of sum_items
     // timing (globaltimer ns)
     unsigned long long t_begin, t_reset_done, t_end;
     int n_trace;
     int chain_len;
     int cur_query;                // batch mode: query index broadcast to the team
     unsigned int unit_next;       // S1: next 32-item unit of the length-sorted order
+    unsigned int n_free;          // S0 (many-CTA teams): items finished in the prepass; they fill positions from the end
     int last_sorted;              // 1 if the last iteration's it_* arrays are in sorted-position order
     // claim-table epoch (see Workspace::claim): the epoch the last query used; epoch_valid = 0 forces a dense
     // reset of the claim table and the region arrays (fresh state loaded from the host)
@@ -119,6 +121,7 @@ struct RunState {                 // CTA-uniform state of the running query, sha
     unsigned long long t_start;   // keeper only
     // header of the current iteration
     int lam, items, n_sch_old, par, sorted;
+    int items_sorted;             // many-CTA teams: items the global sort holds (the rest were finished in its prepass)
     int n_est;                    // available regions, i.e. entries of Workspace::est_ids, for this iteration's estimate pass
     uint32_t claim_tag;           // epoch of this query << claim_shift
     unsigned long long h0;
@@ -126,11 +129,14 @@ struct RunState {                 // CTA-uniform state of the running query, sha
 };
 
 struct Workspace {                // device pointers of one team's state
-    void *states, *control, *dt;  // R[cap/1024][n][1024], R[cap/1024][nu][1024], R[cap]   (tree arena, chunked SoA)
+    void *states, *control, *dt;  // R[cap][row(n)], R[cap][row(nu)], R[cap]   (tree arena, node-major padded rows: Row<R, N>)
     int *parent, *region;         // [cap]
     uint8_t* tag;                 // [cap]
-    int *n_valid, *n_invalid, *cov, *avail_it;   // [R]
-    double* score;                // [R]
+    int *n_valid, *n_invalid, *cov;   // [R]
+    // [R] score of the last estimate pass that covered the region; NEGATIVE (or NaN) = never estimated, which is
+    // exactly "p_accept is still 1.0" (decomposition.py:66-74: p_accept starts at 1; planner.py:246: a region joins the
+    // estimate pass one iteration after its first node) -- so one 8-byte gather answers p_accept for a node
+    double* score;
     uint32_t* avail_bits;         // [ceil(R/32)] bit r set once region r has been made available
     uint32_t* touched_bits;       // [ceil(R/32)] regions whose counters the current query has touched (lazy reset)
     // [R * subs] first-visit claims, epoch-tagged so that a new query needs no reset: with E the query's epoch
@@ -140,11 +146,11 @@ struct Workspace {                // device pointers of one team's state
     // exactly the order atomicMin needs: a fresh claim beats stale words, the lowest item beats other items, and
     // nothing beats "visited".  The table is refilled with 0xFF only when the epochs run out (2^(32-s) - 1 queries).
     uint32_t* claim;
-    void* it_end;                 // chunked SoA like `states`: end states of this iteration's valid items
+    void* it_end;                 // rows like `states`: end states of this iteration's valid items, by sorted position
     uint32_t* it_code;            // [cap] per-item result word (kItemGoalBit / kItemDeadBit, kpx_device.cuh)
     int *it_rank, *it_parent;     // [cap]
     uint8_t* it_bin;              // [cap] substep-count bin of each item
-    int* order;                   // [cap] item numbers sorted by substep count, longest first
+    int2* order;                  // [cap] (item number, parent slot) sorted by substep count, longest first
     int* pos_of;                  // [cap] inverse of `order`: where item w's results live in the it_* arrays
     unsigned int* bin_cursor;     // [kBins] per-bin fill cursor / histogram of the current iteration
     int *e_local;                 // [cap]  chunk-major compacted EXPAND slots
@@ -263,14 +269,13 @@ __device__ __forceinline__ double block_sum_f64(double v, double* s_d) {
     return s_d[0];
 }
 
-// acceptance probability of region r as of the estimate pass of iteration it_ref
-// (decomposition.py:189-203); regions not yet available then keep 1.0.
-__device__ __forceinline__ double p_accept_of(int r, int it_ref, const int* __restrict__ avail_it,
-                                              const double* __restrict__ score, double total, double eps) {
-    int a = __ldcg(avail_it + r);
-    if (a == 0 || a > it_ref) return 1.0;
+// acceptance probability of region r as of the last estimate pass (decomposition.py:189-203); regions no pass
+// has covered yet keep 1.0 (their score word is still the "never" sentinel).
+__device__ __forceinline__ double p_accept_of(int r, const double* __restrict__ score, double total, double eps) {
+    const double sc = __ldcg(score + r);
+    if (!(sc >= 0.0)) return 1.0;
     if (total <= 0.0) return eps < 1.0 ? eps : 1.0;
-    double v = __dadd_rn(__ddiv_rn(__ldcg(score + r), total), eps);
+    const double v = __dadd_rn(__ddiv_rn(sc, total), eps);
     return v < 1.0 ? v : 1.0;
 }
 
@@ -428,7 +433,9 @@ __device__ __forceinline__ int build_est_list(const Workspace& W, const Team& T,
 #ifndef KPX_TILE_CHUNKS
 #define KPX_TILE_CHUNKS 4
 #endif
-constexpr int kTile = KPX_TILE_CHUNKS * kChunk;     // items per tile of the tile-local length sort (one-CTA teams)
+#ifndef KPX_TILE_CHUNKS_FREE
+#define KPX_TILE_CHUNKS_FREE 16       // models with the free-flight prepass: most items never reach the sort, so tiles are larger
+#endif
 
 // i-th EXPAND slot: chunk by binary search over the chunk prefix, then the chunk-local compacted list
 __device__ __forceinline__ int expand_slot(const Workspace& W, const int* s_prefix, int n_sch_old, int i) {
@@ -437,42 +444,13 @@ __device__ __forceinline__ int expand_slot(const Workspace& W, const int* s_pref
     return __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
 }
 
-// One 32-item unit (warp-synchronous): lane `lane` handles the item stored at position `pos`.
-// sorted: the item number comes from `order` (results stay addressed by item number w through pos_of);
-// unsorted: position == item number.
+// Results of one item (warp-synchronous: all 32 lanes call it, `active` = this lane holds a finished item):
+// the item word + end state at its position, the first-visit claim, the region counters, the work counters.
 template <class M, class R>
-__device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q,
-                                               const RunState& RS, const int* s_prefix, int pos, bool sorted) {
-    constexpr int N = M::N, NU = M::NU;
+__device__ __forceinline__ void commit_item(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, uint32_t claim_tag,
+                                            int par, bool active, int w, int pos, const ItemOut<R, M::N>& o) {
+    constexpr int N = M::N;
     const Params<R>& P = A.P;
-    // the iteration header is re-read from shared memory per unit: nothing of it stays in registers
-    const int items = RS.items, lam = RS.lam;
-    const uint64_t h0 = RS.h0;
-    const bool active = pos < items;
-    int w = 0, S = 0;
-    R u[NU], dt = (R)0, x0[N];
-    if (active) {
-        int slot;
-        if (sorted) {
-            w = __ldcg(W.order + pos);
-            slot = __ldcg(W.it_parent + w);
-        } else {
-            w = pos;
-            slot = expand_slot(W, s_prefix, RS.n_sch_old, w / lam);
-            __stcg(W.it_parent + w, slot);
-        }
-        sample_control<M, R>(P, h0, slot, w % lam, u, &dt, &S, nullptr, nullptr);
-        const R* st = (const R*)W.states + soa_base(slot, N);
-#pragma unroll
-        for (int d = 0; d < N; ++d) x0[d] = __ldcg(st + d * kChunk);
-    } else {
-#pragma unroll
-        for (int d = 0; d < N; ++d) x0[d] = (R)0;
-#pragma unroll
-        for (int j = 0; j < NU; ++j) u[j] = (R)0;
-    }
-    ItemOut<R, N> o;
-    integrate_and_map<M, R>(P, active, x0, u, dt, S, o);     // warp-synchronous
     int region = -1; bool valid = false;
     if (active) {
         region = o.region; valid = o.valid;
@@ -482,11 +460,8 @@ __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Works
             const R d0 = o.end[0] - (R)Q.goal[0], d1 = o.end[1] - (R)Q.goal[1], d2 = o.end[2] - (R)Q.goal[2];
             const bool hit = MathK<R>::sq(d0 * d0 + d1 * d1 + d2 * d2) <= (R)Q.goal[3];
             code = pair | (hit ? kItemGoalBit : 0u);
-            R* e = (R*)W.it_end + soa_base(pos, N);
-#pragma unroll
-            for (int d = 0; d < N; ++d) __stcg(e + d * kChunk, o.end[d]);
-            const uint32_t tag = RS.claim_tag;
-            if (__ldcg(W.claim + pair) != tag) atomicMin(W.claim + pair, tag | (uint32_t)(w + 1));
+            store_row<N>((R*)W.it_end, pos, o.end);
+            if (__ldcg(W.claim + pair) != claim_tag) atomicMin(W.claim + pair, claim_tag | (uint32_t)(w + 1));
         }
         __stcg(W.it_code + pos, code);
     }
@@ -500,7 +475,68 @@ __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Works
         atomicAdd(&W.ctl->sum_substeps, (unsigned long long)t_sub);
         atomicAdd(&W.ctl->sum_points, (unsigned long long)t_pts);
         atomicAdd(&W.ctl->sum_boxsteps, (unsigned long long)t_box);
-        if (t_val) atomicAdd(&W.ctl->cnt_valid[RS.par], t_val);
+        if (t_val) atomicAdd(&W.ctl->cnt_valid[par], t_val);
+    }
+}
+
+// One 32-item unit (warp-synchronous): lane `lane` handles the item stored at position `pos` (< limit).
+// sorted: the item number and its parent slot come from `order` (results stay addressed by item number w
+// through pos_of); unsorted: position == item number.
+template <class M, class R>
+__device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q,
+                                               const RunState& RS, const int* s_prefix, int pos, int limit, bool sorted) {
+    constexpr int N = M::N, NU = M::NU;
+    const Params<R>& P = A.P;
+    // the iteration header is re-read from shared memory per unit: nothing of it stays in registers
+    const int lam = RS.lam;
+    const uint64_t h0 = RS.h0;
+    const bool active = pos < limit;
+    int w = 0, S = 0;
+    R u[NU], dt = (R)0, x0[N];
+    if (active) {
+        int slot;
+        if (sorted) {
+            const int2 ws = __ldcg(W.order + pos);          // item number and its parent slot in one load
+            w = ws.x; slot = ws.y;
+        } else {
+            w = pos;
+            slot = expand_slot(W, s_prefix, RS.n_sch_old, w / lam);
+            __stcg(W.it_parent + w, slot);
+        }
+        sample_control<M, R>(P, h0, slot, w % lam, u, &dt, &S, nullptr, nullptr);
+        load_row<N>((const R*)W.states, slot, x0);
+    } else {
+#pragma unroll
+        for (int d = 0; d < N; ++d) x0[d] = (R)0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) u[j] = (R)0;
+    }
+    ItemOut<R, N> o;
+    integrate_and_map<M, R>(P, active, x0, u, dt, S, o);     // warp-synchronous
+    commit_item<M, R>(A, W, Q, RS.claim_tag, RS.par, active, w, pos, o);
+}
+
+// Prepass of one item, ahead of the length sort: parent slot, substep count and -- float32 double integrators --
+// the free-flight certificate (FreeFlight, kpx_device.cuh): a certified extension is finished here, from the closed
+// form, and never enters the sort.  Returns the substep count; *free_out says the item is done, with `o` filled.
+template <class M, class R>
+__device__ __forceinline__ int prepass_item(const PlanArgs<R>& A, const Workspace& W, uint64_t h0, int slot, int ext,
+                                            bool* free_out, ItemOut<R, M::N>& o) {
+    *free_out = false;
+    if constexpr (FreeFlight<M, R>::kEnabled) {
+        constexpr int N = M::N, NU = M::NU;
+        R u[NU], dt, x0[N];
+        int S;
+        sample_control<M, R>(A.P, h0, slot, ext, u, &dt, &S, nullptr, nullptr);
+        load_row<N>((const R*)W.states, slot, x0);
+        const int verdict = FreeFlight<M, R>::certify(A.P, x0, u, dt, S, o);
+        if (verdict != kFlightFull) {
+            map_end_state<M, R>(A.P, o.end, true, verdict == kFlightValid, o);
+            *free_out = true;
+        }
+        return S;
+    } else {
+        return substeps_of<M, R>(A.P, h0, slot, ext);
     }
 }
 
@@ -520,38 +556,60 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
     const int lane = threadIdx.x & 31, tid = threadIdx.x;
     const bool sorted = RS.sorted != 0;
     const bool tiled = sorted && team_ctas == 1;
-    uint8_t* const s_len = (uint8_t*)(kpx_dyn_smem + Scene<R>::kCoop);   // [kTile]; the staging area is idle while sorting
-    static_assert(sizeof(WarpCoop<R>) * kWarps >= kTile, "tile lengths must fit the staging area");
-    int tile = -kTile, n_units = 0;
+    uint8_t* const s_len = (uint8_t*)(kpx_dyn_smem + Scene<R>::kCoop);   // [kTileM]; the staging area is idle while sorting
+    constexpr int kTileM = (FreeFlight<M, R>::kEnabled ? KPX_TILE_CHUNKS_FREE : KPX_TILE_CHUNKS) * kChunk;   // items per tile
+    static_assert(sizeof(WarpCoop<R>) * kWarps >= kTileM, "tile lengths must fit the staging area");
+    int tile = -kTileM, n_units = 0, tile_limit = 0;
     int unit = sorted ? 0x3fffffff : (team_rank * kBlock + tid) >> 5;    // unsorted: this warp's slice of the one round
     // one loop, one copy of the integrator: the three schedules only differ in how the next unit is found
 #pragma unroll 1
     for (;;) {
-        int pos;
+        int pos, limit;
         if (tiled) {
             if (unit >= n_units) {
                 // this warp is through with the tile: every warp of the CTA meets here once per tile.
                 // Counting sort of the next tile by substep count, longest first.
-                tile += kTile;
+                tile += kTileM;
                 const int items = RS.items;
                 if (tile >= items) break;
                 const int lam = RS.lam, n_sch_old = RS.n_sch_old;
                 const uint64_t h0 = RS.h0;
-                const int n_t = items - tile < kTile ? items - tile : kTile;
+                const int n_t = items - tile < kTileM ? items - tile : kTileM;
                 __syncthreads();                        // the previous tile's walks are done with the staging area
                 for (int b = tid; b < 2 * kBins; b += kBlock) s_bin[b] = 0;          // histogram | fill
-                if (tid == 0) s_bin[3 * kBins] = 0;                                  // unit cursor of the tile
+                if (tid < 2) s_bin[3 * kBins + tid] = 0;                             // unit cursor of the tile | free items
                 __syncthreads();
+                // prepass (whole warps: finishing a free item is warp-synchronous): free items are done here and
+                // take the positions at the END of the tile; the others are binned by length
 #pragma unroll 1
-                for (int j = tid; j < n_t; j += kBlock) {
-                    const int w = tile + j;
-                    const int i = w / lam;
-                    const int slot = expand_slot(W, s_prefix, n_sch_old, i);
-                    int S = substeps_of<M, R>(A.P, h0, slot, w - i * lam);
-                    S = S < kBins - 1 ? S : kBins - 1;
-                    __stcg(W.it_parent + w, slot);
-                    s_len[j] = (uint8_t)S;
-                    atomicAdd(&s_bin[S], 1);
+                for (int j0 = 0; j0 < n_t; j0 += kBlock) {
+                    const int j = j0 + tid, w = tile + j;
+                    const bool act = j < n_t;
+                    bool free = false;
+                    int fpos = 0;
+                    ItemOut<R, M::N> o;
+                    if (act) {
+                        const int i = w / lam;
+                        const int slot = expand_slot(W, s_prefix, n_sch_old, i);
+                        __stcg(W.it_parent + w, slot);
+                        int S = prepass_item<M, R>(A, W, h0, slot, w - i * lam, &free, o);
+                        if (free) {
+                            fpos = tile + n_t - 1 - atomicAdd(&s_bin[3 * kBins + 1], 1);
+                            __stcg(W.pos_of + w, fpos);
+                            s_len[j] = 0;                                            // never a substep count (>= 4)
+                        } else {
+                            S = S < kBins - 1 ? S : kBins - 1;
+                            s_len[j] = (uint8_t)S;
+                            atomicAdd(&s_bin[S], 1);
+                        }
+                    }
+                    if constexpr (FreeFlight<M, R>::kEnabled) {
+                        const unsigned fm = __ballot_sync(0xffffffffu, free);
+                        if (fm) {
+                            commit_item<M, R>(A, W, Q, RS.claim_tag, RS.par, free, w, fpos, o);
+                            if (lane == 0) atomicAdd(&W.ctl->sum_free, (unsigned long long)__popc(fm));
+                        }
+                    }
                 }
                 __syncthreads();
                 if (tid < 32) {                         // start of every bin, longest first (2 bins per lane)
@@ -565,29 +623,34 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
 #pragma unroll 1
                 for (int j = tid; j < n_t; j += kBlock) {
                     const int b = s_len[j];
+                    if (b == 0) continue;               // finished in the prepass
                     const int p = tile + s_bin[2 * kBins + b] + atomicAdd(&s_bin[kBins + b], 1);
-                    __stcg(W.order + p, tile + j);
+                    __stcg(W.order + p, make_int2(tile + j, __ldcg(W.it_parent + tile + j)));
                     __stcg(W.pos_of + tile + j, p);     // results of item w are stored at its sorted position
                 }
                 __syncthreads();
-                n_units = (n_t + 31) >> 5;
+                tile_limit = tile + n_t - s_bin[3 * kBins + 1];
+                n_units = (tile_limit - tile + 31) >> 5;
             }
             // warps pull the tile's units from a shared-memory cursor, longest first
             if (lane == 0) unit = atomicAdd(&s_bin[3 * kBins], 1);
             unit = __shfl_sync(0xffffffffu, unit, 0);
             if (unit >= n_units) continue;              // tile exhausted: on to the next one
             pos = tile + unit * 32 + lane;
+            limit = tile_limit;
         } else if (sorted) {
             if (lane == 0) unit = (int)atomicAdd(&W.ctl->unit_next, 1u);
             unit = __shfl_sync(0xffffffffu, unit, 0);
-            if ((long long)unit * 32 >= RS.items) break;
+            limit = RS.items_sorted;                    // the items that were not finished in the prepass (S0)
+            if ((long long)unit * 32 >= limit) break;
             pos = unit * 32 + lane;
         } else {
-            if ((long long)unit * 32 >= RS.items) break;
+            limit = RS.items;
+            if ((long long)unit * 32 >= limit) break;
             pos = unit * 32 + lane;
             unit = 0x3fffffff;                          // one round only
         }
-        propagate_unit<M, R>(A, W, Q, RS, s_prefix, pos, sorted);
+        propagate_unit<M, R>(A, W, Q, RS, s_prefix, pos, limit, sorted);
     }
 }
 
@@ -623,14 +686,23 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
         if (lazy) {
             // the claim table needs nothing (new epoch); the region arrays are cleared where the previous query
             // touched them: one warp per bitmap word, one lane per region
+            // a warp reads 32 bitmap words at once (one coalesced load instead of 32 dependent ones) and then
+            // clears the regions of every non-zero word, one lane per region
             const int lane = tid & 31;
-            for (long long wi = ttid >> 5; wi < n_words; wi += tthreads >> 5) {
-                const uint32_t bits = __ldcg(W.touched_bits + wi);
-                if ((bits >> lane) & 1u) {
-                    const long long r = wi * 32 + lane;
-                    W.n_valid[r] = 0; W.n_invalid[r] = 0; W.cov[r] = 0; W.avail_it[r] = 0; W.score[r] = 0.0;
+            for (long long base = (ttid >> 5) * 32; base < n_words; base += (tthreads >> 5) * 32) {
+                const long long wi = base + lane;
+                const uint32_t mine = wi < n_words ? __ldcg(W.touched_bits + wi) : 0u;
+                unsigned nz = __ballot_sync(0xffffffffu, mine != 0u);
+                if (mine) { W.touched_bits[wi] = 0u; W.avail_bits[wi] = 0u; }
+                while (nz) {
+                    const int src = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const uint32_t bits = __shfl_sync(0xffffffffu, mine, src);
+                    if ((bits >> lane) & 1u) {
+                        const long long r = (base + src) * 32 + lane;
+                        W.n_valid[r] = 0; W.n_invalid[r] = 0; W.cov[r] = 0; W.score[r] = -1.0;
+                    }
                 }
-                if (lane == 0 && bits) { W.touched_bits[wi] = 0u; W.avail_bits[wi] = 0u; }
             }
         } else {   // dense reset: claim table + region arrays, 16-byte stores
             uint4* c4 = (uint4*)W.claim;
@@ -639,7 +711,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             for (long long i = ttid; i < n4; i += tthreads) c4[i] = ones;
             for (long long i = n4 * 4 + ttid; i < (long long)RG * SUBS; i += tthreads) W.claim[i] = kUnclaimed;
             for (long long i = ttid; i < RG; i += tthreads) {
-                W.n_valid[i] = 0; W.n_invalid[i] = 0; W.cov[i] = 0; W.avail_it[i] = 0; W.score[i] = 0.0;
+                W.n_valid[i] = 0; W.n_invalid[i] = 0; W.cov[i] = 0; W.score[i] = -1.0;
             }
             for (long long i = ttid; i < n_words; i += tthreads) { W.avail_bits[i] = 0u; W.touched_bits[i] = 0u; }
         }
@@ -649,7 +721,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             bool in_goal0;
             for (int d = 0; d < N; ++d) {
                 R x = (R)Q.start[d];
-                states[d * kChunk] = x;                                  // slot 0 (chunked SoA)
+                states[d] = x;                                           // row 0
                 if (d < P.grid_n) {
                     R rel = (x - P.grid_lo[d]) / P.grid_width[d];
                     R cl = rel < (R)0 ? (R)0 : (rel > P.grid_cmax[d] ? P.grid_cmax[d] : rel);
@@ -660,7 +732,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
                 double d0 = Q.start[0] - Q.goal[0], d1 = Q.start[1] - Q.goal[1], d2 = Q.start[2] - Q.goal[2];
                 in_goal0 = sqrt(d0 * d0 + d1 * d1 + d2 * d2) <= Q.goal[3];
             }
-            for (int j = 0; j < NU; ++j) control[j * kChunk] = (R)0;
+            for (int j = 0; j < NU; ++j) control[j] = (R)0;
             dts[0] = (R)0;
             W.parent[0] = -1; W.region[0] = reg; W.tag[0] = KPX_TAG_EXPAND;
             W.cnt_expand[0] = 1; W.e_local[0] = 0;
@@ -670,14 +742,13 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             ctl->first_hit_w = 0x7fffffff; ctl->stop = 0; ctl->rescue_key = 0ull; ctl->rescue_slot = 0x7fffffff;
             ctl->n_items_last = 0; ctl->n_keep_last = 0;
             ctl->cnt_valid[0] = ctl->cnt_valid[1] = ctl->cnt_open[0] = ctl->cnt_open[1] = 0;
-            ctl->sum_items = ctl->sum_substeps = ctl->sum_points = ctl->sum_boxsteps = 0ull;
-            ctl->n_trace = 0; ctl->chain_len = 0; ctl->unit_next = 0u;
+            ctl->sum_items = ctl->sum_substeps = ctl->sum_points = ctl->sum_boxsteps = ctl->sum_free = 0ull;
+            ctl->n_trace = 0; ctl->chain_len = 0; ctl->unit_next = 0u; ctl->n_free = 0u;
             for (int b = 0; b < kBins; ++b) W.bin_cursor[b] = 0u;
         }
         team_sync(T);
         if (keeper) {
             const int reg0 = __ldcg(W.region);
-            W.avail_it[reg0] = 1;
             W.avail_bits[reg0 >> 5] = 1u << (reg0 & 31);
             W.touched_bits[reg0 >> 5] = 1u << (reg0 & 31);   // the root's region is dirty from the start
             ctl->epoch_used = e_new; ctl->epoch_valid = 1;
@@ -735,20 +806,35 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
         if (global_sort) {
             for (int b = tid; b < kBins; b += kBlock) { s_bin[b] = 0; s_bin[2 * kBins + b] = 0; }
             __syncthreads();
+            // prepass (whole warps: finishing a free item is warp-synchronous): free items are done here and take
+            // the positions at the END of the iteration's range; the others are binned by length
+            const uint32_t claim_tag = RS.claim_tag;
 #pragma unroll 1
             for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
                 const int w = (int)w0 + tid;
-                if (w < items) {
+                const bool act = w < items;
+                bool free = false;
+                ItemOut<R, M::N> o;
+                if (act) {
                     const int i = w / lam, ext = w - i * lam;
-                    // i-th EXPAND slot: chunk by binary search over the prefix, then the chunk-local list
-                    int lo = 0, hi = n_sch_old;                    // prefix[lo] <= i < prefix[hi]
-                    while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (s_prefix[mid] <= i) lo = mid; else hi = mid; }
-                    const int slot = __ldcg(W.e_local + lo * kChunk + (i - s_prefix[lo]));
-                    int S = substeps_of<M, R>(P, h0, slot, ext);
+                    const int slot = expand_slot(W, s_prefix, n_sch_old, i);
+                    int S = prepass_item<M, R>(A, W, h0, slot, ext, &free, o);
                     S = S < kBins - 1 ? S : kBins - 1;
                     __stcg(W.it_parent + w, slot);
-                    __stcg(W.it_bin + w, (uint8_t)S);
-                    atomicAdd(&s_bin[S], 1);
+                    __stcg(W.it_bin + w, free ? (uint8_t)0 : (uint8_t)S);          // 0: never a substep count (>= 4)
+                    if (!free) atomicAdd(&s_bin[S], 1);
+                }
+                if constexpr (FreeFlight<M, R>::kEnabled) {
+                    const unsigned fm = __ballot_sync(0xffffffffu, free);
+                    if (fm) {
+                        int base = 0;
+                        if ((tid & 31) == 0) base = (int)atomicAdd(&ctl->n_free, (unsigned)__popc(fm));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        const int fpos = items - 1 - (base + __popc(fm & ((1u << (tid & 31)) - 1u)));
+                        if (free) __stcg(W.pos_of + w, fpos);
+                        commit_item<M, R>(A, W, Q, claim_tag, it & 1, free, w, fpos, o);
+                        if ((tid & 31) == 0) atomicAdd(&ctl->sum_free, (unsigned long long)__popc(fm));
+                    }
                 }
             }
             __syncthreads();
@@ -772,13 +858,15 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
                 const int w = (int)w0 + tid;
                 if (w < items) {
                     const int b = (int)__ldcg(W.it_bin + w);
+                    if (b == 0) continue;               // finished in the prepass
                     const int pos = s_bin[3 * kBins + b] + s_bin[kBins + b] + atomicAdd(&s_bin[2 * kBins + b], 1);
-                    __stcg(W.order + pos, w);
+                    __stcg(W.order + pos, make_int2(w, __ldcg(W.it_parent + w)));
                     __stcg(W.pos_of + w, pos);          // results of item w are stored at `pos` (coalesced S1 stores)
                 }
             }
         }
         if (global_sort) team_sync(T);
+        if (tid == 0) RS.items_sorted = global_sort ? items - (int)__ldcg(&ctl->n_free) : items;
         if (keeper) RS.tp[1] = gtimer();
 
     __syncthreads();                            // the iteration header is visible to the whole CTA
@@ -837,7 +925,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                     if (!kp) {
                         const int slot = __ldcg(W.it_parent + w);
                         const double ua = keyed_uniform(h0, (uint64_t)slot, (uint64_t)(w % lam), PH_ACCEPT);
-                        kp = ua < p_accept_of(region, it - 1, W.avail_it, W.score, total_prev, P.epsilon);
+                        kp = ua < p_accept_of(region, W.score, total_prev, P.epsilon);
                     }
                     keep[j] = kp;
                     if (kp) {
@@ -889,16 +977,14 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                 const int region = (int)(pair / (uint32_t)SUBS);
                 R u[NU], dt; int S;
                 sample_control<M, R>(P, h0, par_slot, w % lam, u, &dt, &S, nullptr, nullptr);
-#pragma unroll
-                for (int d = 0; d < N; ++d) states[soa_base(slot, N) + d * kChunk] = __ldcg(it_end + soa_base(ipos, N) + d * kChunk);
-#pragma unroll
-                for (int q = 0; q < NU; ++q) control[soa_base(slot, NU) + q * kChunk] = u[q];
+                copy_row<R, N>(states, slot, it_end, ipos);
+                store_row<NU>(control, slot, u);
                 dts[slot] = dt;
                 W.parent[slot] = par_slot; W.region[slot] = region; W.tag[slot] = KPX_TAG_EXPAND;
-                if (__ldcg(W.avail_it + region) == 0) {                                      // planner.py:246
-                    __stcg(W.avail_it + region, it + 1);
+                // planner.py:246: the region is available from now on; the estimate pass covers it from the next
+                // iteration (build_est_list in the epilogue), until then its score word says "never"
+                if (!((__ldcg(W.avail_bits + (region >> 5)) >> (region & 31)) & 1u))
                     atomicOr(W.avail_bits + (region >> 5), 1u << (region & 31));
-                }
             }
         }
         // estimate pass (decomposition.py:175-203) over the regions available before this append (est_ids, built in
@@ -950,7 +1036,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                     if (s >= new_size) continue;
                     uint8_t t = tg[j];
                     if (s < size) {
-                        const double p = p_accept_of(rg[j], it, W.avail_it, W.score, total, P.epsilon);
+                        const double p = p_accept_of(rg[j], W.score, total, P.epsilon);
                         const uint64_t hs = slot_ext_hash(h0, (uint64_t)s, 0ull);
                         if (t == KPX_TAG_EXPAND) {                                     // phase A, planner.py:219-225
                             const double ud = unit53(draw_u64(mix64(hs ^ (uint64_t)PH_DEMOTE), 0));
@@ -984,6 +1070,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
         if (keeper) {
             __stcg(&ctl->first_hit_w, 0x7fffffff);
             __stcg(&ctl->unit_next, 0u);
+            __stcg(&ctl->n_free, 0u);
             for (int b = 0; b < kBins; ++b) __stcg(W.bin_cursor + b, 0u);
             atomicAdd(&ctl->sum_items, (unsigned long long)items);
             const double el = (double)(gtimer() - RS.t_start) * 1e-9;
@@ -1003,7 +1090,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
             // rescue rule (planner.py:259-265): OPEN slot with max p_accept, lowest slot on ties
             unsigned long long best = 0ull;
             for (long long s = ttid; s < new_size; s += tthreads) {
-                const double p = p_accept_of(__ldcg(W.region + s), it, W.avail_it, W.score, total, P.epsilon);
+                const double p = p_accept_of(__ldcg(W.region + s), W.score, total, P.epsilon);
                 const unsigned long long b = (unsigned long long)__double_as_longlong(p);   // p > 0: bits are ordered
                 best = b > best ? b : best;
             }
@@ -1011,7 +1098,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
             team_sync(T);
             const unsigned long long kmax = __ldcg(&ctl->rescue_key);
             for (long long s = ttid; s < new_size; s += tthreads) {
-                const double p = p_accept_of(__ldcg(W.region + s), it, W.avail_it, W.score, total, P.epsilon);
+                const double p = p_accept_of(__ldcg(W.region + s), W.score, total, P.epsilon);
                 if ((unsigned long long)__double_as_longlong(p) == kmax) { atomicMin(&ctl->rescue_slot, (int)s); break; }
             }
             team_sync(T);
@@ -1078,14 +1165,14 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
                 s = solution_slot;
                 for (int i = len - 1; i >= 0; --i) {
                     const int par_s = __ldcg(W.parent + s);
-                    for (int d = 0; d < N; ++d) c_start[(size_t)i * N + d] = (double)__ldcg(states + soa_base(par_s, N) + d * kChunk);
-                    for (int q = 0; q < NU; ++q) c_ctrl[(size_t)i * NU + q] = (double)__ldcg(control + soa_base(s, NU) + q * kChunk);
+                    for (int d = 0; d < N; ++d) c_start[(size_t)i * N + d] = (double)__ldcg(states + (size_t)par_s * Row<R, N>::kStride + d);
+                    for (int q = 0; q < NU; ++q) c_ctrl[(size_t)i * NU + q] = (double)__ldcg(control + (size_t)s * Row<R, NU>::kStride + q);
                     c_dt[i] = (double)__ldcg(dts + s);
                     if (!res_out && W.chain_slot) W.chain_slot[i] = s;
                     s = par_s;
                 }
                 if (!res_out && W.chain_end)
-                    for (int d = 0; d < N; ++d) W.chain_end[d] = (double)__ldcg(states + soa_base(solution_slot, N) + d * kChunk);
+                    for (int d = 0; d < N; ++d) W.chain_end[d] = (double)__ldcg(states + (size_t)solution_slot * Row<R, N>::kStride + d);
             }
             for (int i = 0; i < A.n_peers; ++i) { *((volatile uint32_t*)A.peer_flags[i]) = 1u; }
             if (A.n_peers) __threadfence_system();
@@ -1109,6 +1196,7 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
             r.chain_len = len; r.device_ms = (double)(ctl->t_end - __ldcg(&ctl->t_begin)) * 1e-6;
             r.checked = 0; r.check_code = 0;        // filled by kpx_batch_validate
             r.items = __ldcg(&ctl->sum_items); r.substeps = __ldcg(&ctl->sum_substeps); r.points = __ldcg(&ctl->sum_points); r.boxsteps = __ldcg(&ctl->sum_boxsteps);
+            r.free_items = __ldcg(&ctl->sum_free);
             *res_out = r;
         }
     }

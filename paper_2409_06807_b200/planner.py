@@ -345,7 +345,7 @@ class KinoPax:
                                             wall_time_ms=(time.perf_counter() - t0) * 1e3,
                                             solution_duration_s=duration))
         result.device = {"device_ms": st.device_ms, "reset_ms": st.reset_ms, "items": int(st.items),
-                         "substeps": int(st.substeps), "points": int(st.points), "boxsteps": int(st.boxsteps), "launches": int(st.launches),
+                         "substeps": int(st.substeps), "points": int(st.points), "boxsteps": int(st.boxsteps), "free_items": int(st.free_items), "launches": int(st.launches),
                          "precision": "f64" if self.precision == _lib.F64 else "f32", "f64_retry": retried,
                          # the raw device status: PlanStatus keeps the reference's four values, so a run stopped by a
                          # race peer (5) reads TIMEOUT there; this tells the two apart
