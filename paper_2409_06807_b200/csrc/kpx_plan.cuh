@@ -93,6 +93,7 @@ struct Ctl {                      // one per workspace, global memory
     int cur_query;                // batch mode: query index broadcast to the team
     unsigned int unit_next;       // S1: next 32-item unit of the length-sorted order
     unsigned int n_free;          // S0 (many-CTA teams): items finished in the prepass; they fill positions from the end
+    unsigned int n_packed;        // ... and the items left for S1, compacted from the start
     int last_sorted;              // 1 if the last iteration's it_* arrays are in sorted-position order
     // claim-table epoch (see Workspace::claim): the epoch the last query used; epoch_valid = 0 forces a dense
     // reset of the claim table and the region arrays (fresh state loaded from the host)
@@ -743,7 +744,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             ctl->n_items_last = 0; ctl->n_keep_last = 0;
             ctl->cnt_valid[0] = ctl->cnt_valid[1] = ctl->cnt_open[0] = ctl->cnt_open[1] = 0;
             ctl->sum_items = ctl->sum_substeps = ctl->sum_points = ctl->sum_boxsteps = ctl->sum_free = 0ull;
-            ctl->n_trace = 0; ctl->chain_len = 0; ctl->unit_next = 0u; ctl->n_free = 0u;
+            ctl->n_trace = 0; ctl->chain_len = 0; ctl->unit_next = 0u; ctl->n_free = 0u; ctl->n_packed = 0u;
             for (int b = 0; b < kBins; ++b) W.bin_cursor[b] = 0u;
         }
         team_sync(T);
@@ -803,38 +804,63 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
         // Results stay indexed by the item number w, so nothing downstream sees the processing order.
         // An iteration that fits in one round (items <= team threads) gains nothing from it and skips S0.
         const bool global_sort = sorted && T.ctas > 1;    // one-CTA teams sort tile by tile inside S1
+        if constexpr (FreeFlight<M, R>::kEnabled) {
+            // Models with the free-flight certificate: ONE pass.  Most items are finished right here from the closed
+            // form (positions from the end of the iteration's range); what is left is a fraction of a round of the
+            // team's threads, so it is only compacted (positions from the start, in arrival order), not sorted --
+            // one team barrier instead of two, and S1's critical path is its longest item either way.
+            if (global_sort) {
+                const uint32_t claim_tag = RS.claim_tag;
+#pragma unroll 1
+                for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
+                    const int w = (int)w0 + tid, lane = tid & 31;
+                    const bool act = w < items;
+                    bool free = false;
+                    int slot = 0;
+                    ItemOut<R, M::N> o;
+                    if (act) {
+                        const int i = w / lam;
+                        slot = expand_slot(W, s_prefix, n_sch_old, i);
+                        prepass_item<M, R>(A, W, h0, slot, w - i * lam, &free, o);
+                        __stcg(W.it_parent + w, slot);
+                    }
+                    const unsigned fm = __ballot_sync(0xffffffffu, free), bm = __ballot_sync(0xffffffffu, act && !free);
+                    int fbase = 0, bbase = 0;
+                    if (lane == 0) {
+                        if (fm) fbase = (int)atomicAdd(&ctl->n_free, (unsigned)__popc(fm));
+                        if (bm) bbase = (int)atomicAdd(&ctl->n_packed, (unsigned)__popc(bm));
+                    }
+                    fbase = __shfl_sync(0xffffffffu, fbase, 0); bbase = __shfl_sync(0xffffffffu, bbase, 0);
+                    const unsigned below = (1u << lane) - 1u;
+                    const int fpos = items - 1 - (fbase + __popc(fm & below));
+                    if (act && !free) {
+                        const int pos = bbase + __popc(bm & below);
+                        __stcg(W.order + pos, make_int2(w, slot));
+                        __stcg(W.pos_of + w, pos);
+                    }
+                    if (fm) {
+                        if (free) __stcg(W.pos_of + w, fpos);
+                        commit_item<M, R>(A, W, Q, claim_tag, it & 1, free, w, fpos, o);
+                        if (lane == 0) atomicAdd(&ctl->sum_free, (unsigned long long)__popc(fm));
+                    }
+                }
+                team_sync(T);
+            }
+        } else {
         if (global_sort) {
             for (int b = tid; b < kBins; b += kBlock) { s_bin[b] = 0; s_bin[2 * kBins + b] = 0; }
             __syncthreads();
-            // prepass (whole warps: finishing a free item is warp-synchronous): free items are done here and take
-            // the positions at the END of the iteration's range; the others are binned by length
-            const uint32_t claim_tag = RS.claim_tag;
 #pragma unroll 1
             for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
                 const int w = (int)w0 + tid;
-                const bool act = w < items;
-                bool free = false;
-                ItemOut<R, M::N> o;
-                if (act) {
+                if (w < items) {
                     const int i = w / lam, ext = w - i * lam;
                     const int slot = expand_slot(W, s_prefix, n_sch_old, i);
-                    int S = prepass_item<M, R>(A, W, h0, slot, ext, &free, o);
+                    int S = substeps_of<M, R>(P, h0, slot, ext);
                     S = S < kBins - 1 ? S : kBins - 1;
                     __stcg(W.it_parent + w, slot);
-                    __stcg(W.it_bin + w, free ? (uint8_t)0 : (uint8_t)S);          // 0: never a substep count (>= 4)
-                    if (!free) atomicAdd(&s_bin[S], 1);
-                }
-                if constexpr (FreeFlight<M, R>::kEnabled) {
-                    const unsigned fm = __ballot_sync(0xffffffffu, free);
-                    if (fm) {
-                        int base = 0;
-                        if ((tid & 31) == 0) base = (int)atomicAdd(&ctl->n_free, (unsigned)__popc(fm));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        const int fpos = items - 1 - (base + __popc(fm & ((1u << (tid & 31)) - 1u)));
-                        if (free) __stcg(W.pos_of + w, fpos);
-                        commit_item<M, R>(A, W, Q, claim_tag, it & 1, free, w, fpos, o);
-                        if ((tid & 31) == 0) atomicAdd(&ctl->sum_free, (unsigned long long)__popc(fm));
-                    }
+                    __stcg(W.it_bin + w, (uint8_t)S);
+                    atomicAdd(&s_bin[S], 1);
                 }
             }
             __syncthreads();
@@ -858,7 +884,6 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
                 const int w = (int)w0 + tid;
                 if (w < items) {
                     const int b = (int)__ldcg(W.it_bin + w);
-                    if (b == 0) continue;               // finished in the prepass
                     const int pos = s_bin[3 * kBins + b] + s_bin[kBins + b] + atomicAdd(&s_bin[2 * kBins + b], 1);
                     __stcg(W.order + pos, make_int2(w, __ldcg(W.it_parent + w)));
                     __stcg(W.pos_of + w, pos);          // results of item w are stored at `pos` (coalesced S1 stores)
@@ -866,7 +891,8 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
             }
         }
         if (global_sort) team_sync(T);
-        if (tid == 0) RS.items_sorted = global_sort ? items - (int)__ldcg(&ctl->n_free) : items;
+        }
+        if (tid == 0) RS.items_sorted = global_sort ? items - (int)__ldcg(&ctl->n_free) : items;    // (= n_packed where that pass ran)
         if (keeper) RS.tp[1] = gtimer();
 
     __syncthreads();                            // the iteration header is visible to the whole CTA
@@ -1071,6 +1097,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
             __stcg(&ctl->first_hit_w, 0x7fffffff);
             __stcg(&ctl->unit_next, 0u);
             __stcg(&ctl->n_free, 0u);
+            __stcg(&ctl->n_packed, 0u);
             for (int b = 0; b < kBins; ++b) __stcg(W.bin_cursor + b, 0u);
             atomicAdd(&ctl->sum_items, (unsigned long long)items);
             const double el = (double)(gtimer() - RS.t_start) * 1e-9;
