@@ -5,6 +5,7 @@ Run in the build container (needs /root/reference; uses the reference's compiled
 kernel from oracle/_ref when built, else its Python backend):
 
     python oracle/make_golden.py small      # seconds: rng, scenes, batches, plan digests
+    python oracle/make_golden.py runner     # ~a minute: the files the reference's bench harness writes (records / summary / csv)
     python oracle/make_golden.py stacked    # ~a minute: stacked integrators (12D/24D) through the Python backend
     python oracle/make_golden.py outcomes   # minutes: full-size solves, seeds 0..N-1
 
@@ -257,6 +258,32 @@ def gen_stacked(K):
     json.dump(out, open(os.path.join(GOLD, "plans_stacked.json"), "w"), indent=1)
 
 
+RUNNER_CASES = [("di6", "forest", 6000, 1, 8), ("dubins6", "building", 20000, 2, 4)]   # model, scene, t_e, first seed, trials
+RUNNER_SWEEP = ("di6", "forest", [1500, 3000, 6000], 3, 6)                              # model, scene, t_e values, first seed, trials
+
+
+def gen_runner(K):
+    """The files the reference's own harness writes (bench.py:106-257: records.jsonl, summary.json, trajectory.csv +
+    sidecar, regions_trialNNN.csv, sweep.jsonl) on small configurations: the fixtures the product's runner is
+    diffed against (tests/test_runner_gpu.py)."""
+    import shutil
+    from kinopax import bench
+    for model_name, kind, t_e, seed, trials in RUNNER_CASES:
+        model = K.get_model(model_name)
+        env = K.gen_environment(kind, model, seed=0)
+        out = os.path.join(GOLD, f"runner_{model_name}_{kind}")
+        shutil.rmtree(out, ignore_errors=True)
+        table, _ = bench.run_trials(_cfg(K, model, t_e, seed), env, model, "kinopax", trials, out_dir=out,
+                                    dump_regions_dir=out)
+        print("runner", model_name, kind, "solved", table.solved, "/", table.trials, "reval failures", table.revalidation_failures)
+    model_name, kind, tes, seed, trials = RUNNER_SWEEP
+    model = K.get_model(model_name)
+    out = os.path.join(GOLD, f"runner_sweep_{model_name}_{kind}")
+    shutil.rmtree(out, ignore_errors=True)
+    rows = bench.sweep_te(_cfg(K, model, tes[0], seed), K.gen_environment(kind, model, seed=0), model, tes, trials, out_dir=out)
+    print("sweep", [(r["t_e"], r["failures"]) for r in rows])
+
+
 # ------------------------------------------------------------------ full-size outcomes
 
 CONFIGS = {
@@ -316,6 +343,8 @@ def main():
         gen_batches(K)
         gen_plans(K)
         gen_checker(K)
+    elif what == "runner":
+        gen_runner(K)
     elif what == "stacked":
         gen_stacked(K)
     elif what == "outcomes":

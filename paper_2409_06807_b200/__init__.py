@@ -20,6 +20,7 @@ from .envgen import GenerationError, gen_environment
 from .planner import (IterationTrace, KinoPax, TreeArena, compute_branching_factor, extract_trajectory, plan)
 from .problem import Problem, build_problem
 from .rng import RngStream
+from .runner import StatsTable, TrialRecord, dump_regions, export_trajectory, run_trials, summarize, sweep_te
 from .validity import ValidityChecker, in_goal
 
 __version__ = "0.1.0"
