@@ -741,7 +741,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="di6_forest", choices=sorted(WORKLOADS))
-    ap.add_argument("--backend", default="cuda-f32", choices=["cuda", "cuda-f32"])
+    ap.add_argument("--backend", default="cuda-f32", choices=["cuda", "cuda-f32", "cuda-philox", "cuda-f32-philox"])
     ap.add_argument("--queries", type=int, default=0, help="queries per GPU per step (default per workload)")
     ap.add_argument("--team-ctas", type=int, default=1)
     ap.add_argument("--latency-seeds", type=int, default=100)

@@ -44,6 +44,8 @@ extern "C" {
 
 /* model ids 0..2 = _kernel.pyx:88-130; 3 = stacked 3-D double integrators (n = 6k) */
 enum { KPX_MODEL_DI6 = 0, KPX_MODEL_DUBINS6 = 1, KPX_MODEL_QUAD12 = 2, KPX_MODEL_STACKED_DI = 3 };
+/* random streams: same identity (seed, iteration, slot, extension, phase) and draw index, different generator */
+enum { KPX_RNG_SPLITMIX64 = 0, KPX_RNG_PHILOX = 1 };
 /* arithmetic of the integration / collision / grid-mapping path */
 enum { KPX_F64 = 0, KPX_F32 = 1 };
 /* planner status (core.py:86-90) + RUNNING for stepped runs */
@@ -62,7 +64,7 @@ typedef struct kpx_problem {
     int32_t subcells;   /* sub-cells per position dimension */
     int32_t grid_n;     /* grid spans state dims [0, grid_n); reference: grid_n == n */
     int32_t lambda_max; /* PlannerConfig.lambda_max */
-    int32_t reserved0;
+    int32_t rng;        /* KPX_RNG_SPLITMIX64: the reference's streams (rng.py:30-54), bit-parity; KPX_RNG_PHILOX: Philox4x32-10 */
     int64_t t_e;        /* tree capacity */
     double t_prop, check_res, epsilon, delta;
     double control_lo[KPX_MAX_CONTROL], control_hi[KPX_MAX_CONTROL];
@@ -131,6 +133,13 @@ int kpx_cull_tables(const kpx_problem *prob, int32_t precision, uint32_t *masks8
 int kpx_sample_goals(int64_t n_queries, const uint64_t *query_ids, int32_t n_obs, const double *obs_min,
                      const double *obs_max, const double *start3, double lo, double hi, double radius,
                      double min_dist, double margin, double *goals, void *stream);
+
+/*
+ * Self-test hook of the production generator: Philox4x32-10 of (counter[4], key[2]) computed on the host and by a
+ * one-thread kernel on the current device (out_host[4], out_device[4]; either may be NULL) -- for the known-answer
+ * vectors of the Random123 distribution.
+ */
+int kpx_philox4x32(const uint32_t *counter4, const uint32_t *key2, uint32_t *out_host4, uint32_t *out_device4);
 
 int kpx_device_info(int device, int32_t *sm_count, int32_t *max_coop_blocks_f32, int32_t *max_coop_blocks_f64);
 

@@ -15,6 +15,7 @@ from .core import ConfigError, DeviceError
 
 MAX_DIM, MAX_CONTROL, MAX_CHAIN = 48, 24, 4096
 F64, F32 = 0, 1
+RNG_SPLITMIX64, RNG_PHILOX = 0, 1
 SOLVED, TIMEOUT, CAPACITY_EXHAUSTED, ERROR, RUNNING, STOPPED = range(6)
 E_ARG, E_CUDA, E_LIMIT, E_STATE = 1, 2, 3, 4
 
@@ -27,7 +28,7 @@ _vp = C.c_void_p
 class Problem(C.Structure):
     _fields_ = [
         ("model_id", C.c_int32), ("n", C.c_int32), ("nu", C.c_int32), ("n_obs", C.c_int32),
-        ("subcells", C.c_int32), ("grid_n", C.c_int32), ("lambda_max", C.c_int32), ("reserved0", C.c_int32),
+        ("subcells", C.c_int32), ("grid_n", C.c_int32), ("lambda_max", C.c_int32), ("rng", C.c_int32),
         ("t_e", C.c_int64),
         ("t_prop", C.c_double), ("check_res", C.c_double), ("epsilon", C.c_double), ("delta", C.c_double),
         ("control_lo", C.c_double * MAX_CONTROL), ("control_hi", C.c_double * MAX_CONTROL),
@@ -79,6 +80,7 @@ _SIGNATURES = {
     "kpx_cull_tables": (C.c_int, [C.POINTER(Problem), C.c_int32, _vp, _vp, _vp]),
     "kpx_sample_goals": (C.c_int, [C.c_int64, _vp, C.c_int32, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double,
                                    C.c_double, C.c_double, _vp, _vp]),
+    "kpx_philox4x32": (C.c_int, [_vp, _vp, _vp, _vp]),
     "kpx_device_info": (C.c_int, [C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kpx_propagate_batch": (C.c_int, [C.POINTER(Problem), _vp, C.c_int64, _vp, C.c_int64, C.c_int32, C.c_uint64,
                                       C.c_uint64, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -161,13 +163,15 @@ def ptr(a):
 
 
 def make_problem(model_id, n, nu, t_e, lambda_max, t_prop, check_res, epsilon, delta, control_lo, control_hi,
-                 state_lo, state_hi, obs_min, obs_max, grid_lo, grid_width, grid_cells, grid_strides, subcells):
+                 state_lo, state_hi, obs_min, obs_max, grid_lo, grid_width, grid_cells, grid_strides, subcells,
+                 rng=RNG_SPLITMIX64):
     """Flatten into ``kpx_problem``.  Returns (struct, keepalive) -- keep both alive during calls."""
     if n > MAX_DIM or nu > MAX_CONTROL:
         raise ValueError("state/control dimension exceeds kernel limits")
     p = Problem()
     p.model_id, p.n, p.nu, p.subcells = int(model_id), int(n), int(nu), int(subcells)
     p.grid_n, p.lambda_max, p.t_e = len(grid_lo), int(lambda_max), int(t_e)
+    p.rng = int(rng)
     p.t_prop, p.check_res, p.epsilon, p.delta = float(t_prop), float(check_res), float(epsilon), float(delta)
     for j in range(nu):
         p.control_lo[j], p.control_hi[j] = float(control_lo[j]), float(control_hi[j])
@@ -184,7 +188,7 @@ def make_problem(model_id, n, nu, t_e, lambda_max, t_prop, check_res, epsilon, d
     return p, (omin, omax)
 
 
-def problem_from(prob) -> tuple:
+def problem_from(prob, rng=RNG_SPLITMIX64) -> tuple:
     """``Problem`` (problem.py) -> ``kpx_problem``."""
     m, g, c = prob.model, prob.grid, prob.cfg
     if m.kernel_id is None:
@@ -192,4 +196,4 @@ def problem_from(prob) -> tuple:
     return make_problem(m.kernel_id, m.n, m.control_dim, c.t_e, c.lambda_max, c.t_prop, prob.check_resolution,
                         c.epsilon, c.delta, m.control_lo, m.control_hi, prob.state_lo, prob.state_hi,
                         prob.env.obstacles_min, prob.env.obstacles_max, g.lo, g.widths, g.cells, g.strides,
-                        g.subcells)
+                        g.subcells, rng=rng)

@@ -6,7 +6,9 @@ Reference ``backend.py`` resolves a name to an object with ``.name`` and
 for field and registers two CUDA backends behind the same call:
 
 * ``"cuda"``      -- float64 instantiation, bit-parity with the reference kernel,
-* ``"cuda-f32"``  -- float32 instantiation (end states within 1e-5 relative).
+* ``"cuda-f32"``  -- float32 instantiation (end states within 1e-5 relative),
+* ``"cuda-philox"`` / ``"cuda-f32-philox"`` -- the same kernels drawing from the production Philox4x32-10 stream
+  instead of the reference's SplitMix64 chains (other random numbers, hence other trees: not a parity mode).
 
 ``KINOPAX_BACKEND`` overrides the default exactly as in the reference.  Unknown
 names and models without a CUDA kernel raise ``ConfigError``; a missing
@@ -66,6 +68,7 @@ class CudaBackend:
 
     name = "cuda"
     precision = _lib.F64
+    rng = _lib.RNG_SPLITMIX64      # the reference's streams; the "-philox" backends draw from Philox4x32-10 instead
 
     def __init__(self, counters: bool = False):
         self.counters = counters
@@ -79,7 +82,7 @@ class CudaBackend:
         prob, keep = _lib.make_problem(
             m.kernel_id, m.n, m.control_dim, max(len(states), 1), 1, ctx.t_prop, ctx.check_res, 0.5, 1.0,
             m.control_lo, m.control_hi, ctx.state_lo, ctx.state_hi, ctx.obs_min, ctx.obs_max, ctx.grid_lo,
-            ctx.grid_width, ctx.grid_cells, ctx.grid_strides, ctx.subcells)
+            ctx.grid_width, ctx.grid_cells, ctx.grid_strides, ctx.subcells, rng=self.rng)
         states = np.ascontiguousarray(states, dtype=np.float64)
         e_slots = np.ascontiguousarray(e_slots, dtype=np.int64)
         items = len(e_slots) * int(lam)
@@ -106,7 +109,18 @@ class CudaF32Backend(CudaBackend):
     precision = _lib.F32
 
 
-_BACKENDS = {"cuda": CudaBackend, "cuda-f32": CudaF32Backend}
+class CudaPhiloxBackend(CudaBackend):
+    name = "cuda-philox"
+    rng = _lib.RNG_PHILOX
+
+
+class CudaF32PhiloxBackend(CudaF32Backend):
+    name = "cuda-f32-philox"
+    rng = _lib.RNG_PHILOX
+
+
+_BACKENDS = {"cuda": CudaBackend, "cuda-f32": CudaF32Backend, "cuda-philox": CudaPhiloxBackend,
+             "cuda-f32-philox": CudaF32PhiloxBackend}
 
 
 def cuda_available() -> bool:

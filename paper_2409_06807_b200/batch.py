@@ -93,9 +93,10 @@ class BatchPlanner:
                  device: int = 0):
         self.problem = build_problem(cfg, env, model, check_resolution)
         self.cfg, self.env, self.model = cfg, env, model
-        self.precision = get_backend(backend, model).precision
+        self.backend = get_backend(backend, model)
+        self.precision = self.backend.precision
         self._lib = _lib.load()
-        self._prob_struct, self._keep = _lib.problem_from(self.problem)
+        self._prob_struct, self._keep = _lib.problem_from(self.problem, rng=self.backend.rng)
         self.max_chain, self.device = int(max_chain), device
         self._handle = _lib._vp()
         # n_teams <= 0: as many teams as are co-resident on the device for this model and precision
@@ -184,7 +185,8 @@ class BatchPlanner:
             if len(bad):
                 if self._f64 is None:       # few queries: teams of 16 CTAs each instead of one (a float64 plan on one
                     # CTA takes ~100x a float32 one; the GPU is otherwise idle here)
-                    self._f64 = BatchPlanner(self.cfg, self.env, self.model, self.problem.check_resolution, "cuda",
+                    self._f64 = BatchPlanner(self.cfg, self.env, self.model, self.problem.check_resolution,
+                                             "cuda-philox" if self.backend.rng == _lib.RNG_PHILOX else "cuda",
                                              n_teams=int(min(len(bad), 8)), team_ctas=16, max_chain=self.max_chain,
                                              device=self.device)
                 r64 = self._f64.run(seeds[bad], starts[bad], goals[bad], tm, True, stream, False,

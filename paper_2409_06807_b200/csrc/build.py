@@ -1,9 +1,10 @@
 #!/usr/bin/env python3
 """Build libkpx.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-Four translation units: the f64 parity instantiations (``-fmad=false``, the
+Seven translation units: the f64 parity instantiations (``-fmad=false``, the
 reference is built with ``-ffp-contract=off``), the f32 throughput
-instantiations, the f32 single-query (latency) instantiations, and the C ABI.  The shared library lands next to the Python
+instantiations, the f32 single-query (latency) instantiations, the same three
+drawing from Philox4x32-10 instead of the reference's SplitMix64 streams, and the C ABI.  The shared library lands next to the Python
 package (``paper_2409_06807_b200/libkpx.so``) so it travels to the GPU box.
 """
 from __future__ import annotations
@@ -24,6 +25,10 @@ UNITS = [
     ("kpx_inst_f64.cu", ["-fmad=false"]),
     ("kpx_inst_f32.cu", []),
     ("kpx_inst_f32lat.cu", []),
+    # the same kernels drawing from Philox4x32-10 (the random stream is a compile-time property of a kernel)
+    ("kpx_inst_f64p.cu", ["-fmad=false"]),
+    ("kpx_inst_f32p.cu", []),
+    ("kpx_inst_f32latp.cu", []),
     ("kpx_api.cu", []),
 ]
 HEADERS = ["kpx_device.cuh", "kpx_plan.cuh", "kpx_launch.h", "kpx_inst.inl", os.path.join("..", "..", "include", "kpx.h")]
@@ -55,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
         return r.stderr
 
-    with ThreadPoolExecutor(max_workers=4) as ex:
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
         logs = list(ex.map(run, jobs))
     if verbose:
         for l in logs:

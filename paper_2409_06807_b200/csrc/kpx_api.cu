@@ -47,6 +47,7 @@ int check_problem(const kpx_problem* pr) {
         return fail(KPX_E_LIMIT, "state/control dimension exceeds kernel limits");
     if (pr->n < 3 || pr->nu < 1 || pr->grid_n < 3 || pr->grid_n > pr->n) return fail(KPX_E_ARG, "bad dimensions");
     if (pr->model_id < 0 || pr->model_id > KPX_MODEL_STACKED_DI) return fail(KPX_E_ARG, "unknown model id");
+    if (pr->rng != KPX_RNG_SPLITMIX64 && pr->rng != KPX_RNG_PHILOX) return fail(KPX_E_ARG, "unknown rng");
     if (pr->n_obs < 0 || (pr->n_obs > 0 && (!pr->obs_min || !pr->obs_max))) return fail(KPX_E_ARG, "bad obstacles");
     if (pr->subcells < 1 || pr->lambda_max < 1 || pr->t_e < 1) return fail(KPX_E_ARG, "bad configuration");
     double regions = 1.0;
@@ -155,6 +156,9 @@ void destroy_batch(kpx_batch& b) {
 }
 
 int blocks_per_sm(const kpx_batch& b) {
+    if (b.prob.rng == KPX_RNG_PHILOX)
+        return b.precision == KPX_F64 ? plan_blocks_per_sm_f64p(b.prob.model_id, b.prob.n, b.smem, b.latency)
+                                      : plan_blocks_per_sm_f32p(b.prob.model_id, b.prob.n, b.smem, b.latency);
     return b.precision == KPX_F64 ? plan_blocks_per_sm_f64(b.prob.model_id, b.prob.n, b.smem, b.latency)
                                   : plan_blocks_per_sm_f32(b.prob.model_id, b.prob.n, b.smem, b.latency);
 }
@@ -287,7 +291,9 @@ int ensure_queries(kpx_batch& b, long long q) {
 }
 
 int launch(kpx_batch& b, const PlanLaunch& L, cudaStream_t st) {
-    cudaError_t e = b.precision == KPX_F64 ? launch_plan_f64(L, st) : launch_plan_f32(L, st);
+    cudaError_t e;
+    if (b.prob.rng == KPX_RNG_PHILOX) e = b.precision == KPX_F64 ? launch_plan_f64p(L, st) : launch_plan_f32p(L, st);
+    else e = b.precision == KPX_F64 ? launch_plan_f64(L, st) : launch_plan_f32(L, st);
     if (e != cudaSuccess) return fail(KPX_E_CUDA, "planner kernel launch: %s", cudaGetErrorString(e));
     ++b.launches;
     return KPX_OK;
@@ -451,6 +457,11 @@ __global__ void chain_pack_kernel(int n_q, const kpx_query_result* __restrict__ 
     for (long long i = threadIdx.x; i < rows; i += blockDim.x) pd[o + i] = cd[src + i];
 }
 
+__global__ void philox_kernel(Philox4 c, uint32_t k0, uint32_t k1, uint32_t* out) {
+    const Philox4 r = philox4x32_10(c, k0, k1);
+    out[0] = r.x; out[1] = r.y; out[2] = r.z; out[3] = r.w;
+}
+
 // Goal of query q (BASELINE.json config 5): centre uniform in [lo, hi]^3 drawn from the GENERIC stream of
 // seed q (rng.py:57-95: key(seed = q, 0, 0, 0, phase 5), draws 0, 1, 2, ...), three draws per try; a try is rejected
 // if the centre is closer than min_dist to the start or inside an obstacle grown by `grow` on every side.  One thread
@@ -486,6 +497,24 @@ __global__ void sample_goals_kernel(int n, const unsigned long long* __restrict_
 }  // namespace
 
 extern "C" {
+
+int kpx_philox4x32(const uint32_t* counter4, const uint32_t* key2, uint32_t* out_host4, uint32_t* out_device4) {
+    if (!counter4 || !key2) return fail(KPX_E_ARG, "null argument");
+    const Philox4 c{counter4[0], counter4[1], counter4[2], counter4[3]};
+    if (out_host4) {
+        const Philox4 r = philox4x32_10(c, key2[0], key2[1]);
+        out_host4[0] = r.x; out_host4[1] = r.y; out_host4[2] = r.z; out_host4[3] = r.w;
+    }
+    if (out_device4) {
+        uint32_t* d = nullptr;
+        CU(cudaMalloc(&d, 16));
+        philox_kernel<<<1, 1>>>(c, key2[0], key2[1], d);
+        cudaError_t e = cudaMemcpy(out_device4, d, 16, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        if (e != cudaSuccess) return fail(KPX_E_CUDA, "philox self-test: %s", cudaGetErrorString(e));
+    }
+    return KPX_OK;
+}
 
 int kpx_sample_goals(int64_t n_queries, const uint64_t* query_ids, int32_t n_obs, const double* obs_min,
                      const double* obs_max, const double* start3, double lo, double hi, double radius, double min_dist,
@@ -628,7 +657,9 @@ int kpx_propagate_batch(const kpx_problem* prob, const double* states, int64_t s
     CU(ev.create());
     const cudaEvent_t e0 = ev.e0, e1 = ev.e1;
     CU(cudaEventRecord(e0, st));
-    cudaError_t e = precision == KPX_F64 ? launch_batch_f64(L, st) : launch_batch_f32(L, st);
+    cudaError_t e;
+    if (prob->rng == KPX_RNG_PHILOX) e = precision == KPX_F64 ? launch_batch_f64p(L, st) : launch_batch_f32p(L, st);
+    else e = precision == KPX_F64 ? launch_batch_f64(L, st) : launch_batch_f32(L, st);
     if (e != cudaSuccess) return fail(e == cudaErrorInvalidValue ? KPX_E_ARG : KPX_E_CUDA,
                                       "propagate kernel launch (model_id=%d n=%d): %s", prob->model_id, n,
                                       cudaGetErrorString(e));

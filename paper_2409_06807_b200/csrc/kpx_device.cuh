@@ -147,6 +147,59 @@ __device__ __forceinline__ double keyed_uniform(uint64_t h0, uint64_t slot, uint
     return unit53(draw_u64(mix64(slot_ext_hash(h0, slot, ext) ^ (uint64_t)phase), 0));
 }
 
+// ---- Philox4x32-10 (Salmon et al., "Parallel random numbers: as easy as 1, 2, 3", SC'11): the production stream.
+// The reference's streams are SplitMix64 chains (above; the parity mode, KPX_RNG_SPLITMIX64).  With KPX_RNG_PHILOX the
+// same five-word stream identity (seed, iteration, slot, extension, phase) and draw index feed a counter-based
+// generator instead of a hash chain:
+//     iteration key  h0 = words 0..1 of philox(counter = (seed_lo, seed_hi, it_lo, it_hi), key = kPhiloxDomain)
+//     draw i         = 64 bits (words 2 (i & 1), 2 (i & 1) + 1) of philox(counter = (slot, ext, phase, i >> 1), key = h0)
+// and a uniform is the top 53 bits of those 64, as in rng.py:52.  Trees then differ from the reference's by
+// construction (other random numbers); everything downstream of a draw is unchanged.
+struct Philox4 { uint32_t x, y, z, w; };
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return __umulhi(a, b);
+#else
+    return (uint32_t)(((uint64_t)a * (uint64_t)b) >> 32);
+#endif
+}
+__host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = mulhi32(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = mulhi32(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = Philox4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+constexpr uint32_t kPhiloxDomain0 = 0x4B696E6Fu, kPhiloxDomain1 = 0x50415821u;      // "Kino" "PAX!"
+__host__ __device__ __forceinline__ uint64_t philox_iter_key(uint64_t seed, uint64_t it) {
+    const Philox4 r = philox4x32_10(Philox4{(uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)it, (uint32_t)(it >> 32)},
+                                    kPhiloxDomain0, kPhiloxDomain1);
+    return (uint64_t)r.x | ((uint64_t)r.y << 32);
+}
+// draws 2 blk and 2 blk + 1 of the stream (slot, ext, phase) under iteration key h0
+__host__ __device__ __forceinline__ void philox_draw2(uint64_t h0, uint32_t slot, uint32_t ext, int phase, uint32_t blk,
+                                                      uint64_t* a, uint64_t* b) {
+    const Philox4 r = philox4x32_10(Philox4{slot, ext, (uint32_t)phase, blk}, (uint32_t)h0, (uint32_t)(h0 >> 32));
+    *a = (uint64_t)r.x | ((uint64_t)r.y << 32);
+    *b = (uint64_t)r.z | ((uint64_t)r.w << 32);
+}
+// the two generators behind one face: iteration key and "draw 0 of stream (slot, ext, phase)"
+__host__ __device__ __forceinline__ uint64_t iter_key(int rng, uint64_t seed, uint64_t it) {
+    return rng == KPX_RNG_PHILOX ? philox_iter_key(seed, it) : iter_hash(seed, it);
+}
+template <int RNG>
+__device__ __forceinline__ double keyed_uniform_of(uint64_t h0, uint64_t slot, uint64_t ext, int phase) {
+    if constexpr (RNG == KPX_RNG_PHILOX) {
+        uint64_t a, b;
+        philox_draw2(h0, (uint32_t)slot, (uint32_t)ext, phase, 0u, &a, &b);
+        return unit53(a);
+    }
+    return keyed_uniform(h0, slot, ext, phase);
+}
+
 // ------------------------------------------------------- typed parameters ----
 template <class R>
 struct Params {
@@ -343,6 +396,8 @@ __device__ __forceinline__ R wrap_angle(R a) {
 }
 
 struct ModelDI6 {
+    using Base = ModelDI6;
+    static constexpr int kRng = KPX_RNG_SPLITMIX64;
     static constexpr int ID = KPX_MODEL_DI6, N = 6, NU = 3;
     template <class R> __device__ static __forceinline__ void deriv(const R* x, const R* u, R* o) {
         o[0] = x[3]; o[1] = x[4]; o[2] = x[5]; o[3] = u[0]; o[4] = u[1]; o[5] = u[2];
@@ -351,6 +406,8 @@ struct ModelDI6 {
 };
 
 struct ModelDubins6 {
+    using Base = ModelDubins6;
+    static constexpr int kRng = KPX_RNG_SPLITMIX64;
     static constexpr int ID = KPX_MODEL_DUBINS6, N = 6, NU = 3;
     template <class R> __device__ static __forceinline__ void deriv(const R* x, const R* u, R* o) {
         R st, ct, sg, cg;
@@ -363,6 +420,8 @@ struct ModelDubins6 {
 };
 
 struct ModelQuad12 {
+    using Base = ModelQuad12;
+    static constexpr int kRng = KPX_RNG_SPLITMIX64;
     static constexpr int ID = KPX_MODEL_QUAD12, N = 12, NU = 4;
     template <class R> __device__ static __forceinline__ void deriv(const R* x, const R* u, R* o) {
         R sphi, cphi, sth, cth, spsi, cpsi;
@@ -406,6 +465,8 @@ struct ModelQuad12 {
 // B stacked 3-D double integrators, state [p1 v1 p2 v2 ...]; only block 1 is workspace position.
 template <int B>
 struct ModelStackedDI {
+    using Base = ModelStackedDI<B>;
+    static constexpr int kRng = KPX_RNG_SPLITMIX64;
     static constexpr int ID = KPX_MODEL_STACKED_DI, N = 6 * B, NU = 3 * B;
     template <class R> __device__ static __forceinline__ void deriv(const R* x, const R* u, R* o) {
 #pragma unroll
@@ -415,6 +476,15 @@ struct ModelStackedDI {
         }
     }
     template <class R> __device__ static __forceinline__ void wrap(R*) {}
+};
+
+// The same model drawing from another generator: the random stream is a compile-time property of the kernel (a
+// run-time switch in the sampling code cost 5-8 % of the throughput of BOTH streams); `Base` keeps the per-model
+// specialisations (Stepper, FreeFlight) keyed on the plain model.
+template <class M0, int RNG>
+struct WithRng : M0 {
+    using Base = typename M0::Base;
+    static constexpr int kRng = RNG;
 };
 
 // One RK4 substep with zero-order hold.  Accumulating k1 + 2k2 + 2k3 + k4 left to
@@ -841,7 +911,7 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
         // for a finite state !(x < lo || x > hi) == (x >= lo) & (x <= hi), and the result is only used then
         bool inb = true;
         if (run) {
-            Stepper<M, R>::step(cur, comp, u, h, h6);
+            Stepper<typename M::Base, R>::step(cur, comp, u, h, h6);
             bool fin = true;
 #pragma unroll
             for (int i = 0; i < N; ++i) fin = fin && isfinite(cur[i]);
@@ -963,14 +1033,27 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
 template <class M, class R>
 __device__ __forceinline__ void sample_control(const Params<R>& P, uint64_t h0, int slot, int ext, R* u, R* dt,
                                                int* substeps, double* u64v, double* dt64) {
-    uint64_t key = mix64(slot_ext_hash(h0, (uint64_t)slot, (uint64_t)ext) ^ (uint64_t)PH_SAMPLE);
+    double unit[M::NU + 1];                 // draws 0..NU-1 -> controls, draw NU -> duration
+    if constexpr (M::kRng == KPX_RNG_PHILOX) {
+#pragma unroll
+        for (int blk = 0; 2 * blk < M::NU + 1; ++blk) {
+            uint64_t a, b;
+            philox_draw2(h0, (uint32_t)slot, (uint32_t)ext, PH_SAMPLE, (uint32_t)blk, &a, &b);
+            unit[2 * blk] = unit53(a);
+            if (2 * blk + 1 < M::NU + 1) unit[2 * blk + 1] = unit53(b);
+        }
+    } else {
+        const uint64_t key = mix64(slot_ext_hash(h0, (uint64_t)slot, (uint64_t)ext) ^ (uint64_t)PH_SAMPLE);
+#pragma unroll
+        for (int j = 0; j < M::NU + 1; ++j) unit[j] = unit53(draw_u64(key, (uint64_t)j));
+    }
 #pragma unroll
     for (int j = 0; j < M::NU; ++j) {
-        double v = __dadd_rn(P.control_lo[j], __dmul_rn(unit53(draw_u64(key, (uint64_t)j)), P.control_span[j]));
+        double v = __dadd_rn(P.control_lo[j], __dmul_rn(unit[j], P.control_span[j]));
         if (u64v) u64v[j] = v;
         u[j] = (R)v;
     }
-    double d = __dmul_rn(__dsub_rn(1.0, unit53(draw_u64(key, (uint64_t)M::NU))), P.t_prop);
+    double d = __dmul_rn(__dsub_rn(1.0, unit[M::NU]), P.t_prop);
     if (dt64) *dt64 = d;
     *dt = (R)d;
     int s = (int)ceil(__ddiv_rn((double)(*dt), 0.02));
@@ -980,8 +1063,16 @@ __device__ __forceinline__ void sample_control(const Params<R>& P, uint64_t h0, 
 // substep count of item (slot, ext) alone: the duration draw and the same rounding as sample_control
 template <class M, class R>
 __device__ __forceinline__ int substeps_of(const Params<R>& P, uint64_t h0, int slot, int ext) {
-    const uint64_t key = mix64(slot_ext_hash(h0, (uint64_t)slot, (uint64_t)ext) ^ (uint64_t)PH_SAMPLE);
-    const double d = __dmul_rn(__dsub_rn(1.0, unit53(draw_u64(key, (uint64_t)M::NU))), P.t_prop);
+    double un;
+    if constexpr (M::kRng == KPX_RNG_PHILOX) {
+        uint64_t a, b;
+        philox_draw2(h0, (uint32_t)slot, (uint32_t)ext, PH_SAMPLE, (uint32_t)(M::NU >> 1), &a, &b);
+        un = unit53((M::NU & 1) ? b : a);
+    } else {
+        const uint64_t key = mix64(slot_ext_hash(h0, (uint64_t)slot, (uint64_t)ext) ^ (uint64_t)PH_SAMPLE);
+        un = unit53(draw_u64(key, (uint64_t)M::NU));
+    }
+    const double d = __dmul_rn(__dsub_rn(1.0, un), P.t_prop);
     const R dt = (R)d;
     const int s = (int)ceil(__ddiv_rn((double)dt, 0.02));
     return s < 4 ? 4 : s;

@@ -4,6 +4,7 @@
 //                       launches to ...
 //   kpx_inst_f32lat.cu  float, LATENCY build of the plan kernels only (KPX_PLAN_ONLY; its own translation unit so
 //                       that the two float32 builds compile in parallel)
+//   kpx_inst_*p.cu      the same three with KPX_INST_RNG = KPX_RNG_PHILOX: the kernels of the "-philox" backends
 #include "kpx_launch.h"
 
 #ifndef KPX_VARIANT
@@ -65,16 +66,21 @@ int do_occupancy(size_t smem) {
     return nb;
 }
 
+// every kernel of this unit draws from ONE generator (KPX_INST_RNG): the stream is a template property of the model
+#ifndef KPX_INST_RNG
+#define KPX_INST_RNG KPX_RNG_SPLITMIX64
+#endif
+#define KPX_MODEL(...) WithRng<__VA_ARGS__, KPX_INST_RNG>
 #define KPX_DISPATCH(CALL)                                                                   \
     switch (model_id) {                                                                      \
-        case KPX_MODEL_DI6: if (n == 6) { CALL(ModelDI6); } break;                           \
-        case KPX_MODEL_DUBINS6: if (n == 6) { CALL(ModelDubins6); } break;                   \
-        case KPX_MODEL_QUAD12: if (n == 12) { CALL(ModelQuad12); } break;                    \
+        case KPX_MODEL_DI6: if (n == 6) { CALL(KPX_MODEL(ModelDI6)); } break;                \
+        case KPX_MODEL_DUBINS6: if (n == 6) { CALL(KPX_MODEL(ModelDubins6)); } break;        \
+        case KPX_MODEL_QUAD12: if (n == 12) { CALL(KPX_MODEL(ModelQuad12)); } break;         \
         case KPX_MODEL_STACKED_DI:                                                           \
-            if (n == 6) { CALL(ModelStackedDI<1>); }                                         \
-            else if (n == 12) { CALL(ModelStackedDI<2>); }                                   \
-            else if (n == 24) { CALL(ModelStackedDI<4>); }                                   \
-            else if (n == 48) { CALL(ModelStackedDI<8>); }                                   \
+            if (n == 6) { CALL(KPX_MODEL(ModelStackedDI<1>)); }                              \
+            else if (n == 12) { CALL(KPX_MODEL(ModelStackedDI<2>)); }                        \
+            else if (n == 24) { CALL(KPX_MODEL(ModelStackedDI<4>)); }                        \
+            else if (n == 48) { CALL(KPX_MODEL(ModelStackedDI<8>)); }                        \
             break;                                                                           \
         default: break;                                                                      \
     }
@@ -86,7 +92,7 @@ int do_occupancy(size_t smem) {
 
 cudaError_t KPX_CAT(launch_plan_, KPX_SUFFIX)(const PlanLaunch& L, cudaStream_t st) {
 #ifdef KPX_FORWARD_LATENCY
-    if (L.latency) return launch_plan_f32lat(L, st);
+    if (L.latency) return KPX_CAT(launch_plan_, KPX_FORWARD_LATENCY)(L, st);
 #endif
     const int model_id = L.prob->model_id, n = L.prob->n;
 #define CALL(M) return do_launch_plan<M>(L, st)
@@ -104,6 +110,7 @@ cudaError_t KPX_CAT(launch_batch_, KPX_SUFFIX)(const BatchLaunch& L, cudaStream_
     return cudaErrorInvalidValue;
 }
 
+#if KPX_INST_RNG == KPX_RNG_SPLITMIX64     // host helpers: once per precision
 void KPX_CAT(occupancy_masks_, KPX_SUFFIX)(const kpx_problem& pr, int n_obs, const double* omin, const double* omax,
                                            uint32_t* masks) {
     Params<Real> P;
@@ -117,12 +124,13 @@ void KPX_CAT(cull_constants_, KPX_SUFFIX)(const kpx_problem& pr, double* thr4, d
     for (int k = 0; k < 4; ++k) thr4[k] = (double)P.d2_thr[k];
     for (int a = 0; a < 3; ++a) { lo3[a] = (double)P.occ_lo[a]; inv3[a] = (double)P.occ_inv[a]; }
 }
+#endif
 
 #endif  // !KPX_PLAN_ONLY
 
 int KPX_CAT(plan_blocks_per_sm_, KPX_SUFFIX)(int model_id, int n, size_t smem, bool latency) {
 #ifdef KPX_FORWARD_LATENCY
-    if (latency) return plan_blocks_per_sm_f32lat(model_id, n, smem, true);
+    if (latency) return KPX_CAT(plan_blocks_per_sm_, KPX_FORWARD_LATENCY)(model_id, n, smem, true);
 #endif
     (void)latency;
 #define CALL(M) return do_occupancy<M>(smem)

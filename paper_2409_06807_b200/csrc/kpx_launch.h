@@ -62,6 +62,15 @@ cudaError_t launch_plan_f32(const PlanLaunch& L, cudaStream_t st);       // forw
 cudaError_t launch_plan_f32lat(const PlanLaunch& L, cudaStream_t st);    // the LATENCY build (own translation unit)
 cudaError_t launch_batch_f64(const BatchLaunch& L, cudaStream_t st);
 cudaError_t launch_batch_f32(const BatchLaunch& L, cudaStream_t st);
+// the same kernels drawing from Philox4x32-10 (kpx_problem.rng = KPX_RNG_PHILOX): own translation units
+cudaError_t launch_plan_f64p(const PlanLaunch& L, cudaStream_t st);
+cudaError_t launch_plan_f32p(const PlanLaunch& L, cudaStream_t st);
+cudaError_t launch_plan_f32latp(const PlanLaunch& L, cudaStream_t st);
+cudaError_t launch_batch_f64p(const BatchLaunch& L, cudaStream_t st);
+cudaError_t launch_batch_f32p(const BatchLaunch& L, cudaStream_t st);
+int plan_blocks_per_sm_f64p(int model_id, int n, size_t smem, bool latency);
+int plan_blocks_per_sm_f32p(int model_id, int n, size_t smem, bool latency);
+int plan_blocks_per_sm_f32latp(int model_id, int n, size_t smem, bool latency);
 // host: occupancy masks (kOccGrid^3 words) computed with the launch precision's own cell arithmetic
 void occupancy_masks_f64(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);
 void occupancy_masks_f32(const kpx_problem& pr, int n_obs, const double* omin, const double* omax, uint32_t* masks);

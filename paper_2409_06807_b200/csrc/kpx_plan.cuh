@@ -524,13 +524,13 @@ template <class M, class R>
 __device__ __forceinline__ int prepass_item(const PlanArgs<R>& A, const Workspace& W, uint64_t h0, int slot, int ext,
                                             bool* free_out, ItemOut<R, M::N>& o) {
     *free_out = false;
-    if constexpr (FreeFlight<M, R>::kEnabled) {
+    if constexpr (FreeFlight<typename M::Base, R>::kEnabled) {
         constexpr int N = M::N, NU = M::NU;
         R u[NU], dt, x0[N];
         int S;
         sample_control<M, R>(A.P, h0, slot, ext, u, &dt, &S, nullptr, nullptr);
         load_row<N>((const R*)W.states, slot, x0);
-        const int verdict = FreeFlight<M, R>::certify(A.P, x0, u, dt, S, o);
+        const int verdict = FreeFlight<typename M::Base, R>::certify(A.P, x0, u, dt, S, o);
         if (verdict != kFlightFull) {
             map_end_state<M, R>(A.P, o.end, true, verdict == kFlightValid, o);
             *free_out = true;
@@ -558,7 +558,7 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
     const bool sorted = RS.sorted != 0;
     const bool tiled = sorted && team_ctas == 1;
     uint8_t* const s_len = (uint8_t*)(kpx_dyn_smem + Scene<R>::kCoop);   // [kTileM]; the staging area is idle while sorting
-    constexpr int kTileM = (FreeFlight<M, R>::kEnabled ? KPX_TILE_CHUNKS_FREE : KPX_TILE_CHUNKS) * kChunk;   // items per tile
+    constexpr int kTileM = (FreeFlight<typename M::Base, R>::kEnabled ? KPX_TILE_CHUNKS_FREE : KPX_TILE_CHUNKS) * kChunk;   // items per tile
     static_assert(sizeof(WarpCoop<R>) * kWarps >= kTileM, "tile lengths must fit the staging area");
     int tile = -kTileM, n_units = 0, tile_limit = 0;
     int unit = sorted ? 0x3fffffff : (team_rank * kBlock + tid) >> 5;    // unsorted: this warp's slice of the one round
@@ -604,7 +604,7 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
                             atomicAdd(&s_bin[S], 1);
                         }
                     }
-                    if constexpr (FreeFlight<M, R>::kEnabled) {
+                    if constexpr (FreeFlight<typename M::Base, R>::kEnabled) {
                         const unsigned fm = __ballot_sync(0xffffffffu, free);
                         if (fm) {
                             commit_item<M, R>(A, W, Q, RS.claim_tag, RS.par, free, w, fpos, o);
@@ -789,7 +789,7 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
     }
     const int items = (int)items_ll;
     const int n_sch_old = (size + kChunk - 1) / kChunk;
-    const uint64_t h0 = iter_hash(Q.seed, (uint64_t)it);
+    const uint64_t h0 = iter_key(M::kRng, Q.seed, (uint64_t)it);
     const bool sorted = items > tthreads;
     if (tid == 0) {
         RS.it = it; RS.iters = iters + 1; RS.lam = lam; RS.items = items; RS.n_sch_old = n_sch_old; RS.par = it & 1;
@@ -804,7 +804,7 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
         // Results stay indexed by the item number w, so nothing downstream sees the processing order.
         // An iteration that fits in one round (items <= team threads) gains nothing from it and skips S0.
         const bool global_sort = sorted && T.ctas > 1;    // one-CTA teams sort tile by tile inside S1
-        if constexpr (FreeFlight<M, R>::kEnabled) {
+        if constexpr (FreeFlight<typename M::Base, R>::kEnabled) {
             // Models with the free-flight certificate: ONE pass.  Most items are finished right here from the closed
             // form (positions from the end of the iteration's range); what is left is a fraction of a round of the
             // team's threads, so it is only compacted (positions from the start, in arrival order), not sorted --
@@ -950,7 +950,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                     bool kp = first;
                     if (!kp) {
                         const int slot = __ldcg(W.it_parent + w);
-                        const double ua = keyed_uniform(h0, (uint64_t)slot, (uint64_t)(w % lam), PH_ACCEPT);
+                        const double ua = keyed_uniform_of<M::kRng>(h0, (uint64_t)slot, (uint64_t)(w % lam), PH_ACCEPT);
                         kp = ua < p_accept_of(region, W.score, total_prev, P.epsilon);
                     }
                     keep[j] = kp;
@@ -1063,13 +1063,16 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
                     uint8_t t = tg[j];
                     if (s < size) {
                         const double p = p_accept_of(rg[j], W.score, total, P.epsilon);
-                        const uint64_t hs = slot_ext_hash(h0, (uint64_t)s, 0ull);
+                        constexpr bool philox = M::kRng == KPX_RNG_PHILOX;
+                        const uint64_t hs = philox ? 0ull : slot_ext_hash(h0, (uint64_t)s, 0ull);
                         if (t == KPX_TAG_EXPAND) {                                     // phase A, planner.py:219-225
-                            const double ud = unit53(draw_u64(mix64(hs ^ (uint64_t)PH_DEMOTE), 0));
+                            const double ud = philox ? keyed_uniform_of<KPX_RNG_PHILOX>(h0, (uint64_t)s, 0ull, PH_DEMOTE)
+                                                     : unit53(draw_u64(mix64(hs ^ (uint64_t)PH_DEMOTE), 0));
                             if (ud >= p) t = KPX_TAG_OPEN;
                         }
                         if (t == KPX_TAG_OPEN) {                                       // phase C, planner.py:251-257
-                            const double up = unit53(draw_u64(mix64(hs ^ (uint64_t)PH_PROMOTE), 0));
+                            const double up = philox ? keyed_uniform_of<KPX_RNG_PHILOX>(h0, (uint64_t)s, 0ull, PH_PROMOTE)
+                                                     : unit53(draw_u64(mix64(hs ^ (uint64_t)PH_PROMOTE), 0));
                             if (up < p) t = KPX_TAG_EXPAND;
                         }
                     } else {
@@ -1345,7 +1348,7 @@ template <class M, class R>
 __global__ void __launch_bounds__(kBlock) batch_kernel(const __grid_constant__ BatchArgs<R> A) {
     constexpr int N = M::N, NU = M::NU;
     Scene<R>::stage(A.P, A.obs, A.occ);
-    const uint64_t h0 = iter_hash(A.seed, A.iteration);
+    const uint64_t h0 = iter_key(M::kRng, A.seed, A.iteration);
     // whole warps iterate together (integrate_and_map is warp-synchronous); lanes past the end idle
     for (long long base = (long long)blockIdx.x * kBlock; base < A.items; base += (long long)gridDim.x * kBlock) {
         const long long w = base + threadIdx.x;
@@ -1376,7 +1379,7 @@ __global__ void __launch_bounds__(kBlock) batch_kernel(const __grid_constant__ B
         A.o_valid[w] = o.valid ? 1 : 0;
         A.o_region[w] = o.region;
         A.o_sub[w] = o.sub;
-        A.o_accept[w] = keyed_uniform(h0, (uint64_t)slot, (uint64_t)ext, PH_ACCEPT);
+        A.o_accept[w] = keyed_uniform_of<M::kRng>(h0, (uint64_t)slot, (uint64_t)ext, PH_ACCEPT);
         if (A.o_substeps) A.o_substeps[w] = o.substeps;
         if (A.o_points) A.o_points[w] = o.points;
     }

@@ -110,7 +110,7 @@ class KinoPax:
         self.backend = get_backend(backend, model)
         self.precision = self.backend.precision
         self._lib = _lib.load()
-        self._prob_struct, self._keep = _lib.problem_from(self.problem)
+        self._prob_struct, self._keep = _lib.problem_from(self.problem, rng=self.backend.rng)
         self._handle = _lib._vp()
         self._traj_buf = None         # reusable host buffers of _trajectory
         _lib.check(self._lib.kpx_plan_create(C.byref(self._prob_struct), self.precision, int(team_ctas), int(device),
@@ -359,7 +359,8 @@ class KinoPax:
 
     def _solve_f64_retry(self, t0, trace_fn, capture_tree) -> PlanResult:
         if self._retry is None:
-            self._retry = KinoPax(self.cfg, self.env, self.model, self.problem.check_resolution, backend="cuda",
+            self._retry = KinoPax(self.cfg, self.env, self.model, self.problem.check_resolution,
+                                  backend="cuda-philox" if self.backend.rng == _lib.RNG_PHILOX else "cuda",
                                   team_ctas=self.team_ctas, device=self.device)
         self._retry.reset(self.seed, self.start, self.goal4)
         res = self._retry.solve(trace_fn=trace_fn, capture_tree=capture_tree)

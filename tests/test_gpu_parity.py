@@ -480,3 +480,77 @@ def test_set_obstacles_capacity(kp):
         _lib.check(eng._lib.kpx_plan_set_obstacles(eng._handle, 0, None, None), "set")
         eng.reset()
         assert eng.solve().solved
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# Philox4x32-10 production stream (north_star: "draws controls from a counter-based Philox stream")
+
+def test_philox_known_answers_on_device(kp):
+    from test_host import PHILOX_KAT
+    from paper_2409_06807_b200 import _lib
+    lib = _lib.load()
+    for ctr, key, want in PHILOX_KAT:
+        c, k = np.array(ctr, np.uint32), np.array(key, np.uint32)
+        host, dev = np.zeros(4, np.uint32), np.zeros(4, np.uint32)
+        _lib.check(lib.kpx_philox4x32(_lib.ptr(c), _lib.ptr(k), _lib.ptr(host), _lib.ptr(dev)), "kpx_philox4x32")
+        assert tuple(int(x) for x in dev) == want and np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("model_name", ["di6", "quad12"])
+def test_philox_kernel_draws_match_the_host_stream(kp, model_name):
+    """The kernel seam with the Philox backends: every item's controls, duration and gate uniform are the draws of
+    the host twin's stream (seed, iteration, slot, extension, phase) -- tests/test_rng.py:70-102 for the production
+    generator -- for both precisions; and the integration that follows is the same code as in the parity mode."""
+    from paper_2409_06807_b200.rng import PHASE_ACCEPT, PHASE_SAMPLE, PhiloxStream
+    g = np.load(os.path.join(GOLDEN, f"batch_{model_name}.npz"))
+    model = kp.get_model(model_name)
+    ctx = _ctx_from_golden(kp, g, model)
+    lam, it = int(g["lam"]), int(g["iteration"])
+    slots = g["e_slots"][:40]
+    out = {name: kp.get_backend(name).propagate_batch(ctx, g["states"], slots, lam, it) for name in ("cuda-philox", "cuda-f32-philox")}
+    for b in out.values():
+        for i, slot in enumerate(slots):
+            for ext in range(lam):
+                w = i * lam + ext
+                s = PhiloxStream(int(g["seed"]), it, int(slot), ext, PHASE_SAMPLE)
+                assert b.control[w].tolist() == [s.uniform_in(model.control_lo[j], model.control_hi[j]) for j in range(model.control_dim)]
+                assert b.dt[w] == s.duration(float(g["t_prop"]))
+                assert b.accept_u[w] == PhiloxStream(int(g["seed"]), it, int(slot), ext, PHASE_ACCEPT).uniform()
+    a, b = out["cuda-philox"], out["cuda-f32-philox"]
+    both = (a.valid == 1) & (b.valid == 1)
+    assert both.sum() >= 40 and np.array_equal(a.region[both], b.region[both])
+    assert np.max(_wrap_diff(a.end, b.end, model.wrap_dims)[both] / np.maximum(np.abs(a.end[both]), 1.0)) < F32_RTOL
+    assert not np.array_equal(a.control, kp.get_backend("cuda").propagate_batch(ctx, g["states"], slots, lam, it).control)
+
+
+def test_philox_plans_solve_revalidate_and_do_not_depend_on_the_team(kp):
+    """Whole plans on the Philox stream: deterministic for any team size, solutions re-validated by the host checker,
+    success over 100 seeds of the full-size Trees configuration statistically equal to the reference's."""
+    import json
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=20000, seed=3)
+    snaps = []
+    for team in (0, 1, 8):
+        with kp.KinoPax(cfg, env, model, backend="cuda-philox", team_ctas=team) as eng:
+            res = eng.solve(capture_tree=True)
+            snaps.append(res.tree_snapshot)
+            assert res.solved and kp.ValidityChecker(env, model, 0.05).trajectory_valid(res.trajectory, start=env.start)
+    for sn in snaps[1:]:
+        assert sn["size"] == snaps[0]["size"]
+        for k in ("states", "parent", "tag", "region", "dt", "control"):
+            assert np.array_equal(sn[k], snaps[0][k]), k
+    ref = kp.plan(cfg, env, model, backend="cuda", capture_tree=True).tree_snapshot
+    assert ref["size"] != snaps[0]["size"] or not np.array_equal(ref["dt"], snaps[0]["dt"])      # other random numbers
+    gold = json.load(open(os.path.join(GOLDEN, "outcomes_di6_forest.json")))
+    ref_solved = sum(1 for r in gold["records"] if r["status"] == "solved")
+    full = kp.PlannerConfig(t_e=model.default_t_e, lambda_max=32, t_prop=model.default_t_prop, epsilon=0.005, delta=1.0,
+                            cells_per_dim=model.default_cells_per_dim, subcells_per_dim=4, t_max=60.0, seed=0)
+    with kp.BatchPlanner(full, env, model, backend="cuda-f32-philox", team_ctas=1) as bp:
+        r = bp.run(np.arange(100))
+    assert abs(int(r.solved.sum()) - ref_solved) <= 4 and r.validated.sum() == r.solved.sum()
+    with kp.KinoPax(full, env, model, backend="cuda-f32-philox") as eng:                         # batch == single query
+        for q in (0, 17):
+            eng.reset(seed=q)
+            one = eng.solve()
+            assert one.stats.iterations == r.records["iterations"][q] and one.stats.tree_size == r.records["tree_size"][q]

@@ -275,3 +275,32 @@ def test_cull_tables_are_conservative(kp, precision):
         for k in range(len(omin)):
             assert np.all((m[inside[:, k]] >> np.uint32(k)) & 1), (scene, k)
         assert inside.any()
+
+
+# Random123 known-answer vectors for Philox4x32-10 (kat_vectors of the Random123 distribution): counter, key, output
+PHILOX_KAT = [((0, 0, 0, 0), (0, 0), (0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8)),
+              ((0xffffffff,) * 4, (0xffffffff,) * 2, (0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd)),
+              ((0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344), (0xa4093822, 0x299f31d0),
+               (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1))]
+
+
+def test_philox_known_answers_host(kp):
+    """The production generator against the published vectors: the Python twin (rng.philox4x32_10) and the C++ one
+    compiled into libkpx.so (host half of kpx_philox4x32; the device half is checked under -m gpu)."""
+    from paper_2409_06807_b200 import _lib, rng
+    lib = _lib.load()
+    for ctr, key, want in PHILOX_KAT:
+        assert rng.philox4x32_10(ctr, key) == want
+        c, k, out = np.array(ctr, np.uint32), np.array(key, np.uint32), np.zeros(4, np.uint32)
+        _lib.check(lib.kpx_philox4x32(_lib.ptr(c), _lib.ptr(k), _lib.ptr(out), None), "kpx_philox4x32")
+        assert tuple(int(x) for x in out) == want
+    # streams: distinct identities give distinct draws, uniforms lie in [0, 1), durations in (0, t_prop]
+    s = rng.PhiloxStream(7, iteration=3, slot=11, extension=2, phase=rng.PHASE_SAMPLE)
+    draws = [s.next_u64() for _ in range(6)]
+    assert len(set(draws)) == 6
+    other = rng.PhiloxStream(7, iteration=3, slot=11, extension=3, phase=rng.PHASE_SAMPLE)
+    assert other.next_u64() not in draws
+    u = [rng.PhiloxStream(1, slot=i).uniform() for i in range(2000)]
+    assert 0.0 <= min(u) and max(u) < 1.0 and abs(np.mean(u) - 0.5) < 0.03
+    assert all(0.0 < rng.PhiloxStream(2, slot=i).duration(0.5) <= 0.5 for i in range(200))
+    assert kp.get_backend("cuda-f32-philox").rng == _lib.RNG_PHILOX and kp.get_backend("cuda").rng == _lib.RNG_SPLITMIX64
