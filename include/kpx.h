@@ -65,7 +65,10 @@ typedef struct kpx_problem {
     int32_t grid_n;     /* grid spans state dims [0, grid_n); reference: grid_n == n */
     int32_t lambda_max; /* PlannerConfig.lambda_max */
     int32_t rng;        /* KPX_RNG_SPLITMIX64: the reference's streams (rng.py:30-54), bit-parity; KPX_RNG_PHILOX: Philox4x32-10 */
-    int64_t t_e;        /* tree capacity */
+    int64_t t_e;        /* tree capacity: nodes the arena is allocated for */
+    int64_t t_e_start;  /* adaptive capacity (paper, Remark 1; not in the reference package): capacity in effect at the
+                           start, 0 = t_e.  A run that would end CAPACITY_EXHAUSTED multiplies it by t_e_growth (never */
+    double t_e_growth;  /* beyond t_e) and carries on; t_e_growth <= 1 keeps the capacity fixed */
     double t_prop, check_res, epsilon, delta;
     double control_lo[KPX_MAX_CONTROL], control_hi[KPX_MAX_CONTROL];
     double state_lo[KPX_MAX_DIM], state_hi[KPX_MAX_DIM];
@@ -90,6 +93,7 @@ typedef struct kpx_stats {
     uint64_t boxsteps;       /* substeps whose state-box test ran */
     uint64_t launches;       /* kernel launches issued by this call */
     uint64_t free_items;     /* extensions certified valid and finished from the closed form (float32 double integrators) */
+    int64_t capacity;        /* tree capacity in effect when the run ended (> t_e_start after adaptive growth) */
 } kpx_stats;
 
 /* IterationTrace (planner.py:121-131). */
@@ -238,6 +242,7 @@ typedef struct kpx_query_result {
     int64_t tree_size, solution_slot, chain_len;
     double device_ms;
     uint64_t items, substeps, points, boxsteps, free_items;
+    int64_t capacity;    /* tree capacity in effect when the query ended */
     int32_t checked;     /* kpx_batch_validate: 1 = solution re-validated in float64, -1 = rejected, 0 = not checked */
     int32_t check_code;  /* 0 ok, 3 a state or interpolant is invalid, 4 goal missed, 5 chain longer than max_chain */
 } kpx_query_result;

@@ -58,6 +58,7 @@ class Plan(C.Structure):
         ("tr_branching", C.c_int64), ("tr_ve", C.c_int64), ("tr_vo", C.c_int64), ("tr_attempted", C.c_int64),
         ("tr_valid", C.c_int64), ("tr_staged", C.c_int64), ("tr_appended", C.c_int64),
         ("total_substeps", C.c_int64), ("total_points", C.c_int64), ("total_items", C.c_int64),
+        ("t_e_alloc", C.c_int64), ("growth", C.c_double), ("growths", C.c_int64),
     ]
 
 
@@ -107,6 +108,8 @@ def lib():
         L.kpo_plan_step.argtypes = [C.POINTER(Plan), C.c_int]
         L.kpo_plan_step_given.restype = C.c_int
         L.kpo_plan_step_given.argtypes = [C.POINTER(Plan), C.c_int, C.c_int64, _P, _P, _P, _P, _P]
+        L.kpo_plan_set_capacity.restype = C.c_int
+        L.kpo_plan_set_capacity.argtypes = [C.POINTER(Plan), C.c_int64, C.c_double]
         L.kpo_plan_solve.restype = C.c_int
         L.kpo_plan_solve.argtypes = [C.POINTER(Plan), C.c_double, C.c_int64, C.POINTER(C.c_double)]
         L.kpo_plan_chain.restype = C.c_int64
@@ -245,6 +248,13 @@ class OraclePlan:
         if st < 0:
             raise ValueError("supplied batch does not match this plan's item count")
         return st
+
+    def set_capacity(self, t_e_start, growth):
+        """Adaptive capacity (Remark 1 -- an extension the reference package does not have): this
+        plan was created with room for its t_e nodes; start with ``t_e_start`` in effect and multiply by ``growth``
+        (never beyond the allocation) whenever the run would end with capacity_exhausted."""
+        if self._L.kpo_plan_set_capacity(self._p, int(t_e_start), float(growth)) != 0:
+            raise ValueError("bad capacity arguments (or the plan has already stepped)")
 
     def solve(self, t_max=60.0, max_iters=0):
         el = C.c_double(0.0)

@@ -29,7 +29,7 @@ class Problem(C.Structure):
     _fields_ = [
         ("model_id", C.c_int32), ("n", C.c_int32), ("nu", C.c_int32), ("n_obs", C.c_int32),
         ("subcells", C.c_int32), ("grid_n", C.c_int32), ("lambda_max", C.c_int32), ("rng", C.c_int32),
-        ("t_e", C.c_int64),
+        ("t_e", C.c_int64), ("t_e_start", C.c_int64), ("t_e_growth", C.c_double),
         ("t_prop", C.c_double), ("check_res", C.c_double), ("epsilon", C.c_double), ("delta", C.c_double),
         ("control_lo", C.c_double * MAX_CONTROL), ("control_hi", C.c_double * MAX_CONTROL),
         ("state_lo", C.c_double * MAX_DIM), ("state_hi", C.c_double * MAX_DIM),
@@ -44,7 +44,7 @@ class Stats(C.Structure):
         ("status", C.c_int32), ("iterations", C.c_int32), ("tree_size", C.c_int64), ("solution_slot", C.c_int64),
         ("chain_len", C.c_int64), ("device_ms", C.c_double), ("reset_ms", C.c_double),
         ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("boxsteps", C.c_uint64), ("launches", C.c_uint64),
-        ("free_items", C.c_uint64),
+        ("free_items", C.c_uint64), ("capacity", C.c_int64),
     ]
 
 
@@ -61,14 +61,14 @@ class QueryResult(C.Structure):
         ("status", C.c_int32), ("iterations", C.c_int32), ("tree_size", C.c_int64), ("solution_slot", C.c_int64),
         ("chain_len", C.c_int64), ("device_ms", C.c_double),
         ("items", C.c_uint64), ("substeps", C.c_uint64), ("points", C.c_uint64), ("boxsteps", C.c_uint64),
-        ("free_items", C.c_uint64), ("checked", C.c_int32), ("check_code", C.c_int32),
+        ("free_items", C.c_uint64), ("capacity", C.c_int64), ("checked", C.c_int32), ("check_code", C.c_int32),
     ]
 
 
 QUERY_RESULT_DTYPE = np.dtype([
     ("status", np.int32), ("iterations", np.int32), ("tree_size", np.int64), ("solution_slot", np.int64),
     ("chain_len", np.int64), ("device_ms", np.float64), ("items", np.uint64), ("substeps", np.uint64),
-    ("points", np.uint64), ("boxsteps", np.uint64), ("free_items", np.uint64), ("checked", np.int32),
+    ("points", np.uint64), ("boxsteps", np.uint64), ("free_items", np.uint64), ("capacity", np.int64), ("checked", np.int32),
     ("check_code", np.int32)], align=True)
 
 _SIGNATURES = {
@@ -164,13 +164,17 @@ def ptr(a):
 
 def make_problem(model_id, n, nu, t_e, lambda_max, t_prop, check_res, epsilon, delta, control_lo, control_hi,
                  state_lo, state_hi, obs_min, obs_max, grid_lo, grid_width, grid_cells, grid_strides, subcells,
-                 rng=RNG_SPLITMIX64):
+                 rng=RNG_SPLITMIX64, t_e_max=None, t_e_growth=2.0):
     """Flatten into ``kpx_problem``.  Returns (struct, keepalive) -- keep both alive during calls."""
     if n > MAX_DIM or nu > MAX_CONTROL:
         raise ValueError("state/control dimension exceeds kernel limits")
     p = Problem()
     p.model_id, p.n, p.nu, p.subcells = int(model_id), int(n), int(nu), int(subcells)
     p.grid_n, p.lambda_max, p.t_e = len(grid_lo), int(lambda_max), int(t_e)
+    if t_e_max is not None and int(t_e_max) != int(t_e):     # adaptive capacity: allocate for t_e_max, start at t_e
+        if int(t_e_max) < int(t_e) or not float(t_e_growth) > 1.0:
+            raise ConfigError("adaptive capacity needs t_e_max >= t_e and t_e_growth > 1")
+        p.t_e, p.t_e_start, p.t_e_growth = int(t_e_max), int(t_e), float(t_e_growth)
     p.rng = int(rng)
     p.t_prop, p.check_res, p.epsilon, p.delta = float(t_prop), float(check_res), float(epsilon), float(delta)
     for j in range(nu):
@@ -188,7 +192,7 @@ def make_problem(model_id, n, nu, t_e, lambda_max, t_prop, check_res, epsilon, d
     return p, (omin, omax)
 
 
-def problem_from(prob, rng=RNG_SPLITMIX64) -> tuple:
+def problem_from(prob, rng=RNG_SPLITMIX64, t_e_max=None, t_e_growth=2.0) -> tuple:
     """``Problem`` (problem.py) -> ``kpx_problem``."""
     m, g, c = prob.model, prob.grid, prob.cfg
     if m.kernel_id is None:
@@ -196,4 +200,4 @@ def problem_from(prob, rng=RNG_SPLITMIX64) -> tuple:
     return make_problem(m.kernel_id, m.n, m.control_dim, c.t_e, c.lambda_max, c.t_prop, prob.check_resolution,
                         c.epsilon, c.delta, m.control_lo, m.control_hi, prob.state_lo, prob.state_hi,
                         prob.env.obstacles_min, prob.env.obstacles_max, g.lo, g.widths, g.cells, g.strides,
-                        g.subcells, rng=rng)
+                        g.subcells, rng=rng, t_e_max=t_e_max, t_e_growth=t_e_growth)

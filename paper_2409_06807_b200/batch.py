@@ -90,13 +90,14 @@ class BatchPlanner:
 
     def __init__(self, cfg: PlannerConfig, env: Environment, model: DynamicsModel, check_resolution: float = 0.05,
                  backend: Optional[str] = None, n_teams: int = 0, team_ctas: int = 1, max_chain: int = 64,
-                 device: int = 0):
+                 device: int = 0, t_e_max: Optional[int] = None, t_e_growth: float = 2.0):
         self.problem = build_problem(cfg, env, model, check_resolution)
         self.cfg, self.env, self.model = cfg, env, model
         self.backend = get_backend(backend, model)
         self.precision = self.backend.precision
         self._lib = _lib.load()
-        self._prob_struct, self._keep = _lib.problem_from(self.problem, rng=self.backend.rng)
+        self.t_e_max, self.t_e_growth = t_e_max, t_e_growth     # adaptive capacity, see KinoPax
+        self._prob_struct, self._keep = _lib.problem_from(self.problem, rng=self.backend.rng, t_e_max=t_e_max, t_e_growth=t_e_growth)
         self.max_chain, self.device = int(max_chain), device
         self._handle = _lib._vp()
         # n_teams <= 0: as many teams as are co-resident on the device for this model and precision
@@ -188,7 +189,7 @@ class BatchPlanner:
                     self._f64 = BatchPlanner(self.cfg, self.env, self.model, self.problem.check_resolution,
                                              "cuda-philox" if self.backend.rng == _lib.RNG_PHILOX else "cuda",
                                              n_teams=int(min(len(bad), 8)), team_ctas=16, max_chain=self.max_chain,
-                                             device=self.device)
+                                             device=self.device, t_e_max=self.t_e_max, t_e_growth=self.t_e_growth)
                 r64 = self._f64.run(seeds[bad], starts[bad], goals[bad], tm, True, stream, False,
                                     validate_resolution)
                 res.records[bad] = r64.records

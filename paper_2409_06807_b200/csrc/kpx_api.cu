@@ -50,6 +50,8 @@ int check_problem(const kpx_problem* pr) {
     if (pr->rng != KPX_RNG_SPLITMIX64 && pr->rng != KPX_RNG_PHILOX) return fail(KPX_E_ARG, "unknown rng");
     if (pr->n_obs < 0 || (pr->n_obs > 0 && (!pr->obs_min || !pr->obs_max))) return fail(KPX_E_ARG, "bad obstacles");
     if (pr->subcells < 1 || pr->lambda_max < 1 || pr->t_e < 1) return fail(KPX_E_ARG, "bad configuration");
+    if (pr->t_e_start < 0 || pr->t_e_start > pr->t_e || (pr->t_e_start > 0 && !(pr->t_e_growth >= 1.0)))
+        return fail(KPX_E_ARG, "adaptive capacity needs 1 <= t_e_start <= t_e and t_e_growth >= 1");
     double regions = 1.0;
     for (int d = 0; d < pr->grid_n; ++d) regions *= (double)pr->grid_cells[d];
     if (regions * pr->subcells * pr->subcells * pr->subcells >= 1073741824.0)
@@ -775,7 +777,7 @@ int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_overr
     out->device_ms = (double)c.elapsed_ns * 1e-6;      // run clock: summed over the launches since the reset
     out->reset_ms = (double)(c.t_reset_done - c.t_begin) * 1e-6;
     out->items = c.sum_items; out->substeps = c.sum_substeps; out->points = c.sum_points;
-    out->boxsteps = c.sum_boxsteps; out->free_items = c.sum_free;
+    out->boxsteps = c.sum_boxsteps; out->free_items = c.sum_free; out->capacity = c.cap;
     out->launches = b.launches - l0;
     return KPX_OK;
 }
@@ -986,6 +988,7 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     memset(&c, 0, sizeof c);
     c.size = (int)rows; c.iteration = iteration; c.status = KPX_RUNNING; c.solution_slot = -1; c.total_prev = total;
     c.ve = ve; c.first_hit_w = 0x7fffffff; c.rescue_slot = 0x7fffffff;
+    c.cap = (int)(b.prob.t_e_start > 0 ? std::max<int64_t>(b.prob.t_e_start, rows) : b.prob.t_e);
     c.epoch_used = load_epoch; c.epoch_valid = 0;      // resumed with this epoch; the next reset is dense
     CU(cudaMemcpy(w.ctl, &c, sizeof c, cudaMemcpyHostToDevice));
     // t_reset_done stays 0: the first resumed launch stamps the start of the run clock itself

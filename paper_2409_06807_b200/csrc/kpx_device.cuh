@@ -204,7 +204,9 @@ __device__ __forceinline__ double keyed_uniform_of(uint64_t h0, uint64_t slot, u
 template <class R>
 struct Params {
     int n, nu, n_obs, subcells, grid_n, lambda_max;
-    long long t_e;
+    long long t_e;                        // nodes the arena holds
+    long long t_e_start;                  // capacity in effect at the start (0: t_e) and its growth factor when a run
+    double t_e_growth;                    // would end exhausted (adaptive t_e); <= 1: fixed capacity
     double t_prop, epsilon, delta, vol;   // RNG / estimates always in f64
     double control_lo[KPX_MAX_CONTROL], control_span[KPX_MAX_CONTROL];  // span = hi - lo (f64, as reference)
     R check_res;
@@ -237,7 +239,7 @@ inline R sqrt_threshold(R thr) {
 template <class R>
 inline void fill_params(Params<R>& P, const kpx_problem& pr) {
     P.n = pr.n; P.nu = pr.nu; P.n_obs = pr.n_obs; P.subcells = pr.subcells; P.grid_n = pr.grid_n;
-    P.lambda_max = pr.lambda_max; P.t_e = pr.t_e;
+    P.lambda_max = pr.lambda_max; P.t_e = pr.t_e; P.t_e_start = pr.t_e_start; P.t_e_growth = pr.t_e_growth;
     P.t_prop = pr.t_prop; P.epsilon = pr.epsilon; P.delta = pr.delta;
     P.vol = pr.grid_width[0] * pr.grid_width[1] * pr.grid_width[2];  // decomposition.py:64
     for (int j = 0; j < KPX_MAX_CONTROL; ++j) {

@@ -103,6 +103,7 @@ struct Ctl {                      // one per workspace, global memory
     // do not count the host's idle time between launches; planner.py:282 compares against t_max)
     unsigned long long elapsed_ns;
     int n_est;                    // regions in Workspace::est_ids (those the next estimate pass covers)
+    int cap, growths;             // capacity in effect and how often it was raised (adaptive t_e)
 };
 
 constexpr int kBins = 64;          // substep-count bins of the S0 counting sort (S >= 63 share the last bin)
@@ -118,6 +119,7 @@ struct ResultPacket {             // everything the host needs after a run, one 
 
 struct RunState {                 // CTA-uniform state of the running query, shared memory (one copy per CTA)
     int size, it, status, solution_slot, ve, iters;
+    int cap;                      // tree capacity in effect (t_e, or what adaptive growth has made of t_e_start)
     double total_prev;
     unsigned long long t_start;   // keeper only
     // header of the current iteration
@@ -660,7 +662,6 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
     constexpr int N = M::N, NU = M::NU;                                                                      \
     const Params<R>& P = A.P;                                                                                \
     const int tid = threadIdx.x;                                                                             \
-    const int cap = (int)P.t_e;                                                                              \
     const int RG = P.n_regions, SUBS = P.subs_per_region;                                                    \
     const bool keeper = (T.rank == 0 && tid == 0);                                                           \
     const long long tthreads = (long long)T.ctas * kBlock;                                                   \
@@ -668,7 +669,7 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
     R* const states = (R*)W.states; R* const control = (R*)W.control; R* const dts = (R*)W.dt;               \
     R* const it_end = (R*)W.it_end;                                                                          \
     Ctl* const ctl = W.ctl;                                                                                  \
-    (void)N; (void)NU; (void)cap; (void)RG; (void)SUBS; (void)keeper; (void)tthreads; (void)ttid;  \
+    (void)N; (void)NU; (void)RG; (void)SUBS; (void)keeper; (void)tthreads; (void)ttid;  \
     (void)states; (void)control; (void)dts; (void)it_end; (void)ctl; (void)P;
 
 // ---- reset of a team's workspace for a new query ---------------------------------------------------------
@@ -738,6 +739,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             W.parent[0] = -1; W.region[0] = reg; W.tag[0] = KPX_TAG_EXPAND;
             W.cnt_expand[0] = 1; W.e_local[0] = 0;
             ctl->size = 1; ctl->iteration = 0; ctl->solution_slot = in_goal0 ? 0 : -1;
+            ctl->cap = (int)(P.t_e_start > 0 ? P.t_e_start : P.t_e); ctl->growths = 0;
             ctl->status = in_goal0 ? KPX_SOLVED : KPX_RUNNING;      // planner.py:278-280
             ctl->total_prev = 0.0; ctl->ve = 1; ctl->lam_last = 0;
             ctl->first_hit_w = 0x7fffffff; ctl->stop = 0; ctl->rescue_key = 0ull; ctl->rescue_slot = 0x7fffffff;
@@ -765,7 +767,7 @@ template <class M, class R>
 __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
                                                RunState& RS, int* s_prefix, int* s_bin) {
     KPX_PHASE_LOCALS
-    const int size = RS.size, ve = RS.ve, iters = RS.iters;
+    const int size = RS.size, ve = RS.ve, iters = RS.iters, cap = RS.cap;
     int it = RS.it, status = RS.status;
     __syncthreads();                            // every thread holds the state before thread 0 rewrites it
     bool go = status == KPX_RUNNING;
@@ -904,7 +906,7 @@ template <class M, class R>
 __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
                                                RunState& RS, int* s_prefix, int* s_w, double* s_d) {
     KPX_PHASE_LOCALS
-    const int size = RS.size, it = RS.it, lam = RS.lam, items = RS.items, par = RS.par;
+    const int size = RS.size, it = RS.it, lam = RS.lam, items = RS.items, par = RS.par, cap = RS.cap;
     const bool sorted = RS.sorted != 0;
     const uint64_t h0 = RS.h0;
     const uint32_t claim_tag = RS.claim_tag;
@@ -1162,7 +1164,15 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
         if (tid == 0) {
             RS.size = new_size; RS.total_prev = total; RS.ve = ve; RS.n_est = n_est_next;
             if (found) { RS.status = KPX_SOLVED; RS.solution_slot = new_size - 1; }              // planner.py:297-303
-            else if (exhausted) RS.status = KPX_CAPACITY_EXHAUSTED;
+            else if (exhausted) {
+                // adaptive capacity (Remark 1): the arena was reserved for P.t_e nodes, so raising
+                // the capacity in effect by the constant multiple costs nothing -- no reallocation, no copy
+                if (P.t_e_growth > 1.0 && cap < (int)P.t_e) {
+                    const long long grown = (long long)((double)cap * P.t_e_growth);
+                    RS.cap = grown < P.t_e ? (int)grown : (int)P.t_e;
+                    ctl->growths = __ldcg(&ctl->growths) + 1;
+                } else RS.status = KPX_CAPACITY_EXHAUSTED;
+            }
         }
         __syncthreads();
     }
@@ -1177,7 +1187,7 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
     if (keeper) {
         const int size = RS.size, it = RS.it, status = RS.status, solution_slot = RS.solution_slot;
         ctl->size = size; ctl->iteration = it; ctl->status = status; ctl->solution_slot = solution_slot;
-        ctl->total_prev = RS.total_prev; ctl->ve = RS.ve; ctl->n_est = RS.n_est;
+        ctl->total_prev = RS.total_prev; ctl->ve = RS.ve; ctl->n_est = RS.n_est; ctl->cap = RS.cap;
         ctl->elapsed_ns = gtimer() - RS.t_start;
         int len = 0;
         if (status == KPX_SOLVED) {
@@ -1226,7 +1236,7 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
             r.chain_len = len; r.device_ms = (double)(ctl->t_end - __ldcg(&ctl->t_begin)) * 1e-6;
             r.checked = 0; r.check_code = 0;        // filled by kpx_batch_validate
             r.items = __ldcg(&ctl->sum_items); r.substeps = __ldcg(&ctl->sum_substeps); r.points = __ldcg(&ctl->sum_points); r.boxsteps = __ldcg(&ctl->sum_boxsteps);
-            r.free_items = __ldcg(&ctl->sum_free);
+            r.free_items = __ldcg(&ctl->sum_free); r.capacity = RS.cap;
             *res_out = r;
         }
     }
@@ -1256,7 +1266,7 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
         if (threadIdx.x == 0) {
             RS.size = size; RS.it = __ldcg(&ctl->iteration); RS.status = status;
             RS.solution_slot = __ldcg(&ctl->solution_slot); RS.total_prev = __ldcg(&ctl->total_prev);
-            RS.ve = ve; RS.iters = 0; RS.n_est = n_est;
+            RS.ve = ve; RS.iters = 0; RS.n_est = n_est; RS.cap = __ldcg(&ctl->cap);
             RS.claim_tag = __ldcg(&ctl->epoch_used) << A.claim_shift;
             unsigned long long t_start = 0;     // run clock origin; only the keeper thread uses it
             if (T.rank == 0) {

@@ -103,14 +103,18 @@ class KinoPax:
 
     def __init__(self, cfg: PlannerConfig, env: Environment, model: DynamicsModel,
                  check_resolution: float = 0.05, backend: Optional[str] = None, team_ctas: int = 0,
-                 device: int = 0):
+                 device: int = 0, t_e_max: Optional[int] = None, t_e_growth: float = 2.0):
+        """``t_e_max`` / ``t_e_growth``: adaptive tree capacity (the paper's Remark 1, not in the reference package):
+        the arena is reserved for ``t_e_max`` nodes; the run starts with ``cfg.t_e`` in effect and, whenever it would
+        end CAPACITY_EXHAUSTED, multiplies the capacity by ``t_e_growth`` (up to ``t_e_max``) and carries on."""
         self.problem: Problem = build_problem(cfg, env, model, check_resolution)
         self.cfg, self.env, self.model = cfg, env, model
         self.checker = self.problem.checker
         self.backend = get_backend(backend, model)
         self.precision = self.backend.precision
         self._lib = _lib.load()
-        self._prob_struct, self._keep = _lib.problem_from(self.problem, rng=self.backend.rng)
+        self.t_e_max, self.t_e_growth = t_e_max, t_e_growth
+        self._prob_struct, self._keep = _lib.problem_from(self.problem, rng=self.backend.rng, t_e_max=t_e_max, t_e_growth=t_e_growth)
         self._handle = _lib._vp()
         self._traj_buf = None         # reusable host buffers of _trajectory
         _lib.check(self._lib.kpx_plan_create(C.byref(self._prob_struct), self.precision, int(team_ctas), int(device),
@@ -209,7 +213,7 @@ class KinoPax:
 
     def last_items(self) -> dict:
         """The Batch of the most recent iteration as the kernel left it in HBM (+ keep flags)."""
-        cap, n = self.cfg.t_e, self.model.n
+        cap, n = int(self.t_e_max or self.cfg.t_e), self.model.n
         cnt = C.c_int64(0)
         out = {"valid": np.zeros(cap, np.uint8), "region": np.zeros(cap, np.int64), "sub": np.zeros(cap, np.int64),
                "end": np.zeros((cap, n)), "keep": np.zeros(cap, np.uint8), "parent_slot": np.zeros(cap, np.int64),
@@ -345,7 +349,7 @@ class KinoPax:
                                             wall_time_ms=(time.perf_counter() - t0) * 1e3,
                                             solution_duration_s=duration))
         result.device = {"device_ms": st.device_ms, "reset_ms": st.reset_ms, "items": int(st.items),
-                         "substeps": int(st.substeps), "points": int(st.points), "boxsteps": int(st.boxsteps), "free_items": int(st.free_items), "launches": int(st.launches),
+                         "substeps": int(st.substeps), "points": int(st.points), "boxsteps": int(st.boxsteps), "free_items": int(st.free_items), "capacity": int(st.capacity), "launches": int(st.launches),
                          "precision": "f64" if self.precision == _lib.F64 else "f32", "f64_retry": retried,
                          # the raw device status: PlanStatus keeps the reference's four values, so a run stopped by a
                          # race peer (5) reads TIMEOUT there; this tells the two apart
@@ -361,7 +365,8 @@ class KinoPax:
         if self._retry is None:
             self._retry = KinoPax(self.cfg, self.env, self.model, self.problem.check_resolution,
                                   backend="cuda-philox" if self.backend.rng == _lib.RNG_PHILOX else "cuda",
-                                  team_ctas=self.team_ctas, device=self.device)
+                                  team_ctas=self.team_ctas, device=self.device, t_e_max=self.t_e_max,
+                                  t_e_growth=self.t_e_growth)
         self._retry.reset(self.seed, self.start, self.goal4)
         res = self._retry.solve(trace_fn=trace_fn, capture_tree=capture_tree)
         res.stats.wall_time_ms = (time.perf_counter() - t0) * 1e3

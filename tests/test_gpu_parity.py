@@ -554,3 +554,52 @@ def test_philox_plans_solve_revalidate_and_do_not_depend_on_the_team(kp):
             eng.reset(seed=q)
             one = eng.solve()
             assert one.stats.iterations == r.records["iterations"][q] and one.stats.tree_size == r.records["tree_size"][q]
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# Adaptive tree capacity (Remark 1) -- an extension the reference package does not have; the
+# oracle carries the same rule (kpo_plan_set_capacity) so that the device can be held to it bit for bit.
+
+def test_adaptive_capacity_matches_oracle_and_rescues_exhausted_runs(kp, orc):
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    small = small_cfg(kp, model, t_e=1500, seed=3)                    # the reference's own sweep: 6 of 6 seeds fail here
+    assert kp.plan(small, env, model, backend="cuda").status is kp.PlanStatus.CAPACITY_EXHAUSTED
+    big = small_cfg(kp, model, t_e=12000, seed=3)
+    for backend in ("cuda", "cuda-f32"):
+        # arena reserved for 12000 nodes, 1500 in effect, doubled whenever the run would end exhausted
+        op = orc.plan_from_problem(kp.build_problem(big, env, model))
+        op.set_capacity(1500, 2.0)
+        with kp.KinoPax(small, env, model, backend=backend, t_e_max=12000, t_e_growth=2.0) as eng:
+            for it in range(1, 200):
+                st = eng.step()
+                if backend == "cuda":
+                    op.step()
+                    a, b = eng.snapshot(), op.snapshot()
+                    assert a["size"] == b["size"], it
+                    for k in ("parent", "tag", "region", "states", "dt"):
+                        assert np.array_equal(a[k], b[k]), (it, k)
+                    assert int(st.capacity) == int(op.raw.t_e), it
+                    assert eng.traces()[-1].branching == op.trace()["branching"], it
+                if st.status != 4:
+                    break
+            assert st.status == 0 and int(st.capacity) in (3000, 6000, 12000) and int(st.tree_size) > 1500
+            if backend == "cuda":
+                assert op.status == "solved" and int(op.raw.growths) >= 1 and int(st.solution_slot) == int(op.raw.solution_slot)
+    # t_e_max == t_e is the fixed-capacity planner; growth needs a factor above 1 and t_e_max >= t_e
+    with kp.KinoPax(small, env, model, backend="cuda", t_e_max=1500) as eng:
+        assert eng.solve().status is kp.PlanStatus.CAPACITY_EXHAUSTED
+    for kw in ({"t_e_max": 1000}, {"t_e_max": 3000, "t_e_growth": 1.0}):
+        with pytest.raises(kp.ConfigError):
+            kp.KinoPax(small, env, model, backend="cuda", **kw)
+    # the batch path: every seed of the sweep that failed at 1500 nodes is solved, each with the capacity it needed
+    with kp.BatchPlanner(small, env, model, backend="cuda", n_teams=6, team_ctas=1, t_e_max=12000) as bp:
+        res = bp.run(np.arange(3, 9))
+        assert res.solved.all() and res.validated.all()
+        assert set(res.records["capacity"].tolist()) <= {3000, 6000, 12000}
+        for q, seed in ((0, 3), (4, 7)):                            # == the oracle planning the same seed
+            op = orc.plan_from_problem(kp.build_problem(big.with_seed(seed), env, model))
+            op.set_capacity(1500, 2.0)
+            op.solve(t_max=60.0)
+            assert int(op.raw.size) == res.records["tree_size"][q] and int(op.raw.iteration) == res.records["iterations"][q]
+            assert int(op.raw.t_e) == res.records["capacity"][q]

@@ -187,6 +187,36 @@ def test_step_given_equals_step(kp, orc):
         assert a.status == b.status == c.status and a.status in ("solved", "capacity_exhausted")
 
 
+def test_oracle_adaptive_capacity_rule(kp, orc):
+    """kpo_plan_set_capacity (the paper's Remark 1, an extension): with growth 1 or the whole allocation in effect the
+    plan is the reference's; with a small start it carries on past the point where the fixed-capacity plan ends
+    exhausted, and its first iterations are the fixed-capacity plan's."""
+    fixed, _ = _oracle_for(kp, orc, "di6", "forest", 1500, 3)
+    same, _ = _oracle_for(kp, orc, "di6", "forest", 1500, 3)
+    same.set_capacity(1500, 2.0)                                   # nothing to grow into
+    grow, _ = _oracle_for(kp, orc, "di6", "forest", 12000, 3)
+    grow.set_capacity(1500, 2.0)
+    with pytest.raises(ValueError):
+        grow.set_capacity(20000, 2.0)
+    diverged = False
+    for it in range(100):
+        sf = fixed.step()
+        assert same.step() == sf
+        grow.step()
+        if sf == 4:
+            a, b = fixed.snapshot(), grow.snapshot()
+            assert a["size"] == b["size"] and np.array_equal(a["tag"], b["tag"]) and np.array_equal(a["states"], b["states"])
+        else:
+            diverged = True
+            break
+    assert diverged and fixed.status == "capacity_exhausted" and same.status == "capacity_exhausted"
+    assert grow.status == "running" and int(grow.raw.t_e) == 3000 and int(grow.raw.growths) == 1
+    grow.solve(t_max=60.0)
+    assert grow.status == "solved" and int(grow.raw.size) > 1500
+    with pytest.raises(ValueError):
+        grow.set_capacity(1500, 2.0)                               # only before the first iteration
+
+
 def test_outcome_fixtures_are_consistent():
     """Full-size reference outcomes (100 seeds per config) that the GPU success-rate test compares against."""
     for name, min_solved in (("di6_forest", 100), ("dubins6_building", 100), ("quad12_narrow", 50),
