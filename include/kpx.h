@@ -257,6 +257,18 @@ int kpx_batch_run(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const 
                   const double *goals, double t_max, kpx_query_result *results, double *chain_start,
                   double *chain_control, double *chain_dt, double *o_kernel_ms, void *stream);
 
+/*
+ * Obstacle sets a query can name ("scenes"): n_scenes sets of n_obs[s] boxes each, concatenated in obs_min / obs_max
+ * ((sum n_obs, 3) row-major).  Every set must fit the obstacle count the batch was created with; scene 0 replaces the
+ * problem's own.  The workspace box, the model and the configuration are shared.  The reference plans one
+ * Environment per process (envgen.py:127-163, core.py:51-83); this is its batched form.
+ */
+int kpx_batch_set_scenes(kpx_batch *b, int32_t n_scenes, const int32_t *n_obs, const double *obs_min,
+                         const double *obs_max);
+/* kpx_batch_upload with the scene of every query (scene_idx[Q], NULL = all scene 0) */
+int kpx_batch_upload_scenes(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const double *starts,
+                            const double *goals, const int32_t *scene_idx, int32_t want_chains, void *stream);
+
 /* the same in three stream-ordered pieces, so a caller can keep queries resident and re-launch:
  * upload (H2D, synchronous), launch (asynchronous, one persistent kernel), download (D2H, synchronises) */
 int kpx_batch_upload(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const double *starts,

@@ -47,6 +47,7 @@ class BatchResult:
     starts: np.ndarray
     goals: np.ndarray
     replanned: Optional[np.ndarray] = None   # indices re-planned in float64 after the re-validation refused them
+    scenes: Optional[np.ndarray] = None      # scene index per query (None: all in the planner's own environment)
 
     def __len__(self) -> int:
         return len(self.records)
@@ -108,6 +109,40 @@ class BatchPlanner:
         _lib.check(self._lib.kpx_batch_info(self._handle, C.byref(nt), C.byref(tc)), "kpx_batch_info")
         self.n_teams, self.team_ctas = int(nt.value), int(tc.value)
         self._f64 = None              # float64 twin, created when a refused float32 solution needs re-planning
+        self.scenes = [env]           # obstacle sets a query can name (set_scenes); scene 0 is `env`
+        self._scene_probs = {0: (self._prob_struct, self._keep)}
+
+    def set_scenes(self, envs: Sequence[Environment]) -> None:
+        """Obstacle sets the queries of a batch can name (``run(..., scenes=idx)``): the batched form of planning in
+        several ``Environment`` s (reference: one per process, ``envgen.py:127-163``).  The scenes share this planner's
+        workspace box, model and configuration; only the obstacles differ, and none may have more obstacles than the
+        environment the planner was created with.  Starts / goals stay per query."""
+        envs = list(envs)
+        if not envs:
+            raise ConfigError("need at least one scene")
+        for e in envs:
+            if not (np.array_equal(e.workspace_lo, self.env.workspace_lo) and np.array_equal(e.workspace_hi, self.env.workspace_hi)):
+                raise ConfigError("scenes must share the planner's workspace box")
+            if e.n_obstacles > self.env.n_obstacles:
+                raise ConfigError(f"scene '{e.name}' has {e.n_obstacles} obstacles, the planner was created for {self.env.n_obstacles}")
+        counts = np.ascontiguousarray([e.n_obstacles for e in envs], dtype=np.int32)
+        omin = np.ascontiguousarray(np.concatenate([np.asarray(e.obstacles_min, dtype=np.float64).reshape(-1, 3) for e in envs]))
+        omax = np.ascontiguousarray(np.concatenate([np.asarray(e.obstacles_max, dtype=np.float64).reshape(-1, 3) for e in envs]))
+        _lib.check(self._lib.kpx_batch_set_scenes(self._handle, len(envs), _lib.ptr(counts), _lib.ptr(omin), _lib.ptr(omax)),
+                   "kpx_batch_set_scenes")
+        self.scenes = envs
+        self._scene_probs = {}
+        if self._f64 is not None:
+            self._f64.set_scenes(envs)
+
+    def _scene_problem(self, scene: int):
+        """kpx_problem of one scene (host-side checks of a solution need that scene's obstacles)."""
+        if scene not in self._scene_probs:
+            import dataclasses
+            env = dataclasses.replace(self.scenes[scene], start=self.env.start, goal=self.env.goal)
+            prob = build_problem(self.cfg, env, self.model, self.problem.check_resolution)
+            self._scene_probs[scene] = _lib.problem_from(prob, rng=self.backend.rng)
+        return self._scene_probs[scene][0]
 
     def close(self) -> None:
         if getattr(self, "_f64", None) is not None:
@@ -129,6 +164,24 @@ class BatchPlanner:
     def __exit__(self, *exc):
         self.close()
 
+    def _scene_index(self, scenes, q: int):
+        if scenes is None:
+            return None
+        idx = np.ascontiguousarray(scenes, dtype=np.int32)
+        if idx.shape != (q,) or (idx < 0).any() or (idx >= len(self.scenes)).any():
+            raise ConfigError(f"scenes must be {q} indices into the {len(self.scenes)} scenes of set_scenes()")
+        return idx
+
+    def _check_starts_in_scenes(self, starts, scenes) -> None:
+        """planner.py:144-145 per scene: every query's start must be a valid state among ITS scene's obstacles."""
+        if scenes is None:
+            return
+        from .validity import ValidityChecker
+        for sc in np.unique(scenes):
+            ck = ValidityChecker(self.scenes[int(sc)], self.model, self.problem.check_resolution)
+            if not ck.state_valid_batch(starts[scenes == sc]).all():
+                raise ConfigError(f"a start state is invalid in scene {int(sc)} ('{self.scenes[int(sc)].name}')")
+
     def _queries(self, seeds, starts, goals) -> tuple:
         """Host arrays of a batch of queries, checked as the reference checks a single one (planner.py:144-145:
         the start must be a valid state): seeds over the whole uint64 domain (negative seeds wrap, as in
@@ -148,7 +201,7 @@ class BatchPlanner:
 
     def run(self, seeds: Sequence[int], starts=None, goals=None, t_max: Optional[float] = None,
             want_chains: bool = True, stream=None, replan_rejected: bool = True,
-            validate_resolution: Optional[float] = None) -> BatchResult:
+            validate_resolution: Optional[float] = None, scenes=None) -> BatchResult:
         """Plan ``len(seeds)`` queries; ``starts`` (Q, n) / ``goals`` (Q, 4) default to the environment's.
 
         With ``want_chains`` every solution is re-validated on the device in float64
@@ -162,9 +215,11 @@ class BatchPlanner:
             raise ConfigError("need at least one query")
         n, nu = self.model.n, self.model.control_dim
         seeds, starts, goals = self._queries(seeds, starts, goals)
+        scenes = self._scene_index(scenes, q)
+        self._check_starts_in_scenes(starts, scenes)
         tm = float(self.cfg.t_max if t_max is None else t_max)
         t0 = time.perf_counter()
-        if validate_resolution is None or not want_chains:
+        if scenes is None and (validate_resolution is None or not want_chains):
             rec = np.zeros(q, dtype=_lib.QUERY_RESULT_DTYPE)
             cs = cc = cd = None
             if want_chains:
@@ -177,10 +232,12 @@ class BatchPlanner:
                                                stream), "kpx_batch_run")
             res = BatchResult(rec, cs, cc, cd, ms.value, 0.0, starts, goals)
         else:
-            self.upload(seeds, starts, goals, want_chains=True, stream=stream)
+            self.upload(seeds, starts, goals, want_chains=want_chains, stream=stream, scenes=scenes)
             self.launch(tm, stream=stream)
-            self.validate(validate_resolution, stream=stream)
+            if want_chains:
+                self.validate(validate_resolution, stream=stream)
             res = self.download(stream=stream)
+        res.scenes = scenes
         if want_chains and replan_rejected and self.precision != _lib.F64:
             bad = np.flatnonzero(res.rejected)
             if len(bad):
@@ -190,8 +247,10 @@ class BatchPlanner:
                                              "cuda-philox" if self.backend.rng == _lib.RNG_PHILOX else "cuda",
                                              n_teams=int(min(len(bad), 8)), team_ctas=16, max_chain=self.max_chain,
                                              device=self.device, t_e_max=self.t_e_max, t_e_growth=self.t_e_growth)
+                    if len(self.scenes) > 1 or self.scenes[0] is not self.env:
+                        self._f64.set_scenes(self.scenes)
                 r64 = self._f64.run(seeds[bad], starts[bad], goals[bad], tm, True, stream, False,
-                                    validate_resolution)
+                                    validate_resolution, None if scenes is None else scenes[bad])
                 res.records[bad] = r64.records
                 res.chain_start[bad], res.chain_control[bad], res.chain_dt[bad] = r64.chain_start, r64.chain_control, r64.chain_dt
                 res.replanned = bad
@@ -199,11 +258,13 @@ class BatchPlanner:
         return res
 
     # -- resident-input form: upload once, launch many times (what bench.py times with CUDA events) ---
-    def upload(self, seeds, starts=None, goals=None, want_chains: bool = False, stream=None) -> int:
+    def upload(self, seeds, starts=None, goals=None, want_chains: bool = False, stream=None, scenes=None) -> int:
         q = len(seeds)
         seeds, starts, goals = self._queries(seeds, starts, goals)
-        _lib.check(self._lib.kpx_batch_upload(self._handle, q, _lib.ptr(seeds), _lib.ptr(starts), _lib.ptr(goals),
-                                              1 if want_chains else 0, stream), "kpx_batch_upload")
+        scenes = self._scene_index(scenes, q)
+        self._check_starts_in_scenes(starts, scenes)
+        _lib.check(self._lib.kpx_batch_upload_scenes(self._handle, q, _lib.ptr(seeds), _lib.ptr(starts), _lib.ptr(goals),
+                                                     _lib.ptr(scenes), 1 if want_chains else 0, stream), "kpx_batch_upload_scenes")
         self._uploaded = (q, starts, goals, want_chains)
         return q
 
@@ -250,7 +311,8 @@ class BatchPlanner:
                                             _lib.ptr(off)), "kpx_trajectory")
         okc, code = C.c_int32(0), C.c_int32(0)
         goal = np.ascontiguousarray(result.goals[q])
-        _lib.check(self._lib.kpx_trajectory_valid(C.byref(self._prob_struct), L, _lib.ptr(sampled), _lib.ptr(off),
+        prob_struct = self._scene_problem(0 if result.scenes is None else int(result.scenes[q]))
+        _lib.check(self._lib.kpx_trajectory_valid(C.byref(prob_struct), L, _lib.ptr(sampled), _lib.ptr(off),
                                                   _lib.ptr(goal), float(resolution or self.problem.check_resolution), C.byref(okc),
                                                   C.byref(code)), "kpx_trajectory_valid")
         segs = [TrajectorySegment(control=ctrl[i].copy(), dt=float(dts[i]), end_state=sampled[off[i + 1] - 1].copy(),

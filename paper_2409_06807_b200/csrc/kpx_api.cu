@@ -110,6 +110,10 @@ struct kpx_batch {
     int precision = KPX_F64, n_teams = 1, team_ctas = 1, device = 0;
     int max_chunks = 0, max_trace = 4096, max_chain = KPX_MAX_CHAIN;
     int obs_cap = 0;                   // obstacles the device buffers (and the shared-memory scene) were sized for
+    // obstacle sets ("scenes") a query can name: n_scenes x scene_obs boxes, each set padded to scene_obs boxes with
+    // boxes nothing can hit; scene 0 is the problem's own.  prob.n_obs == scene_obs.
+    int n_scenes = 1, scene_obs = 0, scenes_alloc = 0;
+    std::vector<double> sc_min, sc_max;
     bool cooperative = false, latency = false;
     size_t rs = 8, smem = 0;
     int cap = 0, cap_pad = 0, regions = 0, subs = 0, claim_shift = 30;
@@ -163,6 +167,29 @@ int blocks_per_sm(const kpx_batch& b) {
                                       : plan_blocks_per_sm_f32p(b.prob.model_id, b.prob.n, b.smem, b.latency);
     return b.precision == KPX_F64 ? plan_blocks_per_sm_f64(b.prob.model_id, b.prob.n, b.smem, b.latency)
                                   : plan_blocks_per_sm_f32(b.prob.model_id, b.prob.n, b.smem, b.latency);
+}
+
+// (re)build the device copies of every obstacle set: boxes in the launch precision + occupancy tables per scene
+int upload_scenes(kpx_batch& b) {
+    const int k = b.scene_obs;
+    if (b.n_scenes > b.scenes_alloc) {
+        cudaFree(b.obs_dev); cudaFree(b.occ_dev);
+        b.obs_dev = nullptr; b.occ_dev = nullptr;
+        CU(cudaMalloc(&b.obs_dev, 8 * (size_t)std::max(b.obs_cap, 1) * b.rs * (size_t)b.n_scenes));
+        CU(cudaMalloc(&b.occ_dev, 2 * sizeof(uint32_t) * (size_t)kOccCells * (size_t)b.n_scenes));
+        b.scenes_alloc = b.n_scenes;
+    }
+    b.prob.n_obs = k;
+    b.obs_min.assign(b.sc_min.begin(), b.sc_min.begin() + 3 * (size_t)k);      // scene 0: what prob.obs_min points at
+    b.obs_max.assign(b.sc_max.begin(), b.sc_max.begin() + 3 * (size_t)k);
+    b.prob.obs_min = b.obs_min.data(); b.prob.obs_max = b.obs_max.data();
+    cudaFree(b.boxes64_dev); b.boxes64_dev = nullptr;                           // rebuilt on the next validation
+    for (int sc = 0; sc < b.n_scenes; ++sc) {
+        int rc = upload_obstacles(b.prob, b.precision, k, b.sc_min.data() + 3 * (size_t)sc * k, b.sc_max.data() + 3 * (size_t)sc * k,
+                                  (char*)b.obs_dev + 8 * (size_t)k * b.rs * sc, b.occ_dev + 2 * (size_t)kOccCells * sc, 0);
+        if (rc) return rc;
+    }
+    return KPX_OK;
 }
 
 // allocate everything a batch of n_teams workspaces needs
@@ -271,9 +298,8 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     CU(cudaMalloc(&b.ws_dev, sizeof(Workspace) * (size_t)n_teams));
     CU(cudaMemcpy(b.ws_dev, b.ws_host.data(), sizeof(Workspace) * (size_t)n_teams, cudaMemcpyHostToDevice));
     b.obs_cap = prob->n_obs;
-    CU(cudaMalloc(&b.obs_dev, 8 * (size_t)std::max(prob->n_obs, 1) * b.rs));
-    CU(cudaMalloc(&b.occ_dev, 2 * sizeof(uint32_t) * (size_t)kOccCells));
-    rc = upload_obstacles(b.prob, precision, prob->n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
+    b.n_scenes = 1; b.scene_obs = prob->n_obs; b.sc_min = b.obs_min; b.sc_max = b.obs_max;
+    rc = upload_scenes(b);
     if (rc) return rc;
     CU(cudaMalloc(&b.queue_dev, 256));
     CU(cudaMemset(b.queue_dev, 0, 256));
@@ -729,12 +755,41 @@ int kpx_plan_set_obstacles(kpx_plan* p, int32_t n_obs, const double* omin, const
     if (n_obs > b.obs_cap)
         return fail(KPX_E_ARG, "obstacle count %d exceeds the capacity (%d) the plan was created with", n_obs, b.obs_cap);
     CU(cudaSetDevice(b.device));
-    b.prob.n_obs = n_obs;
-    b.obs_min.assign(omin, omin + 3 * (size_t)n_obs);
-    b.obs_max.assign(omax, omax + 3 * (size_t)n_obs);
-    b.prob.obs_min = b.obs_min.data(); b.prob.obs_max = b.obs_max.data();
-    cudaFree(b.boxes64_dev); b.boxes64_dev = nullptr;      // rebuilt on the next validation
-    return upload_obstacles(b.prob, b.precision, n_obs, b.obs_min.data(), b.obs_max.data(), b.obs_dev, b.occ_dev, 0);
+    b.n_scenes = 1; b.scene_obs = n_obs;
+    b.sc_min.assign(omin, omin + 3 * (size_t)n_obs);
+    b.sc_max.assign(omax, omax + 3 * (size_t)n_obs);
+    return upload_scenes(b);
+}
+
+int kpx_batch_set_scenes(kpx_batch* bp, int32_t n_scenes, const int32_t* n_obs, const double* omin, const double* omax) {
+    if (!bp || n_scenes < 1 || !n_obs) return fail(KPX_E_ARG, "bad scene arguments");
+    kpx_batch& b = *bp;
+    int k = 0;
+    size_t total = 0;
+    for (int sc = 0; sc < n_scenes; ++sc) {
+        if (n_obs[sc] < 0) return fail(KPX_E_ARG, "scene %d: negative obstacle count", sc);
+        if (n_obs[sc] > b.obs_cap)
+            return fail(KPX_E_ARG, "scene %d has %d obstacles, the batch was created with room for %d", sc, n_obs[sc], b.obs_cap);
+        k = std::max(k, (int)n_obs[sc]);
+        total += (size_t)n_obs[sc];
+    }
+    if (total && (!omin || !omax)) return fail(KPX_E_ARG, "null obstacle arrays");
+    CU(cudaSetDevice(b.device));
+    // pad every set to k boxes with boxes that lie outside the state box and are empty (min > max): no cell of the
+    // occupancy grid gets their bit and no point or box can overlap them
+    b.sc_min.assign(3 * (size_t)k * n_scenes, 0.0);
+    b.sc_max.assign(3 * (size_t)k * n_scenes, 0.0);
+    size_t src = 0;
+    for (int sc = 0; sc < n_scenes; ++sc)
+        for (int j = 0; j < k; ++j)
+            for (int a = 0; a < 3; ++a) {
+                const size_t dst = 3 * ((size_t)sc * k + j) + a;
+                if (j < n_obs[sc]) { b.sc_min[dst] = omin[3 * (src + j) + a]; b.sc_max[dst] = omax[3 * (src + j) + a]; }
+                else { b.sc_min[dst] = b.prob.state_hi[a] + 1.0; b.sc_max[dst] = b.prob.state_lo[a] - 1.0; }
+                if (a == 2 && j + 1 == k) src += (size_t)n_obs[sc];
+            }
+    b.n_scenes = n_scenes; b.scene_obs = k;
+    return upload_scenes(b);
 }
 
 int kpx_plan_run(kpx_plan* p, double t_max, int32_t max_iters, int32_t lam_override, uint32_t* stop_flag,
@@ -1182,9 +1237,18 @@ void kpx_batch_destroy(kpx_batch* b) {
 
 int kpx_batch_upload(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const double* starts,
                      const double* goals, int32_t want_chains, void* stream) {
+    return kpx_batch_upload_scenes(bp, n_queries, seeds, starts, goals, nullptr, want_chains, stream);
+}
+
+int kpx_batch_upload_scenes(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, const double* starts,
+                            const double* goals, const int32_t* scene_idx, int32_t want_chains, void* stream) {
     if (!bp || !seeds || !starts || !goals) return fail(KPX_E_ARG, "null argument");
     if (n_queries < 1) return fail(KPX_E_ARG, "n_queries must be >= 1");
     kpx_batch& b = *bp;
+    if (scene_idx)
+        for (int64_t i = 0; i < n_queries; ++i)
+            if (scene_idx[i] < 0 || scene_idx[i] >= b.n_scenes)
+                return fail(KPX_E_ARG, "query %lld names scene %d, the batch holds %d", (long long)i, scene_idx[i], b.n_scenes);
     cudaStream_t st = (cudaStream_t)stream;
     CU(cudaSetDevice(b.device));
     int rc = ensure_queries(b, n_queries);
@@ -1196,6 +1260,7 @@ int kpx_batch_upload(kpx_batch* bp, int64_t n_queries, const uint64_t* seeds, co
         b.q_stage[i].seed = seeds[i];
         memcpy(b.q_stage[i].start, starts + i * n, sizeof(double) * n);
         memcpy(b.q_stage[i].goal, goals + i * 4, sizeof(double) * 4);
+        b.q_stage[i].scene = scene_idx ? scene_idx[i] : 0;
     }
     if (want_chains && (!b.bc_start || b.bc_cap < b.q_cap)) {
         cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt);
@@ -1241,10 +1306,10 @@ int kpx_batch_validate(kpx_batch* bp, double res, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     CU(cudaSetDevice(b.device));
     if (!b.boxes64_dev) {
-        const int k = std::max(b.prob.n_obs, 1);
-        std::vector<double> h(8 * (size_t)k, 0.0);
-        for (int j = 0; j < b.prob.n_obs; ++j)
-            for (int a = 0; a < 3; ++a) { h[8 * j + a] = b.obs_min[3 * j + a]; h[8 * j + 4 + a] = b.obs_max[3 * j + a]; }
+        const size_t k = (size_t)b.scene_obs, tot = k * (size_t)b.n_scenes;
+        std::vector<double> h(8 * std::max<size_t>(tot, 1), 0.0);
+        for (size_t j = 0; j < tot; ++j)
+            for (int a = 0; a < 3; ++a) { h[8 * j + a] = b.sc_min[3 * j + a]; h[8 * j + 4 + a] = b.sc_max[3 * j + a]; }
         CU(cudaMalloc(&b.boxes64_dev, h.size() * 8));
         CU(cudaMemcpy(b.boxes64_dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     }

@@ -168,13 +168,19 @@ struct Workspace {                // device pointers of one team's state
     ResultPacket* packet;         // packed copy of ctl + the first kPacketSegs chain segments
 };
 
-struct QueryIn { unsigned long long seed; double start[KPX_MAX_DIM]; double goal[4]; };
+struct QueryIn {
+    unsigned long long seed;
+    double start[KPX_MAX_DIM];
+    double goal[4];
+    int scene;                    // obstacle set of this query (kpx_batch_set_scenes); 0 = the problem's own
+    int pad;
+};
 
 template <class R>
 struct PlanArgs {
     Params<R> P;
-    const R* obs;                 // device boxes [n_obs][8]: min xyz, -, max xyz, -
-    const uint32_t* occ;          // device occupancy masks [kOccGrid^3]
+    const R* obs;                 // device boxes [n_scenes][n_obs][8]: min xyz, -, max xyz, -
+    const uint32_t* occ;          // device occupancy masks [n_scenes][2][kOccGrid^3] (exact | dilated)
     Workspace* ws;                // [n_teams]
     const QueryIn* queries;       // [n_queries]
     kpx_query_result* results;    // [n_queries] (may be null)
@@ -1247,7 +1253,13 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
 template <class M, class R>
 __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, const Team& T, const QueryIn& Q,
                                       kpx_query_result* res_out, long long query_index, RunState& RS, int* s_prefix,
-                                      int* s_w, double* s_d, int* s_bin) {
+                                      int* s_w, double* s_d, int* s_bin, int* s_scene) {
+    if (*s_scene != Q.scene) {      // stage this query's obstacle set (boxes + occupancy tables); CTA-uniform
+        __syncthreads();
+        Scene<R>::stage(A.P, A.obs + (size_t)Q.scene * 8 * (size_t)A.P.n_obs, A.occ + (size_t)Q.scene * 2 * kOccCells);
+        if (threadIdx.x == 0) *s_scene = Q.scene;
+        __syncthreads();
+    }
     if (!A.resume) reset_query<M, R>(A, W, T, Q);
     {   // run state out of Ctl (valid between launches: stepped runs, resume)
         Ctl* const ctl = W.ctl;
@@ -1303,7 +1315,9 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R, V>::value) plan_kernel
     __shared__ double s_d[kBlock / 32];
     __shared__ int s_q;
     __shared__ int s_bin[4 * kBins];      // S0: local histogram | CTA base | local fill | global bin start
-    Scene<R>::stage(A.P, A.obs, A.occ);
+    __shared__ int s_scene;               // obstacle set staged in shared memory (queries name theirs: QueryIn::scene)
+    if (threadIdx.x == 0) s_scene = -1;
+    __syncthreads();
 
     Team T;
     T.ctas = A.team_ctas;
@@ -1318,7 +1332,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R, V>::value) plan_kernel
     T.bar = W.bar;
 
     if (A.queue == nullptr) {       // single query bound to team 0 (plan handle: stepped / resumable)
-        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_rs, s_prefix, s_w, s_d, s_bin);
+        run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_rs, s_prefix, s_w, s_d, s_bin, &s_scene);
         return;
     }
     for (;;) {                      // batch: teams pull queries until the queue is drained
@@ -1335,7 +1349,7 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R, V>::value) plan_kernel
         const int q = s_q;
         __syncthreads();
         if (q >= A.n_queries) return;
-        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_rs, s_prefix, s_w, s_d, s_bin);
+        run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_rs, s_prefix, s_w, s_d, s_bin, &s_scene);
         team_sync(T);
     }
 }

@@ -17,7 +17,7 @@ namespace kpx {
 
 struct ValidateArgs {
     Params<double> P;
-    const double* boxes;            // device [n_obs][8] float64: min xyz, -, max xyz, -
+    const double* boxes;            // device [n_scenes][n_obs][8] float64: min xyz, -, max xyz, -  (scene of a query: QueryIn::scene)
     const QueryIn* queries;
     kpx_query_result* results;
     const double* chain_control;    // [n_queries][max_chain][nu]
@@ -52,10 +52,11 @@ __global__ void __launch_bounds__(128) validate_kernel(const __grid_constant__ V
     const long long L = r->chain_len;
     if (L < 0 || L > A.max_chain) { r->checked = -1; r->check_code = 5; return; }     // chain did not fit the buffer
     const QueryIn& Q = A.queries[q];
+    const double* const boxes = A.boxes + (size_t)Q.scene * 8 * (size_t)A.P.n_obs;
     double cur[N], prev[N], st[N], comp[1] = {0.0};
 #pragma unroll
     for (int d = 0; d < N; ++d) cur[d] = Q.start[d];
-    bool ok = state_ok_f64<N>(A.P, A.boxes, cur);
+    bool ok = state_ok_f64<N>(A.P, boxes, cur);
     for (long long s = 0; s < L && ok; ++s) {
         double u[NU];
 #pragma unroll
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(128) validate_kernel(const __grid_constant__ V
         for (int i = 0; i < S && ok; ++i) {
 #pragma unroll
             for (int d = 0; d < N; ++d) prev[d] = cur[d];
-            Stepper<M, double>::step(cur, comp, u, h, h6);
-            if (!state_ok_f64<N>(A.P, A.boxes, cur)) { ok = false; break; }
+            Stepper<typename M::Base, double>::step(cur, comp, u, h, h6);
+            if (!state_ok_f64<N>(A.P, boxes, cur)) { ok = false; break; }
             const double d0 = cur[0] - prev[0], d1 = cur[1] - prev[1], d2 = cur[2] - prev[2];
             const double dist = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
             long long m = 1;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(128) validate_kernel(const __grid_constant__ V
                 const double t = (double)j / (double)m;
 #pragma unroll
                 for (int d = 0; d < N; ++d) st[d] = prev[d] + t * (cur[d] - prev[d]);
-                if (!state_ok_f64<N>(A.P, A.boxes, st)) ok = false;
+                if (!state_ok_f64<N>(A.P, boxes, st)) ok = false;
             }
         }
     }

@@ -323,3 +323,59 @@ def test_batch_refuses_invalid_starts_and_takes_any_seed(kp):
                 eng.reset(seed=sd)
                 one = eng.solve()
                 assert one.stats.iterations == res.records["iterations"][i] and one.stats.tree_size == res.records["tree_size"][i]
+
+
+def test_per_query_scenes_match_single_scene_plans(kp, orc):
+    """Queries of one batch in different obstacle sets (kpx_batch_set_scenes / scene index per query): every query
+    plans exactly as it does alone in its own Environment -- float64 against the CPU oracle of that environment,
+    float32 against a single-scene batch -- and is re-validated against ITS obstacles on the device and the host."""
+    import dataclasses
+    model = kp.get_model("di6")
+    base = kp.gen_environment("forest", model, seed=0)                                  # 14 pillars
+    envs = [base, kp.gen_environment("forest", model, seed=1), kp.gen_environment("forest", model, seed=5),
+            dataclasses.replace(kp.gen_environment("narrow", model, seed=0), start=base.start, goal=base.goal),   # 2 boxes, padded
+            kp.Environment("open", base.workspace_lo, base.workspace_hi, np.zeros((0, 3)), np.zeros((0, 3)), base.start, base.goal)]
+    cfg = small_cfg(kp, model, t_e=8000, seed=0)
+    q = 30
+    seeds, scenes = np.arange(q), np.arange(q) % len(envs)
+    for backend in ("cuda", "cuda-f32"):
+        with kp.BatchPlanner(cfg, base, model, backend=backend, n_teams=10, team_ctas=1) as bp:
+            bp.set_scenes(envs)
+            res = bp.run(seeds, scenes=scenes)
+            again = bp.run(seeds, scenes=scenes)
+            for k in ("status", "iterations", "tree_size", "solution_slot", "chain_len", "checked"):
+                assert np.array_equal(res.records[k], again.records[k]), k
+            assert res.validated.sum() == res.solved.sum() >= q // 2
+            for i in np.flatnonzero(res.solved)[:10]:
+                segs, ok = bp.trajectory(res, int(i))
+                env_i = dataclasses.replace(envs[scenes[i]], start=base.start, goal=base.goal)
+                assert ok and kp.ValidityChecker(env_i, model, 0.05).trajectory_valid(segs, start=base.start)
+            with pytest.raises(kp.ConfigError):
+                bp.run(seeds, scenes=np.full(q, 7))
+        for sc, env in enumerate(envs):                       # the same queries, each scene on its own
+            env_s = dataclasses.replace(env, start=base.start, goal=base.goal)
+            mine = np.flatnonzero(scenes == sc)
+            if backend == "cuda":
+                for i in mine[:3]:
+                    op = orc.plan_from_problem(kp.build_problem(cfg.with_seed(int(seeds[i])), env_s, model))
+                    op.solve(t_max=60.0)
+                    assert op.raw.size == res.records["tree_size"][i] and op.raw.iteration == res.records["iterations"][i], (sc, i)
+                    assert {"solved": 0, "capacity_exhausted": 2}[op.status] == res.records["status"][i]
+            else:
+                if env_s.n_obstacles == 0:
+                    continue
+                with kp.BatchPlanner(cfg, env_s, model, backend=backend, n_teams=6, team_ctas=1) as one:
+                    alone = one.run(seeds[mine])
+                for k in ("status", "iterations", "tree_size", "solution_slot", "chain_len"):
+                    assert np.array_equal(alone.records[k], res.records[k][mine]), (sc, k)
+    # a scene may not have more obstacles than the planner was created for, nor another workspace
+    with kp.BatchPlanner(cfg, envs[3], model, backend="cuda", n_teams=2, team_ctas=1) as small:
+        with pytest.raises(kp.ConfigError):
+            small.set_scenes([envs[3], base])
+    inside = base.start.copy()
+    with kp.BatchPlanner(cfg, base, model, backend="cuda", n_teams=2, team_ctas=1) as bp:
+        blocked = kp.Environment("blocked", base.workspace_lo, base.workspace_hi, np.array([[0.5, 0.5, 0.5]]), np.array([[1.5, 1.5, 1.5]]),
+                                 base.start, base.goal)
+        bp.set_scenes([base, blocked])
+        with pytest.raises(kp.ConfigError):
+            bp.run([0, 1], scenes=[0, 1])                      # the start lies inside scene 1's obstacle
