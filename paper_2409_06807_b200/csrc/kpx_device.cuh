@@ -1093,9 +1093,10 @@ __device__ __forceinline__ int substeps_of(const Params<R>& P, uint64_t h0, int 
 //     by a few float32 ulps of the workspace) stay inside the state box and overlap no obstacle box, nothing the
 //     reference's checker would test can fail.  Obstacles are found through the occupancy grid of the scene (the
 //     dilated table answers a box spanning <= 2 cells per axis in one lookup) and compared box against box, exactly.
-// Either way the extension is finished on the spot -- end state from the closed form, grid mapping, counters -- and
-// never enters the length sort or the substep loop; ~80 % of the Trees workload.  Everything else (extensions that
-// pass near an obstacle, or whose parabola only grazes a box face between samples) takes the full path.
+// Either way the extension is finished on the spot -- end state from the closed form, grid mapping, counters -- with
+// no substep loop at all; ~90 % of the Trees workload.  Everything else (extensions that pass near an obstacle, or
+// whose parabola only grazes a box face between samples) is evaluated one item per warp, lane = substep
+// (di_item_by_substeps below).
 // Work counters of a finished extension: substeps = S (the reference integrates every substep whatever the verdict).
 // Certified valid: boxsteps = S and points = the sum of the densification counts of its S segments (validity.py:26-31),
 // counted from the closed-form segment lengths |h v0 + h^2 u (s - 1/2)|.  Certified invalid: boxsteps = 1, points = 0
@@ -1243,15 +1244,101 @@ __device__ __forceinline__ int di_certify(const Params<float>& P, const float* x
     else { out.boxsteps = 1; out.points = 0; }
     return verdict;
 }
+// An extension the certificate could not settle, evaluated by the WHOLE WARP: lane = RK4 substep.  Sample s of the
+// closed form does not depend on sample s - 1, so the S box tests and segment walks of the extension run side by side,
+// 32 per round; the first failing substep (lowest lane of the first round that has one) decides, exactly as the
+// reference's sequential early-out would: boxsteps = its index, points = the densification counts of the segments
+// before it plus the points walked in it up to and including the hit.  All lanes call it with the same arguments and
+// receive the same result.
+template <int B>
+__device__ __forceinline__ void di_item_by_substeps(const Params<float>& P, const float* x0, const float* u, float dt, int S,
+                                                    bool* ok_out, int* boxsteps_out, int* points_out) {
+    const int lane = threadIdx.x & 31;
+    const float h = dt / (float)S;
+    const int n_obs = P.n_obs;
+    const bool grid = P.occ_g != 0;
+    int points = 0;
+#pragma unroll 1
+    for (int base = 0; base < S; base += 32) {
+        const int s = base + lane + 1;                          // sample index, 1..S
+        const bool act = s <= S;
+        const float t1 = s == S ? dt : (float)s * h, t0 = (float)(s - 1) * h;
+        bool fail = false;
+        int steps = 0, hit = 0;
+        if (act) {
+            bool inb = true;                                    // sample s of every block inside the closed state box
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const float p = di_pos(x0[6 * b + a], x0[6 * b + 3 + a], u[3 * b + a], t1);
+                    const float v = __fmaf_rn(t1, u[3 * b + a], x0[6 * b + 3 + a]);
+                    inb = inb & (p >= P.state_lo[6 * b + a]) & (p <= P.state_hi[6 * b + a]) &
+                          (v >= P.state_lo[6 * b + 3 + a]) & (v <= P.state_hi[6 * b + 3 + a]);
+                }
+            fail = !inb;
+            if (inb && n_obs > 0) {                             // segment (s - 1) -> s of block 1 against the obstacles
+                const float q0 = di_pos(x0[0], x0[3], u[0], t0), q1 = di_pos(x0[1], x0[4], u[1], t0), q2 = di_pos(x0[2], x0[5], u[2], t0);
+                const float c0 = di_pos(x0[0], x0[3], u[0], t1), c1 = di_pos(x0[1], x0[4], u[1], t1), c2 = di_pos(x0[2], x0[5], u[2], t1);
+                const float dx = c0 - q0, dy = c1 - q1, dz = c2 - q2;
+                const float d2 = dx * dx + dy * dy + dz * dz;
+                steps = 1;
+                if (d2 > P.d2_thr[0]) steps = 2;
+                if (d2 > P.d2_thr[1]) steps = 4;
+                if (d2 > P.d2_thr[2]) steps = 8;
+                if (__builtin_expect(d2 > P.d2_thr[3], 0)) {
+                    const float dist = sqrtf(d2);
+                    float thr = P.check_res;
+                    steps = 1;
+                    while (thr < dist) { thr += thr; steps <<= 1; }
+                }
+                // obstacles the segment's box can touch (same cull as the sequential path), then the walk itself
+                const float lo[3] = {fminf(q0, c0), fminf(q1, c1), fminf(q2, c2)}, hi[3] = {fmaxf(q0, c0), fmaxf(q1, c1), fmaxf(q2, c2)};
+                if (!grid || box_touches_obstacle(P, lo, hi)) {
+                    const float inv = 1.0f / (float)steps;
+#pragma unroll 1
+                    for (int j = 1; j < steps && hit == 0; ++j) {
+                        const float t = (float)j * inv;
+                        if (point_hits<float>(P, q0 + t * dx, q1 + t * dy, q2 + t * dz)) hit = j;
+                    }
+                    if (hit == 0 && point_hits<float>(P, c0, c1, c2)) hit = steps;
+                    fail = hit != 0;
+                }
+            }
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, act && fail);
+        const int first = fm ? __ffs(fm) - 1 : 32;
+        points += __reduce_add_sync(0xffffffffu, act ? (lane < first ? steps : (lane == first ? hit : 0)) : 0);
+        if (fm) { *ok_out = false; *boxsteps_out = base + first + 1; *points_out = points; return; }
+    }
+    *ok_out = true; *boxsteps_out = S; *points_out = points;
+}
+template <int B>
+__device__ __forceinline__ void di_end_state(const float* x0, const float* u, float dt, float* end) {
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            end[6 * b + a] = di_pos(x0[6 * b + a], x0[6 * b + 3 + a], u[3 * b + a], dt);
+            end[6 * b + 3 + a] = __fmaf_rn(dt, u[3 * b + a], x0[6 * b + 3 + a]);
+        }
+}
+
 template <> struct FreeFlight<ModelDI6, float> {
     static constexpr bool kEnabled = KPX_FREE_FLIGHT != 0;
     __device__ static __forceinline__ int certify(const Params<float>& P, const float* x0, const float* u, float dt, int S,
                                                   ItemOut<float, 6>& out) { return di_certify<1>(P, x0, u, dt, S, out); }
+    __device__ static __forceinline__ void by_substeps(const Params<float>& P, const float* x0, const float* u, float dt, int S,
+                                                       bool* ok, int* boxsteps, int* points) { di_item_by_substeps<1>(P, x0, u, dt, S, ok, boxsteps, points); }
+    __device__ static __forceinline__ void end_state(const float* x0, const float* u, float dt, float* end) { di_end_state<1>(x0, u, dt, end); }
 };
 template <int B> struct FreeFlight<ModelStackedDI<B>, float> {
     static constexpr bool kEnabled = KPX_FREE_FLIGHT != 0;
     __device__ static __forceinline__ int certify(const Params<float>& P, const float* x0, const float* u, float dt, int S,
                                                   ItemOut<float, 6 * B>& out) { return di_certify<B>(P, x0, u, dt, S, out); }
+    __device__ static __forceinline__ void by_substeps(const Params<float>& P, const float* x0, const float* u, float dt, int S,
+                                                       bool* ok, int* boxsteps, int* points) { di_item_by_substeps<B>(P, x0, u, dt, S, ok, boxsteps, points); }
+    __device__ static __forceinline__ void end_state(const float* x0, const float* u, float dt, float* end) { di_end_state<B>(x0, u, dt, end); }
 };
 
 }  // namespace kpx

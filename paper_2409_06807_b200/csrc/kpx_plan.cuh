@@ -91,9 +91,8 @@ struct Ctl {                      // one per workspace, global memory
     int n_trace;
     int chain_len;
     int cur_query;                // batch mode: query index broadcast to the team
-    unsigned int unit_next;       // S1: next 32-item unit of the length-sorted order
-    unsigned int n_free;          // S0 (many-CTA teams): items finished in the prepass; they fill positions from the end
-    unsigned int n_packed;        // ... and the items left for S1, compacted from the start
+    unsigned int unit_next;       // S1: next 32-item unit of the length-sorted order / of the undecided-item list
+    unsigned int n_todo;          // S1 (float32 double integrators): undecided items in the list (Workspace::order)
     int last_sorted;              // 1 if the last iteration's it_* arrays are in sorted-position order
     // claim-table epoch (see Workspace::claim): the epoch the last query used; epoch_valid = 0 forces a dense
     // reset of the claim table and the region arrays (fresh state loaded from the host)
@@ -124,11 +123,13 @@ struct RunState {                 // CTA-uniform state of the running query, sha
     unsigned long long t_start;   // keeper only
     // header of the current iteration
     int lam, items, n_sch_old, par, sorted;
-    int items_sorted;             // many-CTA teams: items the global sort holds (the rest were finished in its prepass)
     int n_est;                    // available regions, i.e. entries of Workspace::est_ids, for this iteration's estimate pass
     uint32_t claim_tag;           // epoch of this query << claim_shift
     unsigned long long h0;
     unsigned long long tp[7];     // keeper only: phase boundary timestamps
+    // S1 work of this CTA in the current iteration (substeps, points, boxsteps, valid items, closed-form items): summed
+    // here and flushed to Ctl once per CTA -- thousands of units adding to the same global words serialise in L2
+    unsigned long long work[5];
 };
 
 struct Workspace {                // device pointers of one team's state
@@ -442,9 +443,6 @@ __device__ __forceinline__ int build_est_list(const Workspace& W, const Team& T,
 #ifndef KPX_TILE_CHUNKS
 #define KPX_TILE_CHUNKS 4
 #endif
-#ifndef KPX_TILE_CHUNKS_FREE
-#define KPX_TILE_CHUNKS_FREE 16       // models with the free-flight prepass: most items never reach the sort, so tiles are larger
-#endif
 
 // i-th EXPAND slot: chunk by binary search over the chunk prefix, then the chunk-local compacted list
 __device__ __forceinline__ int expand_slot(const Workspace& W, const int* s_prefix, int n_sch_old, int i) {
@@ -457,7 +455,7 @@ __device__ __forceinline__ int expand_slot(const Workspace& W, const int* s_pref
 // the item word + end state at its position, the first-visit claim, the region counters, the work counters.
 template <class M, class R>
 __device__ __forceinline__ void commit_item(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, uint32_t claim_tag,
-                                            int par, bool active, int w, int pos, const ItemOut<R, M::N>& o) {
+                                            unsigned long long* work, bool active, int w, int pos, const ItemOut<R, M::N>& o) {
     constexpr int N = M::N;
     const Params<R>& P = A.P;
     int region = -1; bool valid = false;
@@ -475,16 +473,16 @@ __device__ __forceinline__ void commit_item(const PlanArgs<R>& A, const Workspac
         __stcg(W.it_code + pos, code);
     }
     count_outcome(W.n_valid, W.n_invalid, region, valid, active, W.touched_bits);
-    // work counters: one reduction and one fire-and-forget atomic per unit
+    // work counters: one reduction and one shared-memory atomic per unit (RunState::work)
     const int t_sub = __reduce_add_sync(0xffffffffu, active ? o.substeps : 0);
     const int t_pts = __reduce_add_sync(0xffffffffu, active ? o.points : 0);
     const int t_box = __reduce_add_sync(0xffffffffu, active ? o.boxsteps : 0);
     const int t_val = __popc(__ballot_sync(0xffffffffu, valid));
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&W.ctl->sum_substeps, (unsigned long long)t_sub);
-        atomicAdd(&W.ctl->sum_points, (unsigned long long)t_pts);
-        atomicAdd(&W.ctl->sum_boxsteps, (unsigned long long)t_box);
-        if (t_val) atomicAdd(&W.ctl->cnt_valid[par], t_val);
+        atomicAdd(work + 0, (unsigned long long)t_sub);
+        atomicAdd(work + 1, (unsigned long long)t_pts);
+        atomicAdd(work + 2, (unsigned long long)t_box);
+        if (t_val) atomicAdd(work + 3, (unsigned long long)t_val);
     }
 }
 
@@ -493,7 +491,7 @@ __device__ __forceinline__ void commit_item(const PlanArgs<R>& A, const Workspac
 // through pos_of); unsorted: position == item number.
 template <class M, class R>
 __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q,
-                                               const RunState& RS, const int* s_prefix, int pos, int limit, bool sorted) {
+                                               RunState& RS, const int* s_prefix, int pos, int limit, bool sorted) {
     constexpr int N = M::N, NU = M::NU;
     const Params<R>& P = A.P;
     // the iteration header is re-read from shared memory per unit: nothing of it stays in registers
@@ -522,31 +520,97 @@ __device__ __forceinline__ void propagate_unit(const PlanArgs<R>& A, const Works
     }
     ItemOut<R, N> o;
     integrate_and_map<M, R>(P, active, x0, u, dt, S, o);     // warp-synchronous
-    commit_item<M, R>(A, W, Q, RS.claim_tag, RS.par, active, w, pos, o);
+    commit_item<M, R>(A, W, Q, RS.claim_tag, RS.work, active, w, pos, o);
 }
 
-// Prepass of one item, ahead of the length sort: parent slot, substep count and -- float32 double integrators --
-// the free-flight certificate (FreeFlight, kpx_device.cuh): a certified extension is finished here, from the closed
-// form, and never enters the sort.  Returns the substep count; *free_out says the item is done, with `o` filled.
-template <class M, class R>
-__device__ __forceinline__ int prepass_item(const PlanArgs<R>& A, const Workspace& W, uint64_t h0, int slot, int ext,
-                                            bool* free_out, ItemOut<R, M::N>& o) {
-    *free_out = false;
-    if constexpr (FreeFlight<typename M::Base, R>::kEnabled) {
-        constexpr int N = M::N, NU = M::NU;
-        R u[NU], dt, x0[N];
+// The same for the float32 double integrators (FreeFlight, kpx_device.cuh), in two passes over the iteration.
+// Pass 1 (flight_settle_unit): every lane tries to settle its item from the closed form -- certified valid or invalid,
+// ~90 % of the Trees workload -- and commits it; an undecided item (it passes near an obstacle) is appended to a list.
+// Pass 2 (flight_eval_unit): warps pull 32 list entries at a time, each lane re-derives ITS item's sample, and the
+// warp then evaluates them ONE ITEM AT A TIME, lane = RK4 substep (di_item_by_substeps): the closed form makes the
+// sampled states independent of each other, so the S segment tests of an extension run side by side and an extension
+// costs one or two warp rounds whatever its length.  The list decouples the second pass from where the hard items
+// cluster (the lambda children of a node next to an obstacle are all undecided): every warp gets the same load.
+// Position == item number throughout: nothing is sorted.
+template <class M>
+__device__ __forceinline__ void flight_settle_unit(const PlanArgs<float>& A, const Workspace& W, const QueryIn& Q,
+                                                   RunState& RS, const int* s_prefix, int pos, int limit) {
+    constexpr int N = M::N, NU = M::NU;
+    using F = FreeFlight<typename M::Base, float>;
+    const Params<float>& P = A.P;
+    const int lam = RS.lam, lane = threadIdx.x & 31;
+    const bool active = pos < limit;
+    const int w = pos;
+    int slot = 0, verdict = kFlightInvalid;
+    ItemOut<float, N> o;
+    if (active) {
+        float u[NU], dt, x0[N];
         int S;
-        sample_control<M, R>(A.P, h0, slot, ext, u, &dt, &S, nullptr, nullptr);
-        load_row<N>((const R*)W.states, slot, x0);
-        const int verdict = FreeFlight<typename M::Base, R>::certify(A.P, x0, u, dt, S, o);
-        if (verdict != kFlightFull) {
-            map_end_state<M, R>(A.P, o.end, true, verdict == kFlightValid, o);
-            *free_out = true;
-        }
-        return S;
-    } else {
-        return substeps_of<M, R>(A.P, h0, slot, ext);
+        slot = expand_slot(W, s_prefix, RS.n_sch_old, w / lam);
+        __stcg(W.it_parent + w, slot);
+        sample_control<M, float>(P, RS.h0, slot, w % lam, u, &dt, &S, nullptr, nullptr);
+        load_row<N>((const float*)W.states, slot, x0);
+        verdict = F::certify(P, x0, u, dt, S, o);
+        if (verdict != kFlightFull) map_end_state<M, float>(P, o.end, true, verdict == kFlightValid, o);
     }
+    const bool settled = active && verdict != kFlightFull;
+    const unsigned sm = __ballot_sync(0xffffffffu, settled), tm = __ballot_sync(0xffffffffu, active && !settled);
+    if (tm) {                                       // undecided items: (item, parent slot) into the list, one atomic per warp
+        int base = 0;
+        if (lane == 0) base = (int)atomicAdd(&W.ctl->n_todo, (unsigned)__popc(tm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (active && !settled) __stcg(W.order + base + __popc(tm & ((1u << lane) - 1u)), make_int2(w, slot));
+    }
+    if (sm) {
+        commit_item<M, float>(A, W, Q, RS.claim_tag, RS.work, settled, w, pos, o);
+        if (lane == 0) atomicAdd(RS.work + 4, (unsigned long long)__popc(sm));
+    }
+}
+
+template <class M>
+__device__ __forceinline__ void flight_eval_unit(const PlanArgs<float>& A, const Workspace& W, const QueryIn& Q,
+                                                 RunState& RS, int idx, int n_todo) {
+    constexpr int N = M::N, NU = M::NU;
+    using F = FreeFlight<typename M::Base, float>;
+    const Params<float>& P = A.P;
+    const int lam = RS.lam, lane = threadIdx.x & 31;
+    const bool active = idx < n_todo;
+    int w = 0, S = 0;
+    float u[NU], dt = 0.0f, x0[N];
+    if (active) {
+        const int2 ws = __ldcg(W.order + idx);
+        w = ws.x;
+        sample_control<M, float>(P, RS.h0, ws.y, w % lam, u, &dt, &S, nullptr, nullptr);
+        load_row<N>((const float*)W.states, ws.y, x0);
+    } else {
+#pragma unroll
+        for (int d = 0; d < N; ++d) x0[d] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) u[j] = 0.0f;
+    }
+    ItemOut<float, N> o;
+    bool valid = false;
+    unsigned todo = __ballot_sync(0xffffffffu, active);
+#pragma unroll 1
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        float bx[N], bu[NU];
+#pragma unroll
+        for (int d = 0; d < N; ++d) bx[d] = __shfl_sync(0xffffffffu, x0[d], src);
+#pragma unroll
+        for (int j = 0; j < NU; ++j) bu[j] = __shfl_sync(0xffffffffu, u[j], src);
+        const float bdt = __shfl_sync(0xffffffffu, dt, src);
+        const int bS = __shfl_sync(0xffffffffu, S, src);
+        bool ok; int boxsteps, points;
+        F::by_substeps(P, bx, bu, bdt, bS, &ok, &boxsteps, &points);
+        if (lane == src) { valid = ok; o.substeps = S; o.boxsteps = boxsteps; o.points = points; }
+    }
+    if (active) {
+        F::end_state(x0, u, dt, o.end);
+        map_end_state<M, float>(P, o.end, true, valid, o);
+    }
+    commit_item<M, float>(A, W, Q, RS.claim_tag, RS.work, active, w, w, o);     // results live at the item's own number
 }
 
 // S1 of one iteration: propagate every (EXPAND slot x extension) item, count outcomes per region, claim fresh
@@ -560,13 +624,13 @@ __device__ __forceinline__ int prepass_item(const PlanArgs<R>& A, const Workspac
 //     the parent-state gather stays in a handful of sectors instead of 32 per row, and S0 needs neither global
 //     atomics nor team barriers.
 template <class M, class R>
-__device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, const RunState& RS,
+__device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, RunState& RS,
                                          int team_rank, int team_ctas, const int* s_prefix, int* s_bin) {
     const int lane = threadIdx.x & 31, tid = threadIdx.x;
     const bool sorted = RS.sorted != 0;
     const bool tiled = sorted && team_ctas == 1;
     uint8_t* const s_len = (uint8_t*)(kpx_dyn_smem + Scene<R>::kCoop);   // [kTileM]; the staging area is idle while sorting
-    constexpr int kTileM = (FreeFlight<typename M::Base, R>::kEnabled ? KPX_TILE_CHUNKS_FREE : KPX_TILE_CHUNKS) * kChunk;   // items per tile
+    constexpr int kTileM = KPX_TILE_CHUNKS * kChunk;        // items per tile
     static_assert(sizeof(WarpCoop<R>) * kWarps >= kTileM, "tile lengths must fit the staging area");
     int tile = -kTileM, n_units = 0, tile_limit = 0;
     int unit = sorted ? 0x3fffffff : (team_rank * kBlock + tid) >> 5;    // unsorted: this warp's slice of the one round
@@ -586,39 +650,18 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
                 const int n_t = items - tile < kTileM ? items - tile : kTileM;
                 __syncthreads();                        // the previous tile's walks are done with the staging area
                 for (int b = tid; b < 2 * kBins; b += kBlock) s_bin[b] = 0;          // histogram | fill
-                if (tid < 2) s_bin[3 * kBins + tid] = 0;                             // unit cursor of the tile | free items
+                if (tid == 0) s_bin[3 * kBins] = 0;                                  // unit cursor of the tile
                 __syncthreads();
-                // prepass (whole warps: finishing a free item is warp-synchronous): free items are done here and
-                // take the positions at the END of the tile; the others are binned by length
 #pragma unroll 1
-                for (int j0 = 0; j0 < n_t; j0 += kBlock) {
-                    const int j = j0 + tid, w = tile + j;
-                    const bool act = j < n_t;
-                    bool free = false;
-                    int fpos = 0;
-                    ItemOut<R, M::N> o;
-                    if (act) {
-                        const int i = w / lam;
-                        const int slot = expand_slot(W, s_prefix, n_sch_old, i);
-                        __stcg(W.it_parent + w, slot);
-                        int S = prepass_item<M, R>(A, W, h0, slot, w - i * lam, &free, o);
-                        if (free) {
-                            fpos = tile + n_t - 1 - atomicAdd(&s_bin[3 * kBins + 1], 1);
-                            __stcg(W.pos_of + w, fpos);
-                            s_len[j] = 0;                                            // never a substep count (>= 4)
-                        } else {
-                            S = S < kBins - 1 ? S : kBins - 1;
-                            s_len[j] = (uint8_t)S;
-                            atomicAdd(&s_bin[S], 1);
-                        }
-                    }
-                    if constexpr (FreeFlight<typename M::Base, R>::kEnabled) {
-                        const unsigned fm = __ballot_sync(0xffffffffu, free);
-                        if (fm) {
-                            commit_item<M, R>(A, W, Q, RS.claim_tag, RS.par, free, w, fpos, o);
-                            if (lane == 0) atomicAdd(&W.ctl->sum_free, (unsigned long long)__popc(fm));
-                        }
-                    }
+                for (int j = tid; j < n_t; j += kBlock) {
+                    const int w = tile + j;
+                    const int i = w / lam;
+                    const int slot = expand_slot(W, s_prefix, n_sch_old, i);
+                    int S = substeps_of<M, R>(A.P, h0, slot, w - i * lam);
+                    S = S < kBins - 1 ? S : kBins - 1;
+                    __stcg(W.it_parent + w, slot);
+                    s_len[j] = (uint8_t)S;
+                    atomicAdd(&s_bin[S], 1);
                 }
                 __syncthreads();
                 if (tid < 32) {                         // start of every bin, longest first (2 bins per lane)
@@ -632,14 +675,13 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
 #pragma unroll 1
                 for (int j = tid; j < n_t; j += kBlock) {
                     const int b = s_len[j];
-                    if (b == 0) continue;               // finished in the prepass
                     const int p = tile + s_bin[2 * kBins + b] + atomicAdd(&s_bin[kBins + b], 1);
                     __stcg(W.order + p, make_int2(tile + j, __ldcg(W.it_parent + tile + j)));
                     __stcg(W.pos_of + tile + j, p);     // results of item w are stored at its sorted position
                 }
                 __syncthreads();
-                tile_limit = tile + n_t - s_bin[3 * kBins + 1];
-                n_units = (tile_limit - tile + 31) >> 5;
+                tile_limit = tile + n_t;
+                n_units = (n_t + 31) >> 5;
             }
             // warps pull the tile's units from a shared-memory cursor, longest first
             if (lane == 0) unit = atomicAdd(&s_bin[3 * kBins], 1);
@@ -650,16 +692,45 @@ __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& 
         } else if (sorted) {
             if (lane == 0) unit = (int)atomicAdd(&W.ctl->unit_next, 1u);
             unit = __shfl_sync(0xffffffffu, unit, 0);
-            limit = RS.items_sorted;                    // the items that were not finished in the prepass (S0)
+            limit = RS.items;
             if ((long long)unit * 32 >= limit) break;
             pos = unit * 32 + lane;
         } else {
             limit = RS.items;
             if ((long long)unit * 32 >= limit) break;
             pos = unit * 32 + lane;
-            unit = 0x3fffffff;                          // one round only
+            unit += team_ctas * kWarps;                 // one round, unless nothing is sorted for this model
         }
-        propagate_unit<M, R>(A, W, Q, RS, s_prefix, pos, limit, sorted);
+        if constexpr (FreeFlight<typename M::Base, R>::kEnabled) flight_settle_unit<M>(A, W, Q, RS, s_prefix, pos, limit);
+        else propagate_unit<M, R>(A, W, Q, RS, s_prefix, pos, limit, sorted);
+    }
+    if constexpr (FreeFlight<typename M::Base, R>::kEnabled) {
+        // second pass: the undecided items, 32 list entries per pull
+        Team T;
+        T.ctas = team_ctas; T.rank = team_rank; T.bar = W.bar;
+        team_sync(T);                                   // the list is complete
+        const int n_todo = (int)__ldcg(&W.ctl->n_todo);
+        // entries per pull: a warp's worth when the team is small against the list (many queries per GPU), fewer when
+        // one query has the whole GPU -- a warp evaluates its entries one after the other, and the longest warp is S1
+        const int team_warps = team_ctas * kWarps;
+        int chunk = (n_todo + team_warps - 1) / team_warps;
+        chunk = chunk < 1 ? 1 : (chunk > 32 ? 32 : chunk);
+#pragma unroll 1
+        for (;;) {
+            int unit2 = 0;
+            if (lane == 0) unit2 = (int)atomicAdd(&W.ctl->unit_next, 1u);
+            unit2 = __shfl_sync(0xffffffffu, unit2, 0);
+            if ((long long)unit2 * chunk >= n_todo) break;
+            const int hi = unit2 * chunk + chunk < n_todo ? unit2 * chunk + chunk : n_todo;
+            flight_eval_unit<M>(A, W, Q, RS, unit2 * chunk + lane, lane < chunk ? hi : 0);
+        }
+    }
+    // this CTA's work counters of the iteration: one global atomic each
+    __syncthreads();
+    if (tid < 5 && RS.work[tid]) {
+        Ctl* const c = W.ctl;
+        if (tid == 3) atomicAdd(&c->cnt_valid[RS.par], (int)RS.work[3]);
+        else atomicAdd(tid == 0 ? &c->sum_substeps : (tid == 1 ? &c->sum_points : (tid == 2 ? &c->sum_boxsteps : &c->sum_free)), RS.work[tid]);
     }
 }
 
@@ -752,7 +823,7 @@ __device__ __forceinline__ void reset_query(const PlanArgs<R>& A, const Workspac
             ctl->n_items_last = 0; ctl->n_keep_last = 0;
             ctl->cnt_valid[0] = ctl->cnt_valid[1] = ctl->cnt_open[0] = ctl->cnt_open[1] = 0;
             ctl->sum_items = ctl->sum_substeps = ctl->sum_points = ctl->sum_boxsteps = ctl->sum_free = 0ull;
-            ctl->n_trace = 0; ctl->chain_len = 0; ctl->unit_next = 0u; ctl->n_free = 0u; ctl->n_packed = 0u;
+            ctl->n_trace = 0; ctl->chain_len = 0; ctl->unit_next = 0u; ctl->n_todo = 0u;
             for (int b = 0; b < kBins; ++b) W.bin_cursor[b] = 0u;
         }
         team_sync(T);
@@ -798,10 +869,13 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
     const int items = (int)items_ll;
     const int n_sch_old = (size + kChunk - 1) / kChunk;
     const uint64_t h0 = iter_key(M::kRng, Q.seed, (uint64_t)it);
-    const bool sorted = items > tthreads;
+    // float32 double integrators finish ~90 % of their items from the closed form and evaluate the rest one warp per
+    // item (propagate_unit_flight): no item is longer than another, so there is nothing to sort
+    const bool sorted = items > tthreads && !FreeFlight<typename M::Base, R>::kEnabled;
     if (tid == 0) {
         RS.it = it; RS.iters = iters + 1; RS.lam = lam; RS.items = items; RS.n_sch_old = n_sch_old; RS.par = it & 1;
         RS.sorted = sorted ? 1 : 0; RS.h0 = h0;
+        for (int k = 0; k < 5; ++k) RS.work[k] = 0ull;
     }
     if (keeper) RS.tp[0] = gtimer();
 
@@ -812,49 +886,6 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
         // Results stay indexed by the item number w, so nothing downstream sees the processing order.
         // An iteration that fits in one round (items <= team threads) gains nothing from it and skips S0.
         const bool global_sort = sorted && T.ctas > 1;    // one-CTA teams sort tile by tile inside S1
-        if constexpr (FreeFlight<typename M::Base, R>::kEnabled) {
-            // Models with the free-flight certificate: ONE pass.  Most items are finished right here from the closed
-            // form (positions from the end of the iteration's range); what is left is a fraction of a round of the
-            // team's threads, so it is only compacted (positions from the start, in arrival order), not sorted --
-            // one team barrier instead of two, and S1's critical path is its longest item either way.
-            if (global_sort) {
-                const uint32_t claim_tag = RS.claim_tag;
-#pragma unroll 1
-                for (long long w0 = (long long)T.rank * kBlock; w0 < items; w0 += tthreads) {
-                    const int w = (int)w0 + tid, lane = tid & 31;
-                    const bool act = w < items;
-                    bool free = false;
-                    int slot = 0;
-                    ItemOut<R, M::N> o;
-                    if (act) {
-                        const int i = w / lam;
-                        slot = expand_slot(W, s_prefix, n_sch_old, i);
-                        prepass_item<M, R>(A, W, h0, slot, w - i * lam, &free, o);
-                        __stcg(W.it_parent + w, slot);
-                    }
-                    const unsigned fm = __ballot_sync(0xffffffffu, free), bm = __ballot_sync(0xffffffffu, act && !free);
-                    int fbase = 0, bbase = 0;
-                    if (lane == 0) {
-                        if (fm) fbase = (int)atomicAdd(&ctl->n_free, (unsigned)__popc(fm));
-                        if (bm) bbase = (int)atomicAdd(&ctl->n_packed, (unsigned)__popc(bm));
-                    }
-                    fbase = __shfl_sync(0xffffffffu, fbase, 0); bbase = __shfl_sync(0xffffffffu, bbase, 0);
-                    const unsigned below = (1u << lane) - 1u;
-                    const int fpos = items - 1 - (fbase + __popc(fm & below));
-                    if (act && !free) {
-                        const int pos = bbase + __popc(bm & below);
-                        __stcg(W.order + pos, make_int2(w, slot));
-                        __stcg(W.pos_of + w, pos);
-                    }
-                    if (fm) {
-                        if (free) __stcg(W.pos_of + w, fpos);
-                        commit_item<M, R>(A, W, Q, claim_tag, it & 1, free, w, fpos, o);
-                        if (lane == 0) atomicAdd(&ctl->sum_free, (unsigned long long)__popc(fm));
-                    }
-                }
-                team_sync(T);
-            }
-        } else {
         if (global_sort) {
             for (int b = tid; b < kBins; b += kBlock) { s_bin[b] = 0; s_bin[2 * kBins + b] = 0; }
             __syncthreads();
@@ -899,8 +930,6 @@ __device__ __forceinline__ bool iteration_head(const PlanArgs<R>& A, const Works
             }
         }
         if (global_sort) team_sync(T);
-        }
-        if (tid == 0) RS.items_sorted = global_sort ? items - (int)__ldcg(&ctl->n_free) : items;    // (= n_packed where that pass ran)
         if (keeper) RS.tp[1] = gtimer();
 
     __syncthreads();                            // the iteration header is visible to the whole CTA
@@ -1107,8 +1136,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
         if (keeper) {
             __stcg(&ctl->first_hit_w, 0x7fffffff);
             __stcg(&ctl->unit_next, 0u);
-            __stcg(&ctl->n_free, 0u);
-            __stcg(&ctl->n_packed, 0u);
+            __stcg(&ctl->n_todo, 0u);
             for (int b = 0; b < kBins; ++b) __stcg(W.bin_cursor + b, 0u);
             atomicAdd(&ctl->sum_items, (unsigned long long)items);
             const double el = (double)(gtimer() - RS.t_start) * 1e-9;
