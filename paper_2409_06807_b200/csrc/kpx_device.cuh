@@ -647,6 +647,12 @@ __device__ __forceinline__ void di_step_f32(float* cur, float* comp, const float
 // own h/6 (_kernel.pyx:196-201).
 template <class M, class R>
 struct Stepper {
+    // values carried across the substeps of an extension: the Kahan compensation of every dimension (float32)
+    static constexpr int kCarry = std::is_same<R, float>::value ? M::N : 1;
+    __device__ static __forceinline__ void init(const R*, const R*, R* carry) {
+#pragma unroll
+        for (int i = 0; i < kCarry; ++i) carry[i] = (R)0;
+    }
     __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R h6) {
         if constexpr (std::is_same<R, float>::value) rk4_step_f32<M>(cur, comp, u, h, 0.5f * h, h * 0.16666667f);
         else rk4_step<M, R>(cur, comp, u, h, (R)0.5 * h, h6);
@@ -654,8 +660,56 @@ struct Stepper {
 };
 template <>
 struct Stepper<ModelDI6, float> {
+    static constexpr int kCarry = 6;
+    __device__ static __forceinline__ void init(const float*, const float*, float* carry) {
+#pragma unroll
+        for (int i = 0; i < kCarry; ++i) carry[i] = 0.0f;
+    }
     __device__ static __forceinline__ void step(float* cur, float* comp, const float* u, float h, float) {
         di_step_f32(cur, comp, u, h, 0.5f * h);
+    }
+};
+// float32 Dubins airplane.  Speed, heading and climb angle have constant derivatives (v' = u0, theta' = u1,
+// gamma' = u2), so the position does not feed back into the vector field and RK4 degenerates: stages 2 and 3 see
+// the SAME (v, theta, gamma) -- one evaluation, weight 4 -- and stage 4 sees the state the substep ends in, i.e.
+// the next substep's stage 1.  Per substep that is TWO evaluations of the field (two paired sincos) instead of four;
+// the velocity field at the current state is carried to the next substep (carry[6..8]).  The update
+// p += h/6 (k1 + 4 k2 + k4), (v, theta, gamma) += h u is RK4's, Kahan-compensated like the generic path.
+// (float64 keeps the staged form: it is pinned bit for bit to the reference's rounding order.)
+template <>
+struct Stepper<ModelDubins6, float> {
+    static constexpr int kCarry = 9;
+    __device__ static __forceinline__ void field(float v, float th, float ga, float* f) {
+        float st, ct, sg, cg;
+        MathK<float>::sc2(th, ga, &st, &ct, &sg, &cg);
+        f[0] = v * ct * cg; f[1] = v * st * cg; f[2] = v * sg;
+    }
+    __device__ static __forceinline__ void init(const float* x0, const float*, float* carry) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) carry[i] = 0.0f;
+        field(x0[3], x0[4], x0[5], carry + 6);
+    }
+    __device__ static __forceinline__ void step(float* cur, float* carry, const float* u, float h, float) {
+        const float hh = 0.5f * h, h6 = h * 0.16666667f;
+        float k2[3], k4[3];
+        field(__fmaf_rn(hh, u[0], cur[3]), __fmaf_rn(hh, u[1], cur[4]), __fmaf_rn(hh, u[2], cur[5]), k2);
+#pragma unroll
+        for (int i = 3; i < 6; ++i) {                    // v, theta, gamma: += h u, compensated
+            const float y = __fmaf_rn(h, u[i - 3], -carry[i]);
+            const float t = __fadd_rn(cur[i], y);
+            carry[i] = __fsub_rn(__fsub_rn(t, cur[i]), y);
+            cur[i] = t;
+        }
+        field(cur[3], cur[4], cur[5], k4);               // stage 4 = the state this substep ends in
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {                    // position: Simpson weights, compensated
+            const float y = __fmaf_rn(h6, __fadd_rn(__fmaf_rn(4.0f, k2[i], carry[6 + i]), k4[i]), -carry[i]);
+            const float t = __fadd_rn(cur[i], y);
+            carry[i] = __fsub_rn(__fsub_rn(t, cur[i]), y);
+            cur[i] = t;
+            carry[6 + i] = k4[i];                        // next substep's stage 1
+        }
+        cur[4] = wrap_angle(cur[4]);                     // sin / cos are periodic: the carried field is unchanged
     }
 };
 // Stacked double integrators: the blocks do not couple, so stepping them one 6-D block at a time performs
@@ -663,6 +717,11 @@ struct Stepper<ModelDI6, float> {
 // (N = 48 would otherwise need ~200 registers).
 template <int B, class R>
 struct Stepper<ModelStackedDI<B>, R> {
+    static constexpr int kCarry = std::is_same<R, float>::value ? 6 * B : 1;
+    __device__ static __forceinline__ void init(const R*, const R*, R* carry) {
+#pragma unroll
+        for (int i = 0; i < kCarry; ++i) carry[i] = (R)0;
+    }
     __device__ static __forceinline__ void step(R* cur, R* comp, const R* u, R h, R h6) {
 #pragma unroll
         for (int b = 0; b < B; ++b) Stepper<ModelDI6, R>::step(cur + 6 * b, comp + 6 * b, u + 3 * b, h, h6);
@@ -890,9 +949,10 @@ __device__ KPX_INT_ATTR void integrate_and_map(const Params<R>& P, bool active, 
     const R h = dt / (R)(S > 0 ? S : 1);
     const R h6 = std::is_same<R, float>::value ? (R)0 : h / (R)6;      // float32 re-derives it per step
     R cur[N];
-    R comp[std::is_same<R, float>::value ? N : 1];   // Kahan carry (float32 only)
+    R comp[Stepper<typename M::Base, R>::kCarry];     // carried across substeps: Kahan compensation (float32), ...
 #pragma unroll
-    for (int i = 0; i < N; ++i) { cur[i] = x0[i]; if constexpr (std::is_same<R, float>::value) comp[i] = 0.0f; }
+    for (int i = 0; i < N; ++i) cur[i] = x0[i];
+    Stepper<typename M::Base, R>::init(x0, u, comp);
     bool ok = active, alive = active, pend = false;
     int points = 0, box_end = -1;
     const int n_obs = P.n_obs;
