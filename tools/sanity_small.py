@@ -19,3 +19,11 @@ with kp.BatchPlanner(cfg, env, model, backend="cuda", n_teams=2, team_ctas=2) as
 with kp.KinoPax(cfg, env, model, backend="cuda-f32", team_ctas=4) as eng:
     res = eng.solve()
     print("solo f32, 4 CTAs:", res.status.value, res.stats.iterations, res.stats.tree_size)
+# round 2: per-query scenes, adaptive capacity, the Philox kernels, the packed chain download and the goal sampler
+if which == "di6":
+    with kp.BatchPlanner(cfg, env, model, backend="cuda-f32-philox", n_teams=3, team_ctas=1, t_e_max=12000) as bp:
+        bp.set_scenes([env, kp.gen_environment(scene, model, seed=1)])
+        r = bp.run(np.arange(6), scenes=np.arange(6) % 2)
+        print("batch f32 philox, 2 scenes, adaptive capacity:", int(r.solved.sum()), "solved", int(r.validated.sum()), "validated")
+    g = kp.goals_for_queries(np.arange(40), env)
+    print("goal sampler:", g.shape)
