@@ -573,6 +573,7 @@ CONFIG_LEGS = [
     ("di24_forest", "cuda-f32", 2, 1, 20),          # configs[3]
     ("quad12_config5", "cuda-f32", 1, 1, 0),        # configs[4]: 8192 queries with per-query goals
     ("di6_forest", "cuda", 2, 1, 20),               # the float64 (bit-parity) kernels on the headline workload
+    ("di6_forest", "cuda-f32-philox", 2, 1, 20),    # the production Philox4x32-10 stream on the headline workload
 ]
 
 

@@ -706,7 +706,10 @@ struct Stepper<ModelQuad12, float> {
     }
     // sc_out = sin / cos of (base angles + d), from sc_base = sin / cos of the base angles
     __device__ static __forceinline__ void rotate_sc(const float* sc_base, float d0, float d1, float d2, const float* x_stage, float* sc_out) {
-        if (__builtin_expect(!(fabsf(d0) <= 0.25f && fabsf(d1) <= 0.25f && fabsf(d2) <= 0.25f), 0)) { full_sc(x_stage, sc_out); return; }
+#ifndef KPX_ROT_LIMIT
+#define KPX_ROT_LIMIT 0.25f
+#endif
+        if (__builtin_expect(!(fabsf(d0) <= KPX_ROT_LIMIT && fabsf(d1) <= KPX_ROT_LIMIT && fabsf(d2) <= KPX_ROT_LIMIT), 0)) { full_sc(x_stage, sc_out); return; }
         const float2 d = make_float2(d0, d1);
         const float2 z = __fmul2_rn(d, d);
         // sin d = d + d z (-1/6 + z/120), cos d = 1 + z (-1/2 + z (1/24 - z/720))
