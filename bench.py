@@ -74,6 +74,20 @@ def make_env(kp_envgen, kp_core, model, scene):
     return kp_envgen.gen_environment(scene, model, seed=0)
 
 
+def workload_config(workload, model, cfg_t_e, t_prop, cells) -> dict:
+    """The `config` object of the JSON line: the SAME for the GPU arm and the reference arm (the driver compares
+    them); what differs between the arms (queries per step, teams, backend) is reported under `run`."""
+    model_name, scene, _, _ = WORKLOADS[workload]
+    label = {"di6_forest": "6D double integrator in Trees (BASELINE.json configs[0], the north-star target)",
+             "quad12_narrow": "12D quadcopter in Narrow Passage (configs[1])",
+             "dubins6_building": "Dubins airplane in Building (configs[2])",
+             "quad12_config5": "8192 quadcopter queries with per-query goals (configs[4])"}.get(workload, workload)
+    return {"workload": f"{model_name}/{scene} (gen_environment seed 0): {label}; t_e={cfg_t_e}, lambda_max=32, "
+                        f"t_prop={t_prop}, cells={cells}, subcells=4, epsilon=0.005, delta=1.0; queries = seeds 0, 1, 2, ...",
+            "l2": "inputs larger than L2: the per-step working set (one arena + region state per resident query) far "
+                  "exceeds the 126 MB L2"}
+
+
 def _cfg(kp, model, seed=0, t_max=60.0):
     return kp.PlannerConfig(t_e=model.default_t_e, lambda_max=32, t_prop=model.default_t_prop, epsilon=0.005,
                             delta=1.0, cells_per_dim=model.default_cells_per_dim, subcells_per_dim=4, t_max=t_max,
@@ -170,6 +184,13 @@ def reference_throughput(workload: str, n_plans: int, procs: int):
             "median_wall_time_ms": statistics.median(r[3] for r in recs)}
 
 
+def _reference_config(workload) -> dict:
+    sys.path.insert(0, ROOT)
+    from paper_2409_06807_b200 import dynamics
+    model = get_workload_model(dynamics, WORKLOADS[workload][0])
+    return workload_config(workload, model, model.default_t_e, model.default_t_prop, model.default_cells_per_dim)
+
+
 def run_reference(args):
     """The reference arm: rank 0 only; each step = one plan per host core.  With baseline/_ref present the plans
     go through the UNMODIFIED reference (kind "reference"); otherwise through the pinned C port (kind "port")."""
@@ -207,8 +228,8 @@ def run_reference(args):
         "impl": "reference", "metric": "plans_per_sec", "value": value, "unit": "plans/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warmup, "ms_per_step": 1e3 * wall / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{model_name}/{scene} (gen_environment seed 0), default PlannerConfig, "
-                               f"one plan per worker process per step", "queries_per_step": procs},
+        "config": _reference_config(args.workload),
+        "run": {"queries_per_step": procs, "what": "one plan per worker process per step"},
         "median_time_to_solution_ms": 1e3 * statistics.median(r["median_plan_s"] for r in res),
         "success_rate": sum(r["solved"] for r in res) / plans,
         "cpu_baseline": {"value": value, "unit": "plans/s", "cores": procs, "kind": "reference" if use_ref else "port",
@@ -672,12 +693,9 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": head["total_ms"] / args.steps, "higher_is_better": True,
         "scaling": "strong" if args.workload == "quad12_config5" else "weak",
         "vs_baseline": None, "dtype": "f32" if "f32" in args.backend else "f64", "data": "synthetic",
-        "config": {"workload": f"{model_name}/{scene} (gen_environment seed 0; BASELINE.json config: "
-                               f"{'6D double integrator in Trees' if args.workload == 'di6_forest' else args.workload}), "
-                               f"t_e={cfg.t_e}, lambda_max=32, t_prop={cfg.t_prop}, cells={cfg.cells_per_dim}",
-                   "queries_per_gpu_per_step": head["q_here"], "team_ctas": head["team_ctas"], "teams": head["teams"],
-                   "l2": "per-step working set (one arena + region state per team) far exceeds the 126 MB L2",
-                   "backend": args.backend},
+        "config": workload_config(args.workload, model, cfg.t_e, cfg.t_prop, cfg.cells_per_dim),
+        "run": {"queries_per_gpu_per_step": head["q_here"], "team_ctas": head["team_ctas"], "teams": head["teams"],
+                "backend": args.backend},
         "median_time_to_solution_ms": lat["median_wall_ms"] if lat else None,
         "success_rate": lat["success_rate"] if lat else float((rec["status"] == 0).mean()),
         "time_to_solution": lat,

@@ -49,7 +49,7 @@
 #define KPX_MINB_F32_TRIG6 4     // Dubins airplane, throughput
 #endif
 #ifndef KPX_MINS_F32_TRIG6
-#define KPX_MINS_F32_TRIG6 3
+#define KPX_MINS_F32_TRIG6 2
 #endif
 #ifndef KPX_MINB_F32_MID
 #define KPX_MINB_F32_MID 3       // 12-D models (quadcopter, 2 stacked integrators), throughput

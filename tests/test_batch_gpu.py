@@ -279,7 +279,7 @@ def test_bench_spawns_its_own_ranks(kp):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=root)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["config"]["queries_per_gpu_per_step"] == 96
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["run"]["queries_per_gpu_per_step"] == 96
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["batch"]["queries"] == 96
 
 
