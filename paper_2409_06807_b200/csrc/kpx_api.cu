@@ -1,6 +1,6 @@
 // kpx_api.cu -- the C ABI declared in include/kpx.h.
 //
-// Owns device memory (one slab per handle, carved into the SoA arena, the region
+// Owns device memory (one slab per handle, carved into the node-major arena, the region
 // state and the per-iteration scratch), stages the few host inputs, launches the
 // persistent planner kernel and copies results back.  No CPU fallback exists:
 // every entry point either runs the CUDA path or returns an error code.
@@ -343,7 +343,7 @@ int d2h(std::vector<T>& dst, const void* src, size_t count) {
 }
 
 // node-major device rows (Row<R, N>, kpx_device.cuh) of `rows` x `dims` reals -> dense f64 host rows
-int soa_to_aos(const kpx_batch& b, const void* dev, int dims, long long rows, double* out, bool padded = true) {
+int rows_to_host(const kpx_batch& b, const void* dev, int dims, long long rows, double* out, bool padded = true) {
     if (rows == 0) return KPX_OK;
     const size_t stride = padded ? (size_t)row_elems(dims, (int)b.rs) : (size_t)dims;
     std::vector<char> h((size_t)rows * stride * b.rs);
@@ -356,7 +356,7 @@ int soa_to_aos(const kpx_batch& b, const void* dev, int dims, long long rows, do
     return KPX_OK;
 }
 
-int aos_to_soa(const kpx_batch& b, void* dev, int dims, long long rows, const double* in, bool padded = true) {
+int rows_from_host(const kpx_batch& b, void* dev, int dims, long long rows, const double* in, bool padded = true) {
     if (rows == 0) return KPX_OK;
     const size_t stride = padded ? (size_t)row_elems(dims, (int)b.rs) : (size_t)dims;
     std::vector<char> h((size_t)rows * stride * b.rs, 0);
@@ -847,9 +847,9 @@ int kpx_plan_snapshot(kpx_plan* p, int64_t rows, double* states, int64_t* parent
     if (rc) return rc;
     if (rows > c.size) return fail(KPX_E_ARG, "rows exceeds tree size %d", c.size);
     const Workspace& w = b.ws_host[0];
-    if (states && (rc = soa_to_aos(b, w.states, b.prob.n, rows, states))) return rc;
-    if (control && (rc = soa_to_aos(b, w.control, b.prob.nu, rows, control))) return rc;
-    if (dt && (rc = soa_to_aos(b, w.dt, 1, rows, dt, false))) return rc;      // one real per node, dense
+    if (states && (rc = rows_to_host(b, w.states, b.prob.n, rows, states))) return rc;
+    if (control && (rc = rows_to_host(b, w.control, b.prob.nu, rows, control))) return rc;
+    if (dt && (rc = rows_to_host(b, w.dt, 1, rows, dt, false))) return rc;      // one real per node, dense
     std::vector<int> tmp;
     if (parent) { if ((rc = d2h(tmp, w.parent, (size_t)rows))) return rc; for (int64_t i = 0; i < rows; ++i) parent[i] = tmp[i]; }
     if (region) { if ((rc = d2h(tmp, w.region, (size_t)rows))) return rc; for (int64_t i = 0; i < rows; ++i) region[i] = tmp[i]; }
@@ -966,7 +966,7 @@ int kpx_plan_items(kpx_plan* p, int64_t max_items, int64_t* n_items, uint8_t* va
     if ((rc = d2h(code, w.it_code, (size_t)I)) || (rc = d2h(rank, w.it_rank, (size_t)I)) ||
         (rc = d2h(par, w.it_parent, (size_t)I))) return rc;
     std::vector<double> e;
-    if (end) { e.resize((size_t)I * b.prob.n); if ((rc = soa_to_aos(b, w.it_end, b.prob.n, I, e.data()))) return rc; }
+    if (end) { e.resize((size_t)I * b.prob.n); if ((rc = rows_to_host(b, w.it_end, b.prob.n, I, e.data()))) return rc; }
     std::vector<int> pos;      // sorted iterations keep per-item results at the item's sorted position
     if (c.last_sorted && (rc = d2h(pos, w.pos_of, (size_t)I))) return rc;
     for (int64_t i = 0; i < I; ++i) {
@@ -996,8 +996,8 @@ int kpx_plan_load(kpx_plan* p, uint64_t seed, const double* goal4, int32_t itera
     CU(cudaSetDevice(b.device));
     const Workspace& w = b.ws_host[0];
     int rc;
-    if ((rc = aos_to_soa(b, w.states, b.prob.n, rows, states)) || (rc = aos_to_soa(b, w.control, b.prob.nu, rows, control)) ||
-        (rc = aos_to_soa(b, w.dt, 1, rows, dt, false))) return rc;
+    if ((rc = rows_from_host(b, w.states, b.prob.n, rows, states)) || (rc = rows_from_host(b, w.control, b.prob.nu, rows, control)) ||
+        (rc = rows_from_host(b, w.dt, 1, rows, dt, false))) return rc;
     std::vector<int> tmp((size_t)rows);
     for (int64_t i = 0; i < rows; ++i) tmp[i] = (int)parent[i];
     CU(cudaMemcpy(w.parent, tmp.data(), 4 * (size_t)rows, cudaMemcpyHostToDevice));

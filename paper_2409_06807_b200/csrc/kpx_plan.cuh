@@ -8,22 +8,27 @@
 //
 //   S0  order the items by RK4 substep count (known from the RNG draw alone) so that a warp's 32 items are
 //       equally long: a global counting sort for many-CTA teams, tile by tile in shared memory and fused
-//       with S1 for one-CTA teams; skipped when one round of the team's threads covers the iteration
+//       with S1 for one-CTA teams; skipped when one round of the team's threads covers the iteration, and
+//       absent for the float32 double integrators (nothing there is longer than anything else, see S1)
 //   S1  propagate every (EXPAND slot x extension) item, count outcomes per region
-//       (warp-aggregated atomics), claim fresh (region,sub) pairs with atomicMin on the epoch-tagged table
+//       (warp-aggregated atomics), claim fresh (region,sub) pairs with atomicMin on the epoch-tagged table.
+//       float32 double integrators: every lane first settles its item from the closed form (certified valid or
+//       invalid, ~90 %); the undecided rest goes to a list and is evaluated one item per warp, lane = substep
 //   --- team barrier ---
 //   S2  resolve first-visit winners (lowest item index), acceptance gate against
 //       LAST iteration's p_accept, per-chunk keep counts + chunk-local ranks,
 //       first goal hit (atomicMin over item index)
 //   --- team barrier ---
 //   S3  ordered append: slot = size + rank (capacity clamp, cut at first goal hit),
-//       mark regions available from the NEXT iteration; estimate sweep 1
-//       (free volume, score) with a fixed-order partial sum per CTA
+//       mark regions available from the NEXT iteration; estimate pass over the available regions: one warp
+//       per leaf of NumPy's pairwise-sum tree computes the leaf's scores and their sum in NumPy's order
 //   --- team barrier ---
-//   S4  p_accept on the fly from (score, total); demote / promote every live slot
+//   S4  every CTA combines the leaf sums up the tree -> total (bit-identical to ndarray.sum, for any team size);
+//       p_accept on the fly from (score, total); demote / promote every live slot
 //       from its keyed uniforms; per-chunk compaction of the next EXPAND set
 //   --- team barrier ---
-//       scan chunk counts -> |V_E|; rescue rule; termination
+//       list of available regions for the next estimate pass; scan chunk counts -> |V_E|; rescue rule;
+//       termination (goal, capacity -- adaptive capacity grows it in place --, run clock, stop word)
 //
 // Ordering rules (ascending slot order of V_E, item w = i*lambda + ext, append in
 // item order) are kept by construction: compaction is chunk-ordered and ranks are
@@ -188,7 +193,7 @@ struct PlanArgs {
     unsigned int* queue;          // next query index (batch mode)
     int n_queries, n_teams, team_ctas, max_chunks, max_trace, max_chain;
     int claim_shift;              // bits of a claim word that hold the item index + 1 (2^shift > t_e)
-    int stride;                   // row stride (elements) of every SoA array: capacity padded to a chunk multiple
+    int stride;                   // rows every per-node array is allocated for: capacity padded to a chunk multiple
     int resume;                   // 1: continue from Ctl (no reset), single query
     int max_iters, lam_override;
     double t_max_s;
@@ -614,14 +619,15 @@ __device__ __forceinline__ void flight_eval_unit(const PlanArgs<float>& A, const
 }
 
 // S1 of one iteration: propagate every (EXPAND slot x extension) item, count outcomes per region, claim fresh
-// (region, sub) pairs.  Three schedules, identical results (everything downstream is addressed by item number):
-//   * few items (one round of the team's threads): position == item number, one static unit per warp;
+// (region, sub) pairs.  Schedules, identical results (everything downstream is addressed by item number):
+//   * position == item number, units strided over the team's warps: iterations that fit one round of the team's
+//     threads -- and ALWAYS for the float32 double integrators, whose units all cost the same (flight_settle_unit),
+//     followed by their second pass over the list of undecided items (flight_eval_unit);
 //   * a team of many CTAs: the items were sorted by length over the whole iteration (S0 in iteration_head),
 //     warps pull units from a shared cursor, longest first;
-//   * a team of ONE CTA (many queries per GPU): tiles of kTile consecutive items are sorted by length in shared
+//   * a team of ONE CTA (many queries per GPU): tiles of kTileM consecutive items are sorted by length in shared
 //     memory and propagated right away.  A warp's 32 items then have nearly equal length AND parents that lie
-//     within a few KB of each other in every SoA row (a tile spans kTile / lambda consecutive EXPAND slots), so
-//     the parent-state gather stays in a handful of sectors instead of 32 per row, and S0 needs neither global
+//     close to each other (a tile spans kTileM / lambda consecutive EXPAND slots), and S0 needs neither global
 //     atomics nor team barriers.
 template <class M, class R>
 __device__ KPX_S1_ATTR void s1_propagate(const PlanArgs<R>& A, const Workspace& W, const QueryIn& Q, RunState& RS,
