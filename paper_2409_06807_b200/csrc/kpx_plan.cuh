@@ -62,6 +62,12 @@
 #ifndef KPX_MINS_F32_MID
 #define KPX_MINS_F32_MID 2
 #endif
+#ifndef KPX_MINB_F32_DI12
+#define KPX_MINB_F32_DI12 3      // 12-D stacked integrators, throughput
+#endif
+#ifndef KPX_MINB_F32_BIG
+#define KPX_MINB_F32_BIG 2       // 24-D / 48-D stacked integrators, throughput (1: di24 -21 %, di48 -44 %)
+#endif
 
 // Everything on the propagation path is inlined into the kernel: measured on B200, any out-of-line call on
 // it (the S1 phase, the integrator, or even the rare cooperative walk) costs 30 % of the batch throughput.
@@ -1338,7 +1344,8 @@ template <class M, class R, int V> struct MinBlocks {
     static constexpr bool kDI = M::ID == KPX_MODEL_DI6 || M::ID == KPX_MODEL_STACKED_DI;
     static constexpr int f32 = M::N <= 6 ? (kDI ? (V == KPX_LATENCY ? KPX_MINS_F32_DI : KPX_MINB_F32_DI)
                                                : (V == KPX_LATENCY ? KPX_MINS_F32_TRIG6 : KPX_MINB_F32_TRIG6))
-                                         : (M::N <= 12 ? (V == KPX_LATENCY ? KPX_MINS_F32_MID : KPX_MINB_F32_MID) : 1);
+                                         : (M::N <= 12 ? (V == KPX_LATENCY ? KPX_MINS_F32_MID : (kDI ? KPX_MINB_F32_DI12 : KPX_MINB_F32_MID))
+                                                       : (V == KPX_LATENCY ? 1 : KPX_MINB_F32_BIG));
     static constexpr int value = sizeof(R) == 4 ? f32 : (M::N <= 6 ? 2 : 1);
 };
 
