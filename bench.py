@@ -32,18 +32,19 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     # name: (model, scene, flops per RK4 substep [SURVEY 8d], queries per resident team per step).  A step holds
-    # several queries per team (592 / 444 teams of one CTA on a B200) so that teams keep pulling work while the
-    # slowest queries finish: with one query per team the tail of the launch idles ~17 % of the GPU.
+    # several queries per team (592 / 444 / 296 teams of one CTA on a B200) so that teams keep pulling work while the
+    # slowest queries finish: with one query per team the tail of the launch idles ~17 % of the GPU (8 instead of 4
+    # per team: another +3..5 %).
     "di6_forest": ("di6", "forest", 78, 8),
-    "dubins6_building": ("dubins6", "building", 118, 4),
-    "quad12_narrow": ("quad12", "narrow", 336, 4),
-    "quad12_forest": ("quad12", "forest", 336, 4),
+    "dubins6_building": ("dubins6", "building", 118, 8),
+    "quad12_narrow": ("quad12", "narrow", 336, 8),
+    "quad12_forest": ("quad12", "forest", 336, 8),
     # BASELINE.json config 4: k stacked 3-D double integrators (only block 1 is workspace position).
     # 12D uses the full-state grid (cells=3).  A full-state grid is not representable for 24D/48D (cells=1 is a
     # single region: no guidance, the planner fills its tree without reaching the goal), so those two run the
     # separately labelled variant whose grid spans block 1 only (position + velocity, cells=4, like di6).
-    "di12_forest": ("di12", "forest", 156, 4),
-    "di24_forest": ("di24g6", "forest", 312, 4),
+    "di12_forest": ("di12", "forest", 156, 8),
+    "di24_forest": ("di24g6", "forest", 312, 8),
     "di48_forest": ("di48g6", "forest", 624, 4),
     # BASELINE.json config 5: 8192 quadcopter queries with per-query random goals, sharded q mod N
     # across the GPUs of the job -- the total is fixed, so this workload reports "strong" scaling
