@@ -395,12 +395,21 @@ def test_f32_bookkeeping_is_exact_given_its_own_items(kp, orc, model_name, scene
     cfg = small_cfg(kp, model, t_e=t_e, seed=seed)
     op = orc.plan_from_problem(kp.build_problem(cfg, env, model))
     f32 = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)   # noqa: E731
+    worst_end = 0.0
     with kp.KinoPax(cfg, env, model, backend="cuda-f32", team_ctas=team) as eng:
         for it in range(1, 80):
+            before = op.snapshot()["states"]                                      # == the device tree (float32 values)
             st = eng.step()
             items = eng.last_items()
             ost = op.step_given(items["valid"], items["region"], items["sub"], items["end"], goal_hit=items["goal_hit"])
             ob = op.last_batch()
+            # the loop's own end states (the closed-form paths included) against the float64 RK4 of the reference on
+            # the same (parent state, control, duration): north_star's 1e-5 relative
+            vi = np.flatnonzero(items["valid"])
+            for w in vi[:: max(1, len(vi) // 400)]:
+                ref = orc.propagate_ode(model.kernel_id, before[items["parent_slot"][w]], f32(ob["control"][w]), float(f32(ob["dt"][w])))[-1]
+                err = _wrap_diff(items["end"][w][None, :], ref[None, :], model.wrap_dims)[0] / np.maximum(np.abs(ref), 1.0)
+                worst_end = max(worst_end, float(err.max()))
             # the kernel's parent slots are the oracle's e_slots repeated lambda times (ascending V_E order)
             lam = len(items["valid"]) // len(ob["e_slots"])
             assert np.array_equal(items["parent_slot"], np.repeat(ob["e_slots"], lam)), it
@@ -427,6 +436,7 @@ def test_f32_bookkeeping_is_exact_given_its_own_items(kp, orc, model_name, scene
         if st.status == 0:
             assert int(st.solution_slot) == int(op.raw.solution_slot)
         assert it >= 4
+    assert worst_end < F32_RTOL, worst_end
 
 
 def test_time_budget_rules(kp):
