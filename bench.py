@@ -609,6 +609,9 @@ def config_leg(ctx, workload, backend, steps, warmup, lat_seeds, peaks):
            "batch_revalidated_f64": int((rec["checked"] == 1).sum()),
            "roofline": {"bound": "fp32" if "f32" in backend else "fp64", "achieved": t["achieved_tflops"],
                         "peak": t.get("peak_tflops"), "unit": "TFLOP/s", "frac": t.get("frac")}}
+    traffic, traffic_src, hbm = _traffic(workload, t["q_here"], t["kern_ms"])
+    if traffic is not None:
+        ent["roofline"].update({"traffic": traffic, "traffic_source": traffic_src, "hbm": hbm})
     gold = os.path.join(ROOT, "tests", "golden", f"outcomes_{workload}.json")
     if os.path.isfile(gold) and ctx.world == 1 and len(rec) >= 100:
         g = json.load(open(gold))                          # the batch's first 100 queries are seeds 0..99
