@@ -249,7 +249,8 @@ typedef struct kpx_query_result {
 
 int kpx_batch_create(const kpx_problem *prob, int32_t precision, int32_t n_teams, int32_t team_ctas,
                      int32_t max_chain, int32_t device, kpx_batch **out);
-/* teams / CTAs per team the batch was created with (n_teams <= 0 at creation: as many teams as are co-resident) */
+/* teams / CTAs per team the batch was created with (n_teams = 0 at creation: as many teams as are co-resident;
+ * n_teams = -k: min(k, co-resident), for callers that know how many queries they will ever upload) */
 int kpx_batch_info(const kpx_batch *b, int32_t *n_teams, int32_t *team_ctas);
 void kpx_batch_destroy(kpx_batch *b);
 /* seeds[Q], starts[Q,n], goals[Q,4] host arrays; chain buffers (may be NULL) sized Q*max_chain */

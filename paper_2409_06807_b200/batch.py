@@ -101,8 +101,8 @@ class BatchPlanner:
         self._prob_struct, self._keep = _lib.problem_from(self.problem, rng=self.backend.rng, t_e_max=t_e_max, t_e_growth=t_e_growth)
         self.max_chain, self.device = int(max_chain), device
         self._handle = _lib._vp()
-        # n_teams <= 0: as many teams as are co-resident on the device for this model and precision
-        _lib.check(self._lib.kpx_batch_create(C.byref(self._prob_struct), self.precision, int(max(n_teams, 0)),
+        # n_teams = 0: as many teams as are co-resident on the device for this model and precision; -k: at most k of them
+        _lib.check(self._lib.kpx_batch_create(C.byref(self._prob_struct), self.precision, int(n_teams),
                                               int(team_ctas), self.max_chain, int(device), C.byref(self._handle)),
                    "kpx_batch_create")
         nt, tc = C.c_int32(0), C.c_int32(0)

@@ -229,7 +229,8 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
         n_teams = 1;
         team_ctas = max_resident;
     }
-    if (n_teams <= 0) n_teams = std::max(1, max_resident / team_ctas);     // as many teams as fit the device
+    if (n_teams < 0) n_teams = std::max(1, std::min(-n_teams, max_resident / team_ctas));   // at most -n_teams, never beyond what is co-resident
+    if (n_teams == 0) n_teams = std::max(1, max_resident / team_ctas);     // as many teams as fit the device
     if (n_teams < 1) return fail(KPX_E_ARG, "n_teams must be >= 1");
     b.cooperative = team_ctas > 1;
     if (b.cooperative && (long long)n_teams * team_ctas > max_resident)

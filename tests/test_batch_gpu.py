@@ -379,3 +379,18 @@ def test_per_query_scenes_match_single_scene_plans(kp, orc):
         bp.set_scenes([base, blocked])
         with pytest.raises(kp.ConfigError):
             bp.run([0, 1], scenes=[0, 1])                      # the start lies inside scene 1's obstacle
+
+
+def test_team_count_requests(kp):
+    """kpx_batch_create: n_teams = 0 sizes the batch to what is co-resident on the device, -k asks for at most k teams
+    (what the trial runner does: one team per trial, never more workspaces than can run), k > 0 for exactly k."""
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=2000, seed=0)
+    with kp.BatchPlanner(cfg, env, model, backend="cuda-f32") as auto:
+        resident = auto.n_teams
+    assert resident >= 148
+    for ask, want in ((-5, 5), (-10 ** 6, resident), (7, 7)):
+        with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", n_teams=ask) as bp:
+            assert bp.n_teams == want and bp.team_ctas == 1
+            assert len(bp.run(np.arange(12), want_chains=False)) == 12
