@@ -391,6 +391,9 @@ template <> struct MathK<float> {
 // the in-range fast path returns the identical value.
 template <class R>
 __device__ __forceinline__ R wrap_angle(R a) {
+    // float32: an angle already inside (-pi, pi) is returned as it is -- (a + pi) - pi would round it to a multiple
+    // of ulp(2 pi) = 4.8e-7 after every substep, an error the float64 formula does not have
+    if constexpr (std::is_same<R, float>::value) { if (fabsf(a) < MathK<float>::PI) return a; }
     R t = a + MathK<R>::PI;
     if (!(t >= (R)0 && t < MathK<R>::TWO_PI)) t = MathK<R>::mod(t, MathK<R>::TWO_PI);
     if (t <= (R)0) t += MathK<R>::TWO_PI;
@@ -475,8 +478,8 @@ struct ModelQuad12 {
         o[6] = p + sw * (sth * icth);
         o[7] = q * cphi - r * sphi;
         o[8] = sw * icth;
-        o[9] = (u[1] - 0.01f * q * r) * 100.0f;
-        o[10] = (u[2] + 0.01f * p * r) * 100.0f;
+        o[9] = __fmaf_rn(-q, r, u[1] * 100.0f);          // (u1 - (Jz - Jy) q r) / Jx with J = diag(.01, .01, .02)
+        o[10] = __fmaf_rn(p, r, u[2] * 100.0f);
         o[11] = u[3] * 50.0f;
     }
 };
@@ -749,7 +752,8 @@ struct Stepper<ModelQuad12, float> {
     __device__ static __forceinline__ void step(float* cur, float* comp, const float* u, float h, float) {
         constexpr int N = 12, H = 6;
         const float half_h = 0.5f * h, h6 = h * 0.16666667f;
-        float k[N], tmp[N], sc1[6], sc[6];
+        float k[N], tmp[N], sc[6];
+        float sc1[6];
         float2 acc[H];
         const float2 hh2 = f2(half_h, half_h), h2 = f2(h, h), two = f2(2.0f, 2.0f), h62 = f2(h6, h6);
         full_sc(cur, sc1);
