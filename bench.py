@@ -752,6 +752,12 @@ def _free_port() -> int:
 def self_spawn(args) -> int:
     """`python bench.py --gpus N` outside torchrun: launch the N ranks ourselves, exactly as the driver would
     (one process per GPU, NCCL), and pass the ranks' output through."""
+    if "KPX_BENCH_DEVICE" not in os.environ:       # (the test hook that puts every rank on one GPU)
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py --gpus {args.gpus}: one rank per GPU, but only {have} GPU(s) are visible\n")
+            return 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd)
