@@ -252,6 +252,16 @@ int kpx_batch_create(const kpx_problem *prob, int32_t precision, int32_t n_teams
 /* teams / CTAs per team the batch was created with (n_teams = 0 at creation: as many teams as are co-resident;
  * n_teams = -k: min(k, co-resident), for callers that know how many queries they will ever upload) */
 int kpx_batch_info(const kpx_batch *b, int32_t *n_teams, int32_t *team_ctas);
+/* Hand-off of a batch's stragglers (default on, batches of one-CTA teams with >= 16 queries): when the query queue is
+ * empty and at most (co-resident CTAs / 8) teams are still planning, kpx_batch_launch ends its first kernel and
+ * continues those queries on teams of 8 CTAs in a second one, the last (co-resident / 64) of them on teams of 64 in a
+ * third -- all on the caller's stream, no host synchronisation.  Results are those of the one-CTA run (a plan does
+ * not depend on the team size); only device_ms of the handed-off queries is shorter.  No reference counterpart:
+ * the reference plans one query per process (bench.py:106-171). */
+int kpx_batch_set_handoff(kpx_batch *b, int32_t enable);
+/* queries the last kpx_batch_launch handed to teams of 8 CTAs (counts[0]) and on to teams of 64 (counts[1]);
+ * synchronises the device */
+int kpx_batch_handoff_counts(kpx_batch *b, int32_t *counts);
 void kpx_batch_destroy(kpx_batch *b);
 /* seeds[Q], starts[Q,n], goals[Q,4] host arrays; chain buffers (may be NULL) sized Q*max_chain */
 int kpx_batch_run(kpx_batch *b, int64_t n_queries, const uint64_t *seeds, const double *starts,

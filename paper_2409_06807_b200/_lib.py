@@ -111,6 +111,8 @@ _SIGNATURES = {
     "kpx_batch_set_scenes": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
     "kpx_batch_upload_scenes": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, C.c_int32, _vp]),
     "kpx_batch_launch": (C.c_int, [_vp, C.c_double, _vp]),
+    "kpx_batch_set_handoff": (C.c_int, [_vp, C.c_int32]),
+    "kpx_batch_handoff_counts": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "kpx_batch_validate": (C.c_int, [_vp, C.c_double, _vp]),
     "kpx_batch_download": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "kpx_batch_run": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, _vp,

@@ -91,7 +91,7 @@ class BatchPlanner:
 
     def __init__(self, cfg: PlannerConfig, env: Environment, model: DynamicsModel, check_resolution: float = 0.05,
                  backend: Optional[str] = None, n_teams: int = 0, team_ctas: int = 1, max_chain: int = 64,
-                 device: int = 0, t_e_max: Optional[int] = None, t_e_growth: float = 2.0):
+                 device: int = 0, t_e_max: Optional[int] = None, t_e_growth: float = 2.0, handoff: bool = True):
         self.problem = build_problem(cfg, env, model, check_resolution)
         self.cfg, self.env, self.model = cfg, env, model
         self.backend = get_backend(backend, model)
@@ -108,9 +108,19 @@ class BatchPlanner:
         nt, tc = C.c_int32(0), C.c_int32(0)
         _lib.check(self._lib.kpx_batch_info(self._handle, C.byref(nt), C.byref(tc)), "kpx_batch_info")
         self.n_teams, self.team_ctas = int(nt.value), int(tc.value)
+        # the last queries of a launch carry on on teams of 8, then 64 CTAs (kpx_batch_set_handoff); same results
+        self.handoff = bool(handoff)
+        if not self.handoff:
+            _lib.check(self._lib.kpx_batch_set_handoff(self._handle, 0), "kpx_batch_set_handoff")
         self._f64 = None              # float64 twin, created when a refused float32 solution needs re-planning
         self.scenes = [env]           # obstacle sets a query can name (set_scenes); scene 0 is `env`
         self._scene_probs = {0: (self._prob_struct, self._keep)}
+
+    def handoff_counts(self) -> tuple:
+        """Queries the last launch handed to teams of 8 CTAs and on to teams of 64 (``kpx_batch_handoff_counts``)."""
+        c = (C.c_int32 * 2)()
+        _lib.check(self._lib.kpx_batch_handoff_counts(self._handle, c), "kpx_batch_handoff_counts")
+        return int(c[0]), int(c[1])
 
     def set_scenes(self, envs: Sequence[Environment]) -> None:
         """Obstacle sets the queries of a batch can name (``run(..., scenes=idx)``): the batched form of planning in

@@ -147,7 +147,14 @@ struct kpx_batch {
     ResultPacket* pk_host = nullptr;   // pinned
     QueryIn* q_pinned = nullptr;       // pinned
     bool pk_valid = false;
+    // hand-off of a batch's last queries to wider teams (kpx_batch_launch)
+    int max_resident = 0;              // CTAs of the plan kernel the device holds at once
+    bool handoff = true;
+    unsigned int* hand_dev = nullptr;  // [0..7] idle teams per stage, [8..15] suspended queries per stage
+    int2* susp_dev = nullptr;          // [kHandoffLevels][n_teams] (workspace, query)
+    int hand_levels = 2, hand_width[kHandoffLevels] = {8, 64, 0, 0};   // CTAs per team of the stages after the first
 };
+constexpr int kHandoffLevels = 4;   // at most; kpx_batch::hand_width holds the ones in use
 
 struct kpx_plan { kpx_batch b; };
 
@@ -155,7 +162,7 @@ namespace {
 
 void destroy_batch(kpx_batch& b) {
     cudaSetDevice(b.device);
-    cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.boxes64_dev); cudaFree(b.occ_dev); cudaFree(b.queue_dev); cudaFree(b.q_dev);
+    cudaFree(b.slab); cudaFree(b.ws_dev); cudaFree(b.obs_dev); cudaFree(b.boxes64_dev); cudaFree(b.occ_dev); cudaFree(b.queue_dev); cudaFree(b.hand_dev); cudaFree(b.susp_dev); cudaFree(b.q_dev);
     cudaFree(b.r_dev); cudaFree(b.bc_start); cudaFree(b.bc_ctrl); cudaFree(b.bc_dt); cudaFree(b.peers_dev);
     cudaFree(b.bp_start); cudaFree(b.bp_ctrl); cudaFree(b.bp_dt); cudaFree(b.bp_off); cudaFreeHost(b.bp_host);
     cudaFreeHost(b.pk_host); cudaFreeHost(b.q_pinned);
@@ -228,6 +235,16 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     if (team_ctas <= 0) {
         n_teams = 1;
         team_ctas = max_resident;
+    }
+    b.max_resident = max_resident;
+    if (const char* e = getenv("KPX_HANDOFF")) b.handoff = atoi(e) != 0;     // measurement knobs
+    if (const char* e = getenv("KPX_HANDOFF_WIDTHS")) {
+        b.hand_levels = 0;
+        for (const char* p = e; *p && b.hand_levels < kHandoffLevels;) {
+            b.hand_width[b.hand_levels++] = std::max(2, atoi(p));
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+        }
     }
     if (n_teams < 0) n_teams = std::max(1, std::min(-n_teams, max_resident / team_ctas));   // at most -n_teams, never beyond what is co-resident
     if (n_teams == 0) n_teams = std::max(1, max_resident / team_ctas);     // as many teams as fit the device
@@ -304,6 +321,9 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     if (rc) return rc;
     CU(cudaMalloc(&b.queue_dev, 256));
     CU(cudaMemset(b.queue_dev, 0, 256));
+    CU(cudaMalloc(&b.hand_dev, 64));
+    CU(cudaMemset(b.hand_dev, 0, 64));
+    CU(cudaMalloc(&b.susp_dev, sizeof(int2) * (size_t)kHandoffLevels * (size_t)n_teams));
     CU(cudaMallocHost(&b.pk_host, sizeof(ResultPacket)));
     CU(cudaMallocHost(&b.q_pinned, sizeof(QueryIn)));
     return KPX_OK;
@@ -445,6 +465,13 @@ namespace {
 // Solution chains leave the device packed: off[q] = rows of the solved queries before q (one block scans the
 // chain lengths), then one block per query copies its rows.  A query's chain is chain_len rows of n + nu + 1
 // doubles out of a max_chain-row slot, typically 6 of 64: the packed copy is a tenth of the dense one.
+// a suspended query's workspace still holds the stop word that suspended it: cleared between the launches (inside
+// the resumed kernel one CTA of a team could clear it after another has already read it)
+__global__ void clear_stop_kernel(Workspace* ws, const int2* __restrict__ list, const unsigned int* __restrict__ n_list) {
+    const unsigned int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < *n_list) ws[list[i].x].ctl->stop = 0;
+}
+
 __global__ void chain_offsets_kernel(int n_q, const kpx_query_result* __restrict__ res, long long* __restrict__ off) {
     __shared__ long long s_part[32];
     __shared__ long long s_carry;
@@ -1223,6 +1250,21 @@ int kpx_batch_create(const kpx_problem* prob, int32_t precision, int32_t n_teams
     return KPX_OK;
 }
 
+int kpx_batch_set_handoff(kpx_batch* b, int32_t enable) {
+    if (!b) return fail(KPX_E_ARG, "null batch");
+    b->handoff = enable != 0;
+    return KPX_OK;
+}
+
+int kpx_batch_handoff_counts(kpx_batch* b, int32_t* counts) {
+    if (!b || !counts) return fail(KPX_E_ARG, "null argument");
+    unsigned int h[2] = {0u, 0u};
+    CU(cudaSetDevice(b->device));
+    CU(cudaMemcpy(h, b->hand_dev + 8, sizeof h, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 2; ++i) counts[i] = (int32_t)h[i];
+    return KPX_OK;
+}
+
 int kpx_batch_info(const kpx_batch* b, int32_t* n_teams, int32_t* team_ctas) {
     if (!b) return fail(KPX_E_ARG, "null batch");
     if (n_teams) *n_teams = b->n_teams;
@@ -1296,7 +1338,35 @@ int kpx_batch_launch(kpx_batch* bp, double t_max, void* stream) {
     L.n_queries = (int)b.n_uploaded; L.queries_dev = b.q_dev; L.results_dev = b.r_dev; L.queue_dev = b.queue_dev;
     L.resume = 0; L.max_iters = 0; L.lam_override = 0; L.t_max_s = t_max;
     if (b.want_chains) { L.b_chain_start = b.bc_start; L.b_chain_control = b.bc_ctrl; L.b_chain_dt = b.bc_dt; }
-    return launch(b, L, st);
+    // Hand-off: the launch ends when the queue is empty and only a few teams are still planning; those queries carry
+    // on in the next launch on teams of 8 CTAs, the last of them on teams of 64 -- instead of one CTA each while the
+    // rest of the device idles.  Results do not depend on the team size, so nothing else changes.  Everything is
+    // stream-ordered: a stage that finds nothing suspended costs one empty launch.
+    int levels = 0, keep[kHandoffLevels] = {0, 0, 0, 0};
+    if (b.handoff && b.team_ctas == 1 && b.n_uploaded >= 16)
+        while (levels < b.hand_levels && b.max_resident >= 2 * b.hand_width[levels]) {
+            keep[levels] = b.max_resident / b.hand_width[levels];
+            ++levels;
+        }
+    if (levels) {
+        CU(cudaMemsetAsync(b.hand_dev, 0, 64, st));
+        L.idle = b.hand_dev; L.handoff_at = std::max(1, b.n_teams - keep[0]);
+        L.susp_out = b.susp_dev; L.n_susp_out = b.hand_dev + 8;
+    }
+    int rc = launch(b, L, st);
+    for (int s = 1; s <= levels && rc == KPX_OK; ++s) {
+        const int2* list = b.susp_dev + (size_t)(s - 1) * (size_t)b.n_teams;
+        const unsigned int* n_list = b.hand_dev + 8 + (s - 1);
+        const int teams = std::min(keep[s - 1], b.n_teams);          // at most that many were suspended
+        clear_stop_kernel<<<(teams + 255) / 256, 256, 0, st>>>(b.ws_dev, list, n_list);
+        PlanLaunch H = L;
+        H.queue_dev = nullptr; H.resume = 1; H.n_teams = teams; H.team_ctas = b.hand_width[s - 1]; H.cooperative = true;
+        H.resume_in = list; H.n_resume_in = n_list; H.idle = b.hand_dev + s;
+        H.handoff_at = s < levels ? std::max(1, teams - keep[s]) : 0;
+        H.susp_out = b.susp_dev + (size_t)s * (size_t)b.n_teams; H.n_susp_out = b.hand_dev + 8 + s;
+        rc = launch(b, H, st);
+    }
+    return rc;
 }
 
 int kpx_batch_validate(kpx_batch* bp, double res, void* stream) {

@@ -23,6 +23,11 @@ struct PlanLaunch {
     uint32_t* const* peer_flags;
     int n_peers;
     double *b_chain_start, *b_chain_control, *b_chain_dt;
+    // hand-off of a batch's last queries to wider teams (PlanArgs, kpx_plan.cuh)
+    unsigned int* idle;
+    int handoff_at;
+    int2* susp_out; unsigned int* n_susp_out;
+    const int2* resume_in; const unsigned int* n_resume_in;
     size_t smem;
     bool cooperative;
     bool latency;                   // one query on the whole GPU: the latency build of the float32 kernels

@@ -208,7 +208,16 @@ struct PlanArgs {
     int n_peers;
     // batch-mode chain outputs, [n_queries][max_chain][...] (may be null)
     double *b_chain_start, *b_chain_control, *b_chain_dt;
+    // Hand-off of the last queries of a batch to wider teams (kpx_batch_launch).  Every team that runs out of work
+    // adds 1 to *idle; once handoff_at teams are idle the teams still planning stop after their iteration with the
+    // run state in Ctl (exactly the state a stepped single plan keeps between launches) and list (workspace, query)
+    // in susp_out.  The next launch -- teams of more CTAs, resume = 1 -- continues entry j of resume_in on team j.
+    unsigned int* idle;           // may be null
+    int handoff_at;               // 0: never suspend
+    int2* susp_out; unsigned int* n_susp_out;
+    const int2* resume_in; const unsigned int* n_resume_in;
 };
+constexpr int KPX_HANDOFF = 6;    // internal stop code: never reaches a result (the resumed launch overwrites it)
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -219,6 +228,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct Team {
     int ctas, rank;
     unsigned int* bar;
+    int ws_index;                 // which workspace of PlanArgs::ws this team plans on
 };
 
 // Barrier over the team's CTAs (all co-resident: cooperative launch).  One atomic per CTA: rank 0 adds
@@ -1155,6 +1165,7 @@ __device__ __forceinline__ void iteration_tail(const PlanArgs<R>& A, const Works
             int stop = 0;
             if (!(el < A.t_max_s)) stop = KPX_TIMEOUT;                               // planner.py:282
             if (A.stop_flag && *((volatile const uint32_t*)A.stop_flag)) stop = KPX_STOPPED;
+            if (!stop && A.handoff_at > 0 && *((volatile const unsigned int*)A.idle) >= (unsigned)A.handoff_at) stop = KPX_HANDOFF;
             if (stop) ctl->stop = stop;
         }
         team_sync(T);
@@ -1235,6 +1246,8 @@ __device__ __forceinline__ void finish_query(const PlanArgs<R>& A, const Workspa
         ctl->size = size; ctl->iteration = it; ctl->status = status; ctl->solution_slot = solution_slot;
         ctl->total_prev = RS.total_prev; ctl->ve = RS.ve; ctl->n_est = RS.n_est; ctl->cap = RS.cap;
         ctl->elapsed_ns = gtimer() - RS.t_start;
+        if (status == KPX_HANDOFF && A.susp_out)
+            A.susp_out[atomicAdd(A.n_susp_out, 1u)] = make_int2(T.ws_index, (int)query_index);
         int len = 0;
         if (status == KPX_SOLVED) {
             // parent chain (planner.py:325-336), written root-first
@@ -1313,7 +1326,7 @@ __device__ KPX_RQ_ATTR void run_query(const PlanArgs<R>& A, const Workspace& W, 
         // reference's `while elapsed < t_max` does.  Every CTA of the team evaluates the same words.
         const unsigned long long elapsed0 = A.resume ? __ldcg(&ctl->elapsed_ns) : 0ull;
         int status = __ldcg(&ctl->status);
-        if (A.resume && (status == KPX_TIMEOUT || status == KPX_STOPPED)) status = KPX_RUNNING;
+        if (A.resume && (status == KPX_TIMEOUT || status == KPX_STOPPED || status == KPX_HANDOFF)) status = KPX_RUNNING;
         if (status == KPX_RUNNING && !((double)elapsed0 * 1e-9 < A.t_max_s)) status = KPX_TIMEOUT;
         if (threadIdx.x == 0) {
             RS.size = size; RS.it = __ldcg(&ctl->iteration); RS.status = status;
@@ -1367,10 +1380,25 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R, V>::value) plan_kernel
     if (team_id >= A.n_teams) return;
     __shared__ RunState s_rs;
     __shared__ Workspace s_ws;            // CTA-uniform: one copy in shared memory instead of ~60 registers per thread
-    if (threadIdx.x == 0) s_ws = A.ws[team_id];
+    int2 handed = make_int2(team_id, 0);  // hand-off stage: (workspace, query) this team continues
+    if (A.resume_in) {
+        if ((unsigned)team_id >= __ldcg(A.n_resume_in)) {            // nothing left for this team
+            if (T.rank == 0 && threadIdx.x == 0 && A.idle) atomicAdd(A.idle, 1u);
+            return;
+        }
+        handed = __ldcg(A.resume_in + team_id);
+    }
+    T.ws_index = handed.x;
+    if (threadIdx.x == 0) s_ws = A.ws[handed.x];
     __syncthreads();
     const Workspace& W = s_ws;
     T.bar = W.bar;
+
+    if (A.resume_in) {
+        run_query<M, R>(A, W, T, A.queries[handed.y], A.results + handed.y, handed.y, s_rs, s_prefix, s_w, s_d, s_bin, &s_scene);
+        if (T.rank == 0 && threadIdx.x == 0 && A.idle) atomicAdd(A.idle, 1u);
+        return;
+    }
 
     if (A.queue == nullptr) {       // single query bound to team 0 (plan handle: stepped / resumable)
         run_query<M, R>(A, W, T, A.queries[0], A.results, 0, s_rs, s_prefix, s_w, s_d, s_bin, &s_scene);
@@ -1389,7 +1417,10 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R, V>::value) plan_kernel
         }
         const int q = s_q;
         __syncthreads();
-        if (q >= A.n_queries) return;
+        if (q >= A.n_queries) {
+            if (T.rank == 0 && threadIdx.x == 0 && A.idle) atomicAdd(A.idle, 1u);
+            return;
+        }
         run_query<M, R>(A, W, T, A.queries[q], A.results + q, q, s_rs, s_prefix, s_w, s_d, s_bin, &s_scene);
         team_sync(T);
     }

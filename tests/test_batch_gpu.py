@@ -394,3 +394,26 @@ def test_team_count_requests(kp):
         with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", n_teams=ask) as bp:
             assert bp.n_teams == want and bp.team_ctas == 1
             assert len(bp.run(np.arange(12), want_chains=False)) == 12
+
+
+@pytest.mark.parametrize("backend", ["cuda", "cuda-f32"])
+def test_handoff_to_wider_teams_changes_nothing(kp, backend):
+    """The last queries of a launch carry on on teams of 8 CTAs, the very last on teams of 64 (kpx_batch_set_handoff):
+    every record -- status, iterations, tree size, work counters, chain -- equals the run that keeps one CTA per query
+    to the end, and the hand-off really took place."""
+    model = kp.get_model("di6")
+    env = kp.gen_environment("forest", model, seed=0)
+    cfg = small_cfg(kp, model, t_e=30000, seed=0)
+    seeds = np.arange(150)
+    with kp.BatchPlanner(cfg, env, model, backend=backend, n_teams=32, handoff=False) as plain:
+        a = plain.run(seeds, replan_rejected=False)
+        assert plain.handoff_counts() == (0, 0)
+    with kp.BatchPlanner(cfg, env, model, backend=backend, n_teams=32) as bp:
+        b = bp.run(seeds, replan_rejected=False)
+        first, second = bp.handoff_counts()
+    assert 1 <= first <= 31 and 1 <= second <= 9, (first, second)
+    for key in ("status", "iterations", "tree_size", "solution_slot", "chain_len", "items", "substeps", "points", "boxsteps",
+                "free_items", "checked"):
+        assert np.array_equal(a.records[key], b.records[key]), key
+    assert np.array_equal(a.chain_dt, b.chain_dt) and np.array_equal(a.chain_control, b.chain_control)
+    assert int(a.solved.sum()) >= 140

@@ -15,5 +15,5 @@ python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/final_bench_ref.json 2> gpurun_out/final_bench_ref.err
 python bench.py --gpus 2 --steps 2 --warmup 1 --no-configs --no-latency --no-kernel-seam --no-cpu-baseline > gpurun_out/final_bench_2ranks.json 2> gpurun_out/final_bench_2ranks.err
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/final_launches.log 2>&1
-for m in di6 dubins6 quad12; do for t in memcheck racecheck synccheck; do echo "== $m $t"; timeout 700 compute-sanitizer --tool $t python tools/sanity_small.py $m 2>&1 | grep -E "solved|validated|SUMMARY|sampler|rror" | head -12; done; done > gpurun_out/final_sanitizer.txt 2>&1
+for m in di6 dubins6 quad12; do for t in memcheck racecheck synccheck; do echo "== $m $t"; timeout 700 compute-sanitizer --tool $t python tools/sanity_small.py $m 2>&1 | grep -E "solved|validated|SUMMARY|sampler|rror" | head -14; done; done > gpurun_out/final_sanitizer.txt 2>&1
 tail -2 gpurun_out/final_tests.log; head -c 600 gpurun_out/final_bench.json; tail -3 gpurun_out/final_sanitizer.txt

@@ -25,5 +25,8 @@ if which == "di6":
         bp.set_scenes([env, kp.gen_environment(scene, model, seed=1)])
         r = bp.run(np.arange(6), scenes=np.arange(6) % 2)
         print("batch f32 philox, 2 scenes, adaptive capacity:", int(r.solved.sum()), "solved", int(r.validated.sum()), "validated")
+    with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", n_teams=6, team_ctas=1) as bp:      # hand-off to teams of 8 / 64 CTAs
+        r = bp.run(np.arange(20))
+        print("batch f32 with hand-off:", int(r.solved.sum()), "solved", int(r.validated.sum()), "validated, handed on", bp.handoff_counts())
     g = kp.goals_for_queries(np.arange(40), env)
     print("goal sampler:", g.shape)
