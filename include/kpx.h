@@ -250,7 +250,9 @@ typedef struct kpx_query_result {
 int kpx_batch_create(const kpx_problem *prob, int32_t precision, int32_t n_teams, int32_t team_ctas,
                      int32_t max_chain, int32_t device, kpx_batch **out);
 /* teams / CTAs per team the batch was created with (n_teams = 0 at creation: as many teams as are co-resident;
- * n_teams = -k: min(k, co-resident), for callers that know how many queries they will ever upload) */
+ * n_teams = -k: min(k, co-resident), for callers that know how many queries they will ever upload;
+ * team_ctas = 0: 1, 2, 4, 8 or 16 CTAs per team, the widest that keeps all n_teams teams co-resident -- the
+ * trial runner's choice: 100 trials on a device that holds 592 CTAs plan on teams of 4) */
 int kpx_batch_info(const kpx_batch *b, int32_t *n_teams, int32_t *team_ctas);
 /* Hand-off of a batch's stragglers (default on, batches of one-CTA teams with >= 16 queries): when the query queue is
  * empty and at most (co-resident CTAs / 8) teams are still planning, kpx_batch_launch ends its first kernel and

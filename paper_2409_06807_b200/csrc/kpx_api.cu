@@ -104,6 +104,8 @@ struct Carver {
 
 }  // namespace
 
+constexpr int kHandoffLevels = 4;   // hand-off stages at most; kpx_batch::hand_width holds the ones in use
+
 struct kpx_batch {
     kpx_problem prob;
     std::vector<double> obs_min, obs_max;
@@ -150,11 +152,11 @@ struct kpx_batch {
     // hand-off of a batch's last queries to wider teams (kpx_batch_launch)
     int max_resident = 0;              // CTAs of the plan kernel the device holds at once
     bool handoff = true;
+    bool auto_width = false;           // kpx_batch_create(team_ctas = 0): teams as wide as the team count leaves room for
     unsigned int* hand_dev = nullptr;  // [0..7] idle teams per stage, [8..15] suspended queries per stage
     int2* susp_dev = nullptr;          // [kHandoffLevels][n_teams] (workspace, query)
     int hand_levels = 2, hand_width[kHandoffLevels] = {8, 64, 0, 0};   // CTAs per team of the stages after the first
 };
-constexpr int kHandoffLevels = 4;   // at most; kpx_batch::hand_width holds the ones in use
 
 struct kpx_plan { kpx_batch b; };
 
@@ -249,6 +251,10 @@ int init_batch(kpx_batch& b, const kpx_problem* prob, int precision, int n_teams
     if (n_teams < 0) n_teams = std::max(1, std::min(-n_teams, max_resident / team_ctas));   // at most -n_teams, never beyond what is co-resident
     if (n_teams == 0) n_teams = std::max(1, max_resident / team_ctas);     // as many teams as fit the device
     if (n_teams < 1) return fail(KPX_E_ARG, "n_teams must be >= 1");
+    if (b.auto_width) {                // few queries on a big device: 2, 4, 8 or 16 CTAs per team from the start
+        team_ctas = 1;
+        while (team_ctas < 16 && (long long)n_teams * team_ctas * 2 <= max_resident) team_ctas *= 2;
+    }
     b.cooperative = team_ctas > 1;
     if (b.cooperative && (long long)n_teams * team_ctas > max_resident)
         return fail(KPX_E_LIMIT, "teams of %d CTAs x %d exceed the %d co-resident CTAs of this device", team_ctas,
@@ -1242,9 +1248,10 @@ int kpx_batch_create(const kpx_problem* prob, int32_t precision, int32_t n_teams
                      int32_t device, kpx_batch** out) {
     if (!out) return fail(KPX_E_ARG, "out is null");
     *out = nullptr;
-    if (team_ctas < 1) return fail(KPX_E_ARG, "team_ctas must be >= 1 for batches");
+    if (team_ctas < 0) return fail(KPX_E_ARG, "team_ctas must be >= 0 for batches (0: as wide as n_teams leaves room for)");
     kpx_batch* b = new kpx_batch();
-    int rc = init_batch(*b, prob, precision, n_teams, team_ctas, max_chain > 0 ? max_chain : 64, device);
+    b->auto_width = team_ctas == 0;
+    int rc = init_batch(*b, prob, precision, n_teams, std::max(team_ctas, 1), max_chain > 0 ? max_chain : 64, device);
     if (rc) { destroy_batch(*b); delete b; return rc; }
     *out = b;
     return KPX_OK;
@@ -1342,12 +1349,14 @@ int kpx_batch_launch(kpx_batch* bp, double t_max, void* stream) {
     // on in the next launch on teams of 8 CTAs, the last of them on teams of 64 -- instead of one CTA each while the
     // rest of the device idles.  Results do not depend on the team size, so nothing else changes.  Everything is
     // stream-ordered: a stage that finds nothing suspended costs one empty launch.
-    int levels = 0, keep[kHandoffLevels] = {0, 0, 0, 0};
-    if (b.handoff && b.team_ctas == 1 && b.n_uploaded >= 16)
-        while (levels < b.hand_levels && b.max_resident >= 2 * b.hand_width[levels]) {
-            keep[levels] = b.max_resident / b.hand_width[levels];
-            ++levels;
-        }
+    int levels = 0, keep[kHandoffLevels] = {0, 0, 0, 0}, width[kHandoffLevels] = {0, 0, 0, 0};
+    if (b.handoff && !b.latency && b.n_uploaded >= 16)
+        for (int i = 0; i < b.hand_levels; ++i)            // the stages wider than the teams the batch starts with
+            if (b.hand_width[i] > b.team_ctas && b.max_resident >= 2 * b.hand_width[i]) {
+                width[levels] = b.hand_width[i];
+                keep[levels] = b.max_resident / b.hand_width[i];
+                ++levels;
+            }
     if (levels) {
         CU(cudaMemsetAsync(b.hand_dev, 0, 64, st));
         L.idle = b.hand_dev; L.handoff_at = std::max(1, b.n_teams - keep[0]);
@@ -1360,7 +1369,7 @@ int kpx_batch_launch(kpx_batch* bp, double t_max, void* stream) {
         const int teams = std::min(keep[s - 1], b.n_teams);          // at most that many were suspended
         clear_stop_kernel<<<(teams + 255) / 256, 256, 0, st>>>(b.ws_dev, list, n_list);
         PlanLaunch H = L;
-        H.queue_dev = nullptr; H.resume = 1; H.n_teams = teams; H.team_ctas = b.hand_width[s - 1]; H.cooperative = true;
+        H.queue_dev = nullptr; H.resume = 1; H.n_teams = teams; H.team_ctas = width[s - 1]; H.cooperative = true;
         H.resume_in = list; H.n_resume_in = n_list; H.idle = b.hand_dev + s;
         H.handoff_at = s < levels ? std::max(1, teams - keep[s]) : 0;
         H.susp_out = b.susp_dev + (size_t)s * (size_t)b.n_teams; H.n_susp_out = b.hand_dev + 8 + s;

@@ -393,7 +393,16 @@ def test_team_count_requests(kp):
     for ask, want in ((-5, 5), (-10 ** 6, resident), (7, 7)):
         with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", n_teams=ask) as bp:
             assert bp.n_teams == want and bp.team_ctas == 1
-            assert len(bp.run(np.arange(12), want_chains=False)) == 12
+            r1 = bp.run(np.arange(12), want_chains=False)
+            assert len(r1) == 12
+    # team_ctas = 0: the widest teams (1, 2, 4, 8 or 16 CTAs) that keep every team co-resident -- what the trial
+    # runner asks for; the plans are the same
+    for ask, want_w in ((-20, 16), (-(resident // 4), 4), (0, 1)):
+        with kp.BatchPlanner(cfg, env, model, backend="cuda-f32", n_teams=ask, team_ctas=0) as bp:
+            assert bp.team_ctas == want_w and bp.n_teams * bp.team_ctas <= resident, (bp.n_teams, bp.team_ctas)
+            rw = bp.run(np.arange(12), want_chains=False)
+            for key in ("status", "iterations", "tree_size"):
+                assert np.array_equal(rw.records[key], r1.records[key]), key
 
 
 @pytest.mark.parametrize("backend", ["cuda", "cuda-f32"])
