@@ -254,15 +254,17 @@ int kpx_batch_create(const kpx_problem *prob, int32_t precision, int32_t n_teams
  * team_ctas = 0: 1, 2, 4, 8 or 16 CTAs per team, the widest that keeps all n_teams teams co-resident -- the
  * trial runner's choice: 100 trials on a device that holds 592 CTAs plan on teams of 4) */
 int kpx_batch_info(const kpx_batch *b, int32_t *n_teams, int32_t *team_ctas);
-/* Hand-off of a batch's stragglers (default on, batches of one-CTA teams with >= 16 queries): when the query queue is
- * empty and at most (co-resident CTAs / 8) teams are still planning, kpx_batch_launch ends its first kernel and
- * continues those queries on teams of 8 CTAs in a second one, the last (co-resident / 64) of them on teams of 64 in a
- * third -- all on the caller's stream, no host synchronisation.  Results are those of the one-CTA run (a plan does
- * not depend on the team size); only device_ms of the handed-off queries is shorter.  No reference counterpart:
- * the reference plans one query per process (bench.py:106-171). */
+/* Hand-off of a batch's stragglers (default on, batches of >= 16 queries): when the query queue is empty and half of
+ * the teams have run out of work, kpx_batch_launch ends its first kernel after the current iteration of the teams still
+ * planning and continues those queries in a second one on teams of twice the width, and so on through teams of
+ * 2, 4, 8, 16, 64 and finally all co-resident CTAs -- KPX_HANDOFF_STAGES follow-up launches on the caller's stream,
+ * no host synchronisation; a stage whose queries already fit the next one passes them straight on.  Results are those
+ * of the one-CTA run (a plan does not depend on the team size); only device_ms of the handed-off queries is shorter.
+ * No reference counterpart: the reference plans one query per process (bench.py:106-171). */
+#define KPX_HANDOFF_STAGES 6
 int kpx_batch_set_handoff(kpx_batch *b, int32_t enable);
-/* queries the last kpx_batch_launch handed to teams of 8 CTAs (counts[0]) and on to teams of 64 (counts[1]);
- * synchronises the device */
+/* queries the last kpx_batch_launch handed on at the end of its first kernel (counts[0]) and of every follow-up stage
+ * (counts[1 .. KPX_HANDOFF_STAGES - 1]); synchronises the device */
 int kpx_batch_handoff_counts(kpx_batch *b, int32_t *counts);
 void kpx_batch_destroy(kpx_batch *b);
 /* seeds[Q], starts[Q,n], goals[Q,4] host arrays; chain buffers (may be NULL) sized Q*max_chain */

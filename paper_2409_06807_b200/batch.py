@@ -108,7 +108,7 @@ class BatchPlanner:
         nt, tc = C.c_int32(0), C.c_int32(0)
         _lib.check(self._lib.kpx_batch_info(self._handle, C.byref(nt), C.byref(tc)), "kpx_batch_info")
         self.n_teams, self.team_ctas = int(nt.value), int(tc.value)
-        # the last queries of a launch carry on on teams of 8, then 64 CTAs (kpx_batch_set_handoff); same results
+        # the last queries of a launch carry on on wider and wider teams (kpx_batch_set_handoff); same results
         self.handoff = bool(handoff)
         if not self.handoff:
             _lib.check(self._lib.kpx_batch_set_handoff(self._handle, 0), "kpx_batch_set_handoff")
@@ -117,10 +117,11 @@ class BatchPlanner:
         self._scene_probs = {0: (self._prob_struct, self._keep)}
 
     def handoff_counts(self) -> tuple:
-        """Queries the last launch handed to teams of 8 CTAs and on to teams of 64 (``kpx_batch_handoff_counts``)."""
-        c = (C.c_int32 * 2)()
+        """Queries the last launch handed on to wider teams at the end of its first kernel and of every follow-up stage
+        (``kpx_batch_handoff_counts``)."""
+        c = (C.c_int32 * 6)()
         _lib.check(self._lib.kpx_batch_handoff_counts(self._handle, c), "kpx_batch_handoff_counts")
-        return int(c[0]), int(c[1])
+        return tuple(int(v) for v in c)
 
     def set_scenes(self, envs: Sequence[Environment]) -> None:
         """Obstacle sets the queries of a batch can name (``run(..., scenes=idx)``): the batched form of planning in

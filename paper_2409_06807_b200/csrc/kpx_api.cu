@@ -104,7 +104,7 @@ struct Carver {
 
 }  // namespace
 
-constexpr int kHandoffLevels = 4;   // hand-off stages at most; kpx_batch::hand_width holds the ones in use
+constexpr int kHandoffLevels = KPX_HANDOFF_STAGES;   // hand-off stages at most; kpx_batch::hand_width holds the ones in use
 
 struct kpx_batch {
     kpx_problem prob;
@@ -155,7 +155,7 @@ struct kpx_batch {
     bool auto_width = false;           // kpx_batch_create(team_ctas = 0): teams as wide as the team count leaves room for
     unsigned int* hand_dev = nullptr;  // [0..7] idle teams per stage, [8..15] suspended queries per stage
     int2* susp_dev = nullptr;          // [kHandoffLevels][n_teams] (workspace, query)
-    int hand_levels = 2, hand_width[kHandoffLevels] = {8, 64, 0, 0};   // CTAs per team of the stages after the first
+    int hand_levels = 6, hand_width[kHandoffLevels] = {2, 4, 8, 16, 64, 512};   // CTAs per team of the follow-up stages (clamped to the device)
 };
 
 struct kpx_plan { kpx_batch b; };
@@ -1265,10 +1265,10 @@ int kpx_batch_set_handoff(kpx_batch* b, int32_t enable) {
 
 int kpx_batch_handoff_counts(kpx_batch* b, int32_t* counts) {
     if (!b || !counts) return fail(KPX_E_ARG, "null argument");
-    unsigned int h[2] = {0u, 0u};
+    unsigned int h[KPX_HANDOFF_STAGES];
     CU(cudaSetDevice(b->device));
     CU(cudaMemcpy(h, b->hand_dev + 8, sizeof h, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 2; ++i) counts[i] = (int32_t)h[i];
+    for (int i = 0; i < KPX_HANDOFF_STAGES; ++i) counts[i] = (int32_t)h[i];
     return KPX_OK;
 }
 
@@ -1349,14 +1349,16 @@ int kpx_batch_launch(kpx_batch* bp, double t_max, void* stream) {
     // on in the next launch on teams of 8 CTAs, the last of them on teams of 64 -- instead of one CTA each while the
     // rest of the device idles.  Results do not depend on the team size, so nothing else changes.  Everything is
     // stream-ordered: a stage that finds nothing suspended costs one empty launch.
-    int levels = 0, keep[kHandoffLevels] = {0, 0, 0, 0}, width[kHandoffLevels] = {0, 0, 0, 0};
+    int levels = 0, keep[kHandoffLevels] = {}, width[kHandoffLevels] = {};
     if (b.handoff && !b.latency && b.n_uploaded >= 16)
-        for (int i = 0; i < b.hand_levels; ++i)            // the stages wider than the teams the batch starts with
-            if (b.hand_width[i] > b.team_ctas && b.max_resident >= 2 * b.hand_width[i]) {
-                width[levels] = b.hand_width[i];
-                keep[levels] = b.max_resident / b.hand_width[i];
+        for (int i = 0; i < b.hand_levels; ++i) {          // the stages wider than the teams the batch starts with
+            const int w = std::min(b.hand_width[i], b.max_resident);
+            if (w > (levels ? width[levels - 1] : b.team_ctas)) {
+                width[levels] = w;
+                keep[levels] = b.max_resident / w;
                 ++levels;
             }
+        }
     if (levels) {
         CU(cudaMemsetAsync(b.hand_dev, 0, 64, st));
         L.idle = b.hand_dev; L.handoff_at = std::max(1, b.n_teams - keep[0]);
@@ -1372,6 +1374,7 @@ int kpx_batch_launch(kpx_batch* bp, double t_max, void* stream) {
         H.queue_dev = nullptr; H.resume = 1; H.n_teams = teams; H.team_ctas = width[s - 1]; H.cooperative = true;
         H.resume_in = list; H.n_resume_in = n_list; H.idle = b.hand_dev + s;
         H.handoff_at = s < levels ? std::max(1, teams - keep[s]) : 0;
+        H.pass_on_below = s < levels ? keep[s] : 0;
         H.susp_out = b.susp_dev + (size_t)s * (size_t)b.n_teams; H.n_susp_out = b.hand_dev + 8 + s;
         rc = launch(b, H, st);
     }

@@ -27,7 +27,7 @@ cudaError_t do_launch_plan(const PlanLaunch& L, cudaStream_t st) {
     A.max_iters = L.max_iters; A.lam_override = L.lam_override; A.t_max_s = L.t_max_s;
     A.stop_flag = L.stop_flag; A.peer_flags = L.peer_flags; A.n_peers = L.n_peers;
     A.b_chain_start = L.b_chain_start; A.b_chain_control = L.b_chain_control; A.b_chain_dt = L.b_chain_dt;
-    A.idle = L.idle; A.handoff_at = L.handoff_at; A.susp_out = L.susp_out; A.n_susp_out = L.n_susp_out;
+    A.idle = L.idle; A.handoff_at = L.handoff_at; A.pass_on_below = L.pass_on_below; A.susp_out = L.susp_out; A.n_susp_out = L.n_susp_out;
     A.resume_in = L.resume_in; A.n_resume_in = L.n_resume_in;
     auto kern = plan_kernel<M, Real, KPX_VARIANT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);

@@ -25,7 +25,7 @@ struct PlanLaunch {
     double *b_chain_start, *b_chain_control, *b_chain_dt;
     // hand-off of a batch's last queries to wider teams (PlanArgs, kpx_plan.cuh)
     unsigned int* idle;
-    int handoff_at;
+    int handoff_at, pass_on_below;
     int2* susp_out; unsigned int* n_susp_out;
     const int2* resume_in; const unsigned int* n_resume_in;
     size_t smem;

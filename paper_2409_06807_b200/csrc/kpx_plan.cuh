@@ -214,6 +214,8 @@ struct PlanArgs {
     // in susp_out.  The next launch -- teams of more CTAs, resume = 1 -- continues entry j of resume_in on team j.
     unsigned int* idle;           // may be null
     int handoff_at;               // 0: never suspend
+    int pass_on_below;            // a resumed stage handed this many queries or fewer passes them straight on (they
+                                  // already fit the next, wider stage)
     int2* susp_out; unsigned int* n_susp_out;
     const int2* resume_in; const unsigned int* n_resume_in;
 };
@@ -1387,6 +1389,10 @@ __global__ void __launch_bounds__(kBlock, MinBlocks<M, R, V>::value) plan_kernel
             return;
         }
         handed = __ldcg(A.resume_in + team_id);
+        if (A.handoff_at > 0 && __ldcg(A.n_resume_in) <= (unsigned)A.pass_on_below) {
+            if (T.rank == 0 && threadIdx.x == 0) A.susp_out[atomicAdd(A.n_susp_out, 1u)] = handed;
+            return;
+        }
     }
     T.ws_index = handed.x;
     if (threadIdx.x == 0) s_ws = A.ws[handed.x];

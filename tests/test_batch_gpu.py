@@ -407,7 +407,7 @@ def test_team_count_requests(kp):
 
 @pytest.mark.parametrize("backend", ["cuda", "cuda-f32"])
 def test_handoff_to_wider_teams_changes_nothing(kp, backend):
-    """The last queries of a launch carry on on teams of 8 CTAs, the very last on teams of 64 (kpx_batch_set_handoff):
+    """The last queries of a launch carry on on wider and wider teams (kpx_batch_set_handoff):
     every record -- status, iterations, tree size, work counters, chain -- equals the run that keeps one CTA per query
     to the end, and the hand-off really took place."""
     model = kp.get_model("di6")
@@ -416,11 +416,13 @@ def test_handoff_to_wider_teams_changes_nothing(kp, backend):
     seeds = np.arange(150)
     with kp.BatchPlanner(cfg, env, model, backend=backend, n_teams=32, handoff=False) as plain:
         a = plain.run(seeds, replan_rejected=False)
-        assert plain.handoff_counts() == (0, 0)
+        assert not any(plain.handoff_counts())
     with kp.BatchPlanner(cfg, env, model, backend=backend, n_teams=32) as bp:
         b = bp.run(seeds, replan_rejected=False)
-        first, second = bp.handoff_counts()
-    assert 1 <= first <= 31 and 1 <= second <= 9, (first, second)
+        handed = bp.handoff_counts()
+    # 32 teams: the first idle team sends the (at most 31) queries still running to wider teams; they fit teams of 16
+    # CTAs at once, so the stages in between pass them straight on, and the last ones end on still wider teams
+    assert 1 <= handed[0] <= 31 and handed[1] == handed[0] and handed[2] == handed[0] and handed[3] <= handed[2], handed
     for key in ("status", "iterations", "tree_size", "solution_slot", "chain_len", "items", "substeps", "points", "boxsteps",
                 "free_items", "checked"):
         assert np.array_equal(a.records[key], b.records[key]), key
