@@ -713,14 +713,14 @@ def run_gpu(args):
                   "median_tree_size": float(np.median(rec["tree_size"])), "host_checker_sample": f"{okc}/{checked}",
                   "host_and_device_verdicts_agree": f"{agree}/{checked}"},
         "e2e": head["e2e"],
-        # per step: plan_kernel, the two hand-off stages (a one-block kernel that clears the suspended queries' stop
-        # words + plan_kernel on teams of 8 / 64 CTAs, each), validate_kernel
-        "gpu_launches": 6 * args.steps,
+        # per step: plan_kernel, the six hand-off stages (a small kernel that clears the suspended queries' stop words
+        # + plan_kernel on teams of 2 / 4 / 8 / 16 / 64 / all CTAs, each), validate_kernel
+        "gpu_launches": 14 * args.steps,
         "roofline": {"bound": "fp32" if "f32" in args.backend else "fp64", "achieved": head["achieved_tflops"],
                      "peak": head["peak_tflops"], "unit": "TFLOP/s", "frac": head["frac"], "traffic": traffic,
                      "traffic_source": traffic_src, "hbm": hbm,
-                     "kernel": "kpx::plan_kernel (one persistent launch per step + two short follow-up launches that finish "
-                               "the last queries on teams of 8 / 64 CTAs; the validate kernel after them is < 1 % of the step)", "kernel_ms": head["kern_ms"],
+                     "kernel": "kpx::plan_kernel (one persistent launch per step + six short follow-up launches that finish "
+                               "the last queries on wider and wider teams; the validate kernel after them is < 1 % of the step)", "kernel_ms": head["kern_ms"],
                      "algorithmic_flops_per_launch": head["flops"],
                      "note": "non-tensor compute bound (no dense contraction): peak = FMA micro-benchmark measured "
                              "in this run (MEASURED_PEAKS.json holds only HBM / bf16 numbers); achieved counts "
