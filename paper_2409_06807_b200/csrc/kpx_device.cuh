@@ -325,11 +325,24 @@ template <> struct MathK<float> {
     // reduction with the magic-number round (no int<->float conversions) and the Cephes minimax polynomials
     // on [-pi/4, pi/4]; max error 9e-8 absolute (1.4 ulp), ~22 instructions for the pair versus ~50 for
     // sincosf, whose general-range reduction these arguments never need.
+#ifndef KPX_SC_REDUCE
+#define KPX_SC_REDUCE 1
+#endif
+    // whole turns off first (exact no-op inside (-pi, pi); three instructions, no branch): a diverged angle of
+    // hundreds of radians is brought back into the range the quadrant reduction is accurate for, and a non-finite one
+    // stays non-finite
+    __device__ static __forceinline__ float reduce_turns(float x) {
+        return __fmaf_rn(rintf(x * 0.15915494309189535f), -6.283185307179586f, x);
+    }
     __device__ static __forceinline__ void sc(float x, float* s, float* c) {
         // Angles are wrapped to (-pi, pi] after every substep, so only states that have already diverged (body
         // rates of hundreds of rad/s inside an RK4 stage) come here; they get the hardware approximation instead
         // of 12 inlined copies of sincosf's Payne-Hanek path in the substep loop (17 % no-instruction stalls).
+#if KPX_SC_REDUCE
+        x = reduce_turns(x);
+#else
         if (!(fabsf(x) < 512.0f)) { __sincosf(x, s, c); return; }
+#endif
         const float t = __fmaf_rn(x, 0.636619772f, 12582912.0f);
         const int q = __float_as_int(t);
         const float qf = t - 12582912.0f;
@@ -353,7 +366,21 @@ template <> struct MathK<float> {
     __device__ static __forceinline__ void sc2(float xa, float xb, float* sa, float* ca, float* sb, float* cb) {
 #if KPX_PACKED_F32
         // a diverged angle means a diverged state: both components take the hardware approximation (see sc)
+#if KPX_SC_REDUCE
+        xa = reduce_turns(xa); xb = reduce_turns(xb);
+#else
         if (!(fabsf(xa) < 512.0f) || !(fabsf(xb) < 512.0f)) { __sincosf(xa, sa, ca); __sincosf(xb, sb, cb); return; }
+#endif
+        sc2_bounded(xa, xb, sa, ca, sb, cb);
+#else
+        sc(xa, sa, ca); sc(xb, sb, cb);
+#endif
+    }
+    // the same without the large-argument path, for angles that cannot grow (the Dubins airplane's heading is wrapped
+    // after every substep and its climb angle moves by |u| dt at most): the compiler predicates that path instead of
+    // branching around it, 16 of ~45 instructions per call.  A non-finite argument still gives NaN.
+    __device__ static __forceinline__ void sc2_bounded(float xa, float xb, float* sa, float* ca, float* sb, float* cb) {
+#if KPX_PACKED_F32
         const float2 x = make_float2(xa, xb);
         const float2 t = __ffma2_rn(x, make_float2(0.636619772f, 0.636619772f), make_float2(12582912.0f, 12582912.0f));
         const float2 qf = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
@@ -811,7 +838,7 @@ struct Stepper<ModelDubins6, float> {
     static constexpr int kCarry = 9;
     __device__ static __forceinline__ void field(float v, float th, float ga, float* f) {
         float st, ct, sg, cg;
-        MathK<float>::sc2(th, ga, &st, &ct, &sg, &cg);
+        MathK<float>::sc2_bounded(th, ga, &st, &ct, &sg, &cg);
         f[0] = v * ct * cg; f[1] = v * st * cg; f[2] = v * sg;
     }
     __device__ static __forceinline__ void init(const float* x0, const float*, float* carry) {
@@ -839,7 +866,12 @@ struct Stepper<ModelDubins6, float> {
             cur[i] = t;
             carry[6 + i] = k4[i];                        // next substep's stage 1
         }
-        cur[4] = wrap_angle(cur[4]);                     // sin / cos are periodic: the carried field is unchanged
+        // sin / cos are periodic: the carried field is unchanged.  The heading moves by |u1| h per substep, so one turn
+        // back is the whole wrap unless the state has diverged (the general form handles that)
+        {
+            const float a = cur[4], b = a - copysignf(MathK<float>::TWO_PI, a);
+            cur[4] = fabsf(a) < MathK<float>::PI ? a : (fabsf(b) < MathK<float>::PI ? b : wrap_angle(a));
+        }
     }
 };
 // Stacked double integrators: the blocks do not couple, so stepping them one 6-D block at a time performs
