@@ -420,7 +420,11 @@ template <class R>
 __device__ __forceinline__ R wrap_angle(R a) {
     // float32: an angle already inside (-pi, pi) is returned as it is -- (a + pi) - pi would round it to a multiple
     // of ulp(2 pi) = 4.8e-7 after every substep, an error the float64 formula does not have
-    if constexpr (std::is_same<R, float>::value) { if (fabsf(a) < MathK<float>::PI) return a; }
+    if constexpr (std::is_same<R, float>::value) {
+        // ... and whole turns come off in three instructions (fmod's exact reduction buys nothing at float32; the result
+        // lies in [-pi, pi], the closed end only for an argument that is an exact odd multiple of pi)
+        return fabsf(a) < MathK<float>::PI ? a : MathK<float>::reduce_turns(a);
+    }
     R t = a + MathK<R>::PI;
     if (!(t >= (R)0 && t < MathK<R>::TWO_PI)) t = MathK<R>::mod(t, MathK<R>::TWO_PI);
     if (t <= (R)0) t += MathK<R>::TWO_PI;
@@ -866,12 +870,8 @@ struct Stepper<ModelDubins6, float> {
             cur[i] = t;
             carry[6 + i] = k4[i];                        // next substep's stage 1
         }
-        // sin / cos are periodic: the carried field is unchanged.  The heading moves by |u1| h per substep, so one turn
-        // back is the whole wrap unless the state has diverged (the general form handles that)
-        {
-            const float a = cur[4], b = a - copysignf(MathK<float>::TWO_PI, a);
-            cur[4] = fabsf(a) < MathK<float>::PI ? a : (fabsf(b) < MathK<float>::PI ? b : wrap_angle(a));
-        }
+        // sin / cos are periodic: the carried field is unchanged
+        cur[4] = wrap_angle(cur[4]);
     }
 };
 // Stacked double integrators: the blocks do not couple, so stepping them one 6-D block at a time performs
