@@ -19,6 +19,9 @@
 
 #include "../../include/kpx.h"
 
+#ifndef KPX_Q12_KAHAN
+#define KPX_Q12_KAHAN 1              // Kahan-compensated float32 quadcopter update (0: plain; measured knob, profiles/tuning_r02.md)
+#endif
 #ifndef KPX_DI_KAHAN
 #define KPX_DI_KAHAN 1               // Kahan-compensated float32 double-integrator step (0: plain, ~3 % faster, 10x the error)
 #endif
@@ -818,12 +821,18 @@ struct Stepper<ModelQuad12, float> {
         ModelQuad12::deriv_sc(tmp, u, sc, k);
 #pragma unroll
         for (int j = 0; j < H; ++j) {
-            const float2 c = f2(cur[2 * j], cur[2 * j + 1]), e = f2(comp[2 * j], comp[2 * j + 1]);
+            const float2 c = f2(cur[2 * j], cur[2 * j + 1]);
             const float2 s4 = __fadd2_rn(acc[j], f2(k[2 * j], k[2 * j + 1]));
-            const float2 y = __ffma2_rn(h62, s4, f2(-e.x, -e.y));
-            const float2 t = __fadd2_rn(c, y);
-            const float2 dd = __fadd2_rn(__fadd2_rn(t, f2(-c.x, -c.y)), f2(-y.x, -y.y));
-            comp[2 * j] = dd.x; comp[2 * j + 1] = dd.y;
+            float2 t;
+            if (KPX_Q12_KAHAN == 1 || (KPX_Q12_KAHAN == 2 && j < 2)) {      // 2: position (and v_x, its pair) only
+                const float2 e = f2(comp[2 * j], comp[2 * j + 1]);
+                const float2 y = __ffma2_rn(h62, s4, f2(-e.x, -e.y));
+                t = __fadd2_rn(c, y);
+                const float2 dd = __fadd2_rn(__fadd2_rn(t, f2(-c.x, -c.y)), f2(-y.x, -y.y));
+                comp[2 * j] = dd.x; comp[2 * j + 1] = dd.y;
+            } else {
+                t = __ffma2_rn(h62, s4, c);              // plain update
+            }
             cur[2 * j] = t.x; cur[2 * j + 1] = t.y;
         }
         ModelQuad12::wrap<float>(cur);
