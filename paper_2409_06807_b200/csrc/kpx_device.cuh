@@ -20,7 +20,14 @@
 #include "../../include/kpx.h"
 
 #ifndef KPX_Q12_KAHAN
-#define KPX_Q12_KAHAN 1              // Kahan-compensated float32 quadcopter update (0: plain; measured knob, profiles/tuning_r02.md)
+// Kahan-compensated float32 quadcopter update: OFF.  Measured on 1 M extensions against the float64 kernel
+// (tools/f32_err.py, profiles/tuning_r02.md): max relative end-state error 1.2e-6 with, 2.4e-6 without (tolerance 1e-5),
+// the same verdicts and cells (<= 1 flip per million either way), the same success over 1000 seeds (599 / 608; float64
+// 591) -- and 12 fewer live registers: spill loads 400 -> 208 B, quad12/narrow +9 %, config 5 +11 %.
+#define KPX_Q12_KAHAN 0
+#endif
+#ifndef KPX_DUB_KAHAN
+#define KPX_DUB_KAHAN 1              // float32 Dubins airplane: 1 = Kahan-compensated accumulation, 0 = closed-form (v, theta, gamma) + plain position update
 #endif
 #ifndef KPX_DI_KAHAN
 #define KPX_DI_KAHAN 1               // Kahan-compensated float32 double-integrator step (0: plain, ~3 % faster, 10x the error)
@@ -728,7 +735,7 @@ struct Stepper<ModelDI6, float> {
 // 2-4 ROTATE the stage-1 values -- sin(a + d) = s cos d + c sin d with short polynomials for sin d, cos d (|d| <= 1/4:
 // error < 2e-8) -- instead of three more full reductions + polynomials + quadrant fix-ups per stage: 12 full sincos per
 // substep become 3 plus 9 rotations (~11 packed / scalar operations per angle).  A larger step of an angle (only next
-// to the pitch singularity) takes the full evaluation.  Same RK4, same Kahan-compensated update as the generic path.
+// to the pitch singularity) takes the full evaluation.  Same RK4; the update is plain (KPX_Q12_KAHAN, measured) -- the generic path and the other models compensate it.
 #if KPX_PACKED_F32
 template <>
 struct Stepper<ModelQuad12, float> {
@@ -824,7 +831,7 @@ struct Stepper<ModelQuad12, float> {
             const float2 c = f2(cur[2 * j], cur[2 * j + 1]);
             const float2 s4 = __fadd2_rn(acc[j], f2(k[2 * j], k[2 * j + 1]));
             float2 t;
-            if (KPX_Q12_KAHAN == 1 || (KPX_Q12_KAHAN == 2 && j < 2)) {      // 2: position (and v_x, its pair) only
+            if (KPX_Q12_KAHAN) {
                 const float2 e = f2(comp[2 * j], comp[2 * j + 1]);
                 const float2 y = __ffma2_rn(h62, s4, f2(-e.x, -e.y));
                 t = __fadd2_rn(c, y);
@@ -857,8 +864,32 @@ struct Stepper<ModelDubins6, float> {
     __device__ static __forceinline__ void init(const float* x0, const float*, float* carry) {
 #pragma unroll
         for (int i = 0; i < 6; ++i) carry[i] = 0.0f;
+#if !KPX_DUB_KAHAN
+        carry[3] = x0[3]; carry[4] = x0[4]; carry[5] = x0[5];      // (v, theta, gamma) the extension starts from
+#endif
         field(x0[3], x0[4], x0[5], carry + 6);
     }
+#if !KPX_DUB_KAHAN
+    // Measured alternative (profiles/tuning_r02.md).  (v, theta, gamma) have constant derivatives, so RK4's update of
+    // them is exact and the state after n substeps is x0 + (n h) u: ONE rounding instead of n accumulated ones (and
+    // instead of the compensation); the position update is plain.  carry[0] = n (exact in float32).
+    __device__ static __forceinline__ void step(float* cur, float* carry, const float* u, float h, float) {
+        const float hh = 0.5f * h, h6 = h * 0.16666667f;
+        float k2[3], k4[3];
+        field(__fmaf_rn(hh, u[0], cur[3]), __fmaf_rn(hh, u[1], cur[4]), __fmaf_rn(hh, u[2], cur[5]), k2);
+        carry[0] += 1.0f;
+        const float tn = carry[0] * h;
+        cur[3] = __fmaf_rn(tn, u[0], carry[3]);
+        cur[4] = wrap_angle(__fmaf_rn(tn, u[1], carry[4]));
+        cur[5] = __fmaf_rn(tn, u[2], carry[5]);
+        field(cur[3], cur[4], cur[5], k4);               // stage 4 = the state this substep ends in
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {                    // position: Simpson weights
+            cur[i] = __fmaf_rn(h6, __fadd_rn(__fmaf_rn(4.0f, k2[i], carry[6 + i]), k4[i]), cur[i]);
+            carry[6 + i] = k4[i];                        // next substep's stage 1
+        }
+    }
+#else
     __device__ static __forceinline__ void step(float* cur, float* carry, const float* u, float h, float) {
         const float hh = 0.5f * h, h6 = h * 0.16666667f;
         float k2[3], k4[3];
@@ -882,6 +913,7 @@ struct Stepper<ModelDubins6, float> {
         // sin / cos are periodic: the carried field is unchanged
         cur[4] = wrap_angle(cur[4]);
     }
+#endif
 };
 // Stacked double integrators: the blocks do not couple, so stepping them one 6-D block at a time performs
 // exactly the same operations per dimension while keeping only a 6-D set of RK4 temporaries live

@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
-"""float32 vs float64 end states of quadcopter extensions on a large batch (the float64 kernel is pinned bit for bit
+"""float32 vs float64 end states of the extensions of a large batch (the float64 kernel is pinned bit for bit
 to the reference): max / p99.9 relative error over the items valid in both, verdict and cell agreement.
 
-    [KPX_LIB_PATH=.../libkpx_<variant>.so] python tools/q12_err.py [scene] [lam]
+    [KPX_LIB_PATH=.../libkpx_<variant>.so] python tools/f32_err.py [scene] [lam] [model]
 """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,7 +12,8 @@ from paper_2409_06807_b200.backend import PlanContext
 
 scene = sys.argv[1] if len(sys.argv) > 1 else "narrow"
 lam = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-model = kp.get_model("quad12")
+model_name = sys.argv[3] if len(sys.argv) > 3 else "quad12"
+model = kp.get_model(model_name)
 env = kp.gen_environment(scene, model, seed=0)
 cfg = kp.PlannerConfig(t_e=model.default_t_e, t_prop=model.default_t_prop, cells_per_dim=model.default_cells_per_dim, seed=3)
 prob = kp.build_problem(cfg, env, model)
@@ -35,7 +36,7 @@ for w in model.wrap_dims:
     d[:, w] = np.minimum(d[:, w], np.abs(2 * np.pi - d[:, w]))
 rel = (d / np.maximum(np.abs(r.end), 1.0))[keep]
 per_item = rel.max(axis=1)
-print(f"lib {os.environ.get('KPX_LIB_PATH', 'libkpx.so')}: quad12/{scene}, {m * lam} extensions of {m} tree nodes, "
+print(f"lib {os.environ.get('KPX_LIB_PATH', 'libkpx.so')}: {model_name}/{scene}, {m * lam} extensions of {m} tree nodes, "
       f"{int(keep.sum())} valid in both")
 print(f"  relative end-state error (float32 vs float64): max {per_item.max():.3e}  p99.9 {np.quantile(per_item, 0.999):.3e}  "
       f"median {np.median(per_item):.3e}; worst component {int(np.unravel_index(rel.argmax(), rel.shape)[1])}")
